@@ -1,0 +1,834 @@
+// api.cu — the C-ABI (include/tidal.h): handles, template server (pinned
+// pool + device template/arena), adaptive fork and the overlapped invoke.
+#include <cuda_runtime.h>
+
+#include <atomic>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <deque>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "../../include/tidal.h"
+#include "../../include/tidal_kernels.h"
+#include "plan.h"
+#include "runtime.h"
+
+using namespace tidal;
+
+namespace tidal {
+bool nccl_unique_id(void* out128);
+void* nccl_comm_create(int world, int rank, const void* id128, int device);
+void nccl_comm_destroy(void* c);
+}  // namespace tidal
+
+namespace {
+thread_local std::string g_err;
+
+tidal_status set_err(int code, const std::string& msg) {
+  g_err = msg;
+  return (tidal_status)code;
+}
+
+#define TIDAL_TRY try {
+#define TIDAL_CATCH                                         \
+  }                                                         \
+  catch (const Error& e) {                                  \
+    return set_err(e.code, e.msg);                          \
+  }                                                         \
+  catch (const std::bad_alloc&) {                           \
+    return set_err(TIDAL_ERR_OOM, "host allocation failed"); \
+  }                                                         \
+  catch (const std::exception& e) {                         \
+    return set_err(TIDAL_ERR_INVALID, e.what());            \
+  }                                                         \
+  return TIDAL_OK;
+
+void require(bool c, const std::string& msg, int code = TIDAL_ERR_INVALID) {
+  if (!c) fail(code, msg);
+}
+
+__global__ void sleep_kernel(int us) {
+  for (int i = 0; i < us; ++i) __nanosleep(1000);
+}
+}  // namespace
+
+struct tidal_model {
+  ModelShape shape;
+  float theta = 1e4f, eps = 1e-5f;
+  std::string checkpoint;
+  int world = 1, rank = 0;
+  TensorTable tt;
+  std::vector<const void*> host;  // per base tensor id
+  std::vector<int> user_index;
+  tidal_fill_fn fill = nullptr;
+  void* ctx = nullptr;
+
+  void produce(int id, void* dst) const {
+    const uint64_t b = tt.t[id].bytes;
+    if (host[id]) {
+      memcpy(dst, host[id], b);
+    } else {
+      require(fill != nullptr, "tensor " + tt.t[id].name + " has neither data nor fill callback");
+      fill(dst, b, user_index[id], ctx);
+    }
+  }
+};
+
+struct tidal_trace_rec {
+  TensorTable tt;
+  Trace tr;
+};
+
+struct tidal_comm {
+  void* nccl = nullptr;
+  int world = 1, rank = 0, device = 0;
+};
+
+struct tidal_template {
+  ModelShape shape;
+  float theta = 1e4f, eps = 1e-5f;
+  int world = 1, rank = 0;
+  TensorTable tt;
+  Trace tr;
+  TemplateChoice choice;
+  Plan plan;
+  uint64_t gen = 1;
+  bool dry = true;
+  int device = -1;
+  int max_tokens = 0;
+  uint8_t* pool = nullptr;
+  uint8_t* dev = nullptr;
+  Exec ex;
+  std::vector<cudaEvent_t> ev;
+  cudaEvent_t e_start = nullptr, e_h2d0 = nullptr, e_h2d1 = nullptr, e_c0 = nullptr, e_end = nullptr;
+  uint8_t* arena = nullptr;  // adapter arena
+  uint64_t arena_cap = 0;
+  int debug = 0, debug_arg = -1;
+  void* scrub = nullptr;
+  unsigned long long* d_sum = nullptr;
+  tidal_comm* comm = nullptr;
+  std::deque<std::string> names;
+
+  void ensure_events(size_t n) {
+    while (ev.size() < n) {
+      cudaEvent_t e;
+      cuda_check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "cudaEventCreate");
+      ev.push_back(e);
+    }
+  }
+};
+
+struct tidal_adapter {
+  tidal_template* tpl = nullptr;
+  TensorTable tt;
+  Plan plan;
+  uint64_t plan_gen = 0;
+  int rank = 0;
+  float scale = 1.f;
+  uint32_t mask = 0;
+  const uint8_t* host = nullptr;
+  uint64_t bytes = 0;
+};
+
+static ModelShape shape_of(const tidal_model_config* c) {
+  ModelShape m;
+  m.n_layers = c->n_layers;
+  m.d_model = c->d_model;
+  m.n_heads = c->n_heads;
+  m.n_kv_heads = c->n_kv_heads;
+  m.d_ff = c->d_ff;
+  m.vocab = c->vocab;
+  m.tie = c->tie_embeddings != 0;
+  return m;
+}
+
+static std::string dump_copy(const std::string& s, char* buf, size_t cap, size_t* needed) {
+  if (needed) *needed = s.size() + 1;
+  if (buf && cap >= s.size() + 1) memcpy(buf, s.c_str(), s.size() + 1);
+  else if (buf && cap) fail(TIDAL_ERR_BUFSZ, "buffer too small");
+  return s;
+}
+
+extern "C" {
+
+const char* tidal_last_error(void) { return g_err.c_str(); }
+const char* tidal_version(void) { return "tidal-b200 0.1 (sm_100a)"; }
+
+tidal_status tidal_model_create(const tidal_model_config* cfg, const tidal_host_tensor* w, int n,
+                                const char* checkpoint, tidal_fill_fn fill, void* fill_ctx,
+                                int world, int rank, tidal_model** out) {
+  TIDAL_TRY
+  require(cfg && w && out && n > 0, "null argument");
+  require(world >= 1 && rank >= 0 && rank < world, "bad world/rank");
+  ModelShape m = shape_of(cfg);
+  require(m.n_layers >= 0 && m.d_model > 0 && m.n_heads > 0 && m.n_kv_heads > 0 && m.d_ff > 0 &&
+              m.vocab > 0,
+          "bad model config");
+  require(m.d_model % m.n_heads == 0 && m.n_heads % m.n_kv_heads == 0, "bad head config");
+  const int hd = m.head_dim();
+  require(hd == 64 || hd == 128, "head_dim must be 64 or 128");
+  require(m.d_model % 64 == 0 && m.d_ff % 8 == 0, "d_model % 64, d_ff % 8 required");
+  require(m.n_kv_heads % world == 0 && m.d_ff % world == 0 && m.vocab % world == 0,
+          "model does not shard evenly over world");
+  require((m.d_ff / world) % 8 == 0, "d_ff/world must be a multiple of 8");
+  auto* mo = new tidal_model();
+  mo->shape = m;
+  mo->theta = cfg->rope_theta;
+  mo->eps = cfg->rms_eps;
+  mo->checkpoint = checkpoint ? checkpoint : "base";
+  mo->world = world;
+  mo->rank = rank;
+  mo->fill = fill;
+  mo->ctx = fill_ctx;
+  build_base(mo->tt, m, world, rank, mo->checkpoint);
+  mo->host.assign(mo->tt.n_base, nullptr);
+  mo->user_index.assign(mo->tt.n_base, -1);
+  for (int i = 0; i < n; ++i) {
+    require(w[i].name != nullptr, "tensor without a name");
+    const int id = mo->tt.find(w[i].name);
+    if (id < 0 || id >= mo->tt.n_base) {
+      delete mo;
+      fail(TIDAL_ERR_STRUCTURE, std::string("unexpected tensor ") + w[i].name);
+    }
+    if (mo->user_index[id] >= 0 || w[i].bytes != mo->tt.t[id].bytes) {
+      const std::string nm = w[i].name;
+      delete mo;
+      fail(TIDAL_ERR_STRUCTURE, "duplicate or mis-sized tensor " + nm);
+    }
+    mo->user_index[id] = i;
+    mo->host[id] = w[i].host_bf16;
+    if (!w[i].host_bf16 && !fill) {
+      delete mo;
+      fail(TIDAL_ERR_INVALID, "tensor without data and no fill callback");
+    }
+  }
+  for (int id = 0; id < mo->tt.n_base; ++id)
+    if (mo->user_index[id] < 0) {
+      const std::string nm = mo->tt.t[id].name;
+      delete mo;
+      fail(TIDAL_ERR_STRUCTURE, "missing tensor " + nm);
+    }
+  *out = mo;
+  TIDAL_CATCH
+}
+
+void tidal_model_destroy(tidal_model* m) { delete m; }
+
+tidal_status tidal_trace(tidal_model* m, const int32_t* host_tokens, int n_tokens, int device,
+                         float* host_logits_out, int32_t* host_token_out, double* cold_ttft_ms_out,
+                         tidal_trace_rec** out) {
+  TIDAL_TRY
+  require(m && out, "null argument");
+  auto* tr = new tidal_trace_rec();
+  tr->tt = m->tt;
+  tr->tr = make_trace(m->tt);
+  if (device < 0) {
+    *out = tr;
+    return TIDAL_OK;
+  }
+  require(host_tokens && n_tokens >= 1, "tokens required for a traced first run");
+  for (int i = 0; i < n_tokens; ++i)
+    require(host_tokens[i] >= 0 && host_tokens[i] < m->shape.vocab, "token out of range");
+  // First run: every weight copied in registration order, then the forward
+  // with a Recorder capturing which weights each launched op reads.
+  const auto t0 = std::chrono::steady_clock::now();
+  Exec ex;
+  uint8_t* dbuf = nullptr;
+  uint8_t* stage = nullptr;
+  try {
+    ex.init(device, m->shape, m->eps, m->theta, m->world, m->rank, n_tokens);
+    std::vector<uint64_t> off(m->tt.n_base);
+    uint64_t cur = 0, maxb = 0;
+    for (int id = 0; id < m->tt.n_base; ++id) {
+      cur = (cur + kAlign - 1) / kAlign * kAlign;
+      off[id] = cur;
+      cur += m->tt.t[id].bytes;
+      maxb = std::max(maxb, m->tt.t[id].bytes);
+    }
+    cuda_check(cudaMalloc(&dbuf, cur), "cudaMalloc(trace weights)");
+    cuda_check(cudaHostAlloc(&stage, maxb, cudaHostAllocDefault), "cudaHostAlloc(stage)");
+    ex.wptr.assign(m->tt.t.size(), nullptr);
+    for (int id = 0; id < m->tt.n_base; ++id) {
+      m->produce(id, stage);
+      cuda_check(cudaMemcpy(dbuf + off[id], stage, m->tt.t[id].bytes, cudaMemcpyHostToDevice),
+                 "H2D (first run)");
+      ex.wptr[id] = dbuf + off[id];
+    }
+    memcpy(ex.h_tok, host_tokens, sizeof(int32_t) * n_tokens);
+    cuda_check(cudaMemcpyAsync(ex.tok, ex.h_tok, 4 * n_tokens, cudaMemcpyHostToDevice, ex.compute),
+               "H2D tokens");
+    Recorder rec;
+    rec.seen.assign(m->tt.t.size(), 0);
+    RunArgs a;
+    a.tt = &m->tt;
+    a.ops = &tr->tr.ops;
+    a.S = n_tokens;
+    a.rec = &rec;
+    a.akey = nullptr;
+    run_forward(ex, a);
+    cuda_check(cudaMemcpyAsync(ex.h_key, ex.key, 8, cudaMemcpyDeviceToHost, ex.compute), "D2H");
+    if (host_logits_out)
+      cuda_check(cudaMemcpyAsync(ex.h_logits, ex.logits, 4ull * m->shape.vocab,
+                                 cudaMemcpyDeviceToHost, ex.compute),
+                 "D2H");
+    cuda_check(cudaStreamSynchronize(ex.compute), "first run");
+    const auto t1 = std::chrono::steady_clock::now();
+    if (cold_ttft_ms_out) *cold_ttft_ms_out = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    if (host_logits_out) memcpy(host_logits_out, ex.h_logits, 4ull * m->shape.vocab);
+    if (host_token_out) *host_token_out = (int32_t)(0xFFFFFFFFu - (uint32_t)(*ex.h_key & 0xFFFFFFFFu));
+    // the recorded order must be the planner's trace (never-read weights at the tail)
+    std::vector<char> seen(m->tt.n_base, 0);
+    for (auto& p : rec.access) seen[p.first] = 1;
+    for (int id = 0; id < m->tt.n_base; ++id)
+      if (!seen[id]) rec.access.emplace_back(id, -1);
+    if (rec.access != tr->tr.access) fail(TIDAL_ERR_INVALID, "recorded access order != planner order");
+  } catch (...) {
+    if (dbuf) cudaFree(dbuf);
+    if (stage) cudaFreeHost(stage);
+    ex.destroy();
+    delete tr;
+    throw;
+  }
+  cudaFree(dbuf);
+  cudaFreeHost(stage);
+  ex.destroy();
+  *out = tr;
+  TIDAL_CATCH
+}
+
+void tidal_trace_destroy(tidal_trace_rec* t) { delete t; }
+
+tidal_status tidal_trace_dump(const tidal_trace_rec* t, char* buf, size_t cap, size_t* needed) {
+  TIDAL_TRY
+  require(t != nullptr, "null trace");
+  dump_copy(trace_dump(t->tt, t->tr), buf, cap, needed);
+  TIDAL_CATCH
+}
+
+static TemplateChoice choice_of(const tidal_template_opts* o) {
+  TemplateChoice c;
+  c.resident_bytes = o->resident_bytes;
+  c.eq1 = o->eq1 != 0;
+  c.t_ttft_s = o->t_ttft_s;
+  c.b_pcie_Bps = o->b_pcie_Bps;
+  c.group_policy = o->group_policy;
+  c.max_transfers = o->max_transfers > 0 ? o->max_transfers : 300;
+  return c;
+}
+
+static void warm_kernels(tidal_template* tp) {
+  // A8 proactive code loading: one warm run of every kernel on dummy inputs
+  // (reduced dimensions), so no invocation pays a lazy module load.
+  Exec& ex = tp->ex;
+  const int S = std::min(tp->max_tokens, 16);
+  std::vector<int32_t> tok(S, 0);
+  memcpy(ex.h_tok, tok.data(), 4 * S);
+  cuda_check(cudaMemcpyAsync(ex.tok, ex.h_tok, 4 * S, cudaMemcpyHostToDevice, ex.compute), "H2D");
+  ex.wptr.assign(tp->tt.t.size(), nullptr);
+  for (int id = 0; id < tp->tt.n_base; ++id) ex.wptr[id] = tp->dev + tp->plan.offset[id];
+  RunArgs a;
+  a.tt = &tp->tt;
+  a.ops = &tp->plan.ops;
+  a.S = S;
+  a.akey = nullptr;
+  a.gen = tp->gen;
+  a.nccl = tp->comm ? tp->comm->nccl : nullptr;
+  run_forward(ex, a);
+  const bf16* A[1] = {ex.Xn};
+  bf16* T[1] = {ex.T[0]};
+  for (int r : {8, 16, 32, 64})
+    cuda_check(lora_shrink_launch(ex.Xn, 64, 1, 64, A, T, 1, r, 1.f, ex.compute), "warm shrink");
+  cuda_check(cudaStreamSynchronize(ex.compute), "warm run");
+  ex.cache.clear();
+}
+
+tidal_status tidal_template_create(tidal_model* m, const tidal_trace_rec* t,
+                                   const tidal_template_opts* opts, tidal_template** out) {
+  TIDAL_TRY
+  require(m && t && opts && out, "null argument");
+  require(t->tt.n_base == m->tt.n_base, "trace is from a different model", TIDAL_ERR_STRUCTURE);
+  auto* tp = new tidal_template();
+  tp->shape = m->shape;
+  tp->theta = m->theta;
+  tp->eps = m->eps;
+  tp->world = m->world;
+  tp->rank = m->rank;
+  tp->tt = m->tt;
+  tp->tr = t->tr;
+  tp->choice = choice_of(opts);
+  tp->plan = make_plan(tp->tt, tp->tr, tp->choice);
+  tp->device = opts->device;
+  tp->dry = opts->device < 0;
+  tp->max_tokens = opts->max_tokens > 0 ? opts->max_tokens : 2048;
+  tp->comm = opts->comm;
+  if (tp->dry) {
+    *out = tp;
+    return TIDAL_OK;
+  }
+  try {
+    require(m->world == 1 || (opts->comm && opts->comm->world == m->world && opts->comm->rank == m->rank),
+            "tensor-parallel model needs a matching communicator");
+    tp->ex.init(tp->device, tp->shape, tp->eps, tp->theta, tp->world, tp->rank, tp->max_tokens);
+    const uint64_t L = tp->plan.layout_bytes;
+    {
+      // pinned pool, NUMA-local to the device, whole image in layout order
+      NumaGuard numa(tp->device);
+      cuda_check(cudaHostAlloc((void**)&tp->pool, L, cudaHostAllocDefault), "cudaHostAlloc(pool)");
+      uint64_t prev_end = 0;
+      for (int id : tp->plan.layout) {
+        const uint64_t o = tp->plan.offset[id];
+        if (o > prev_end) memset(tp->pool + prev_end, 0, o - prev_end);
+        m->produce(id, tp->pool + o);
+        prev_end = o + tp->tt.t[id].bytes;
+      }
+    }
+    cuda_check(cudaMalloc((void**)&tp->dev, L), "cudaMalloc(template+arena)");
+    if (tp->plan.resident_end)
+      cuda_check(cudaMemcpy(tp->dev, tp->pool, tp->plan.resident_end, cudaMemcpyHostToDevice),
+                 "H2D resident prefix");
+    for (cudaEvent_t* e : {&tp->e_start, &tp->e_h2d0, &tp->e_h2d1, &tp->e_c0, &tp->e_end})
+      cuda_check(cudaEventCreate(e), "cudaEventCreate");
+    tp->ensure_events(tp->plan.groups.size() + 2 * tp->shape.n_layers + 4);
+    cuda_check(cudaMalloc((void**)&tp->d_sum, 64), "cudaMalloc");
+    // warm run streams nothing: make every weight valid once (prefix resident,
+    // suffix copied) so the warm launches read real bytes
+    if (tp->plan.resident_end < L)
+      cuda_check(cudaMemcpy(tp->dev + tp->plan.resident_end, tp->pool + tp->plan.resident_end,
+                            L - tp->plan.resident_end, cudaMemcpyHostToDevice),
+                 "H2D warm");
+    warm_kernels(tp);
+  } catch (...) {
+    tidal_template_destroy(tp);
+    throw;
+  }
+  *out = tp;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_template_resize(tidal_template* tp, const tidal_template_opts* opts) {
+  TIDAL_TRY
+  require(tp && opts, "null argument");
+  TemplateChoice c = tp->choice;
+  c.resident_bytes = opts->resident_bytes;
+  c.eq1 = opts->eq1 != 0;
+  c.t_ttft_s = opts->t_ttft_s;
+  c.b_pcie_Bps = opts->b_pcie_Bps;
+  const uint64_t old_end = tp->plan.resident_end;
+  Plan p = make_plan(tp->tt, tp->tr, c);
+  if (!tp->dry) {
+    cuda_check(cudaSetDevice(tp->device), "cudaSetDevice");
+    cuda_check(cudaDeviceSynchronize(), "sync");
+    if (p.resident_end > old_end)
+      cuda_check(cudaMemcpy(tp->dev + old_end, tp->pool + old_end, p.resident_end - old_end,
+                            cudaMemcpyHostToDevice),
+                 "H2D grow template");
+    tp->ensure_events(p.groups.size() + 2 * tp->shape.n_layers + 4);
+  }
+  tp->choice = c;
+  tp->plan = std::move(p);
+  ++tp->gen;
+  TIDAL_CATCH
+}
+
+void tidal_template_destroy(tidal_template* tp) {
+  if (!tp) return;
+  if (!tp->dry && tp->device >= 0) {
+    cudaSetDevice(tp->device);
+    cudaDeviceSynchronize();
+    for (cudaEvent_t e : tp->ev) cudaEventDestroy(e);
+    for (cudaEvent_t e : {tp->e_start, tp->e_h2d0, tp->e_h2d1, tp->e_c0, tp->e_end})
+      if (e) cudaEventDestroy(e);
+    if (tp->dev) cudaFree(tp->dev);
+    if (tp->arena) cudaFree(tp->arena);
+    if (tp->scrub) cudaFree(tp->scrub);
+    if (tp->d_sum) cudaFree(tp->d_sum);
+    if (tp->pool) cudaFreeHost(tp->pool);
+    tp->ex.destroy();
+  }
+  delete tp;
+}
+
+static void adapter_table(const tidal_template* tp, int rank, uint32_t mask, TensorTable& tt,
+                          const std::string& ckpt) {
+  require(rank == 8 || rank == 16 || rank == 32 || rank == 64, "LoRA rank must be 8, 16, 32 or 64");
+  require(mask != 0 && (mask & ~0x7Fu) == 0, "target_mask must be a non-empty subset of 0x7F");
+  require(((mask >> T_GATE) & 1u) == ((mask >> T_UP) & 1u),
+          "gate and up must be targeted together (paired tiles)");
+  tt = tp->tt;
+  add_adapter(tt, rank, mask, ckpt);
+}
+
+tidal_status tidal_adapter_layout(const tidal_template* tp, int rank, uint32_t mask,
+                                  tidal_slot* slots, int cap, int* n, uint64_t* total) {
+  TIDAL_TRY
+  require(tp != nullptr, "null template");
+  TensorTable tt;
+  adapter_table(tp, rank, mask, tt, "adapter");
+  std::vector<int> ids;
+  std::vector<uint64_t> offs;
+  uint64_t tot = 0;
+  adapter_layout(tt, ids, offs, tot);
+  if (n) *n = (int)ids.size();
+  if (total) *total = tot;
+  auto* mtp = const_cast<tidal_template*>(tp);
+  for (int i = 0; i < (int)ids.size() && i < cap && slots; ++i) {
+    mtp->names.push_back(tt.t[ids[i]].name);
+    slots[i].name = mtp->names.back().c_str();
+    slots[i].offset = offs[i];
+    slots[i].bytes = tt.t[ids[i]].bytes;
+    slots[i].rows = tt.t[ids[i]].rows;
+    slots[i].cols = tt.t[ids[i]].cols;
+  }
+  TIDAL_CATCH
+}
+
+tidal_status tidal_attach_lora(tidal_template* tp, const tidal_lora_desc* d, tidal_adapter** out) {
+  TIDAL_TRY
+  require(tp && d && out, "null argument");
+  auto* a = new tidal_adapter();
+  try {
+    adapter_table(tp, d->rank, d->target_mask, a->tt, d->checkpoint ? d->checkpoint : "adapter");
+    a->plan = make_plan(a->tt, tp->tr, tp->choice);
+    a->plan_gen = tp->gen;
+    require(d->bytes == a->plan.adapter_bytes,
+            "adapter buffer is " + std::to_string(d->bytes) + " B, layout needs " +
+                std::to_string(a->plan.adapter_bytes),
+            TIDAL_ERR_STRUCTURE);
+    require(d->host_pinned != nullptr || tp->dry, "adapter needs a pinned host buffer");
+  } catch (...) {
+    delete a;
+    throw;
+  }
+  a->tpl = tp;
+  a->rank = d->rank;
+  a->scale = d->scale;
+  a->mask = d->target_mask;
+  a->host = reinterpret_cast<const uint8_t*>(d->host_pinned);
+  a->bytes = d->bytes;
+  *out = a;
+  TIDAL_CATCH
+}
+
+void tidal_adapter_destroy(tidal_adapter* a) { delete a; }
+
+tidal_status tidal_plan_dump(const tidal_template* tp, const tidal_adapter* a, char* buf, size_t cap,
+                             size_t* needed) {
+  TIDAL_TRY
+  require(tp != nullptr, "null template");
+  if (a) {
+    require(a->tpl == tp, "adapter attached to another template");
+    if (a->plan_gen != tp->gen) {
+      auto* ma = const_cast<tidal_adapter*>(a);
+      ma->plan = make_plan(ma->tt, tp->tr, tp->choice);
+      ma->plan_gen = tp->gen;
+    }
+    dump_copy(plan_dump(a->tt, a->plan), buf, cap, needed);
+  } else {
+    dump_copy(plan_dump(tp->tt, tp->plan), buf, cap, needed);
+  }
+  TIDAL_CATCH
+}
+
+tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
+                                  const int32_t* host_tokens, int n_tokens, float* host_logits_out,
+                                  int32_t* host_token_out, tidal_stats* stats) {
+  TIDAL_TRY
+  const auto t_entry = std::chrono::steady_clock::now();
+  require(tp && host_tokens && host_token_out, "null argument");
+  require(!tp->dry, "dry template cannot be invoked");
+  require(n_tokens >= 1 && n_tokens <= tp->max_tokens, "n_tokens out of range");
+  const int V = tp->shape.vocab;
+  for (int i = 0; i < n_tokens; ++i)
+    require(host_tokens[i] >= 0 && host_tokens[i] < V, "token out of range");
+  auto* a = const_cast<tidal_adapter*>(ca);
+  if (a) {
+    require(a->tpl == tp, "adapter attached to another template");
+    if (a->plan_gen != tp->gen) {
+      a->plan = make_plan(a->tt, tp->tr, tp->choice);
+      a->plan_gen = tp->gen;
+    }
+  }
+  const Plan& P = a ? a->plan : tp->plan;
+  const TensorTable& tt = a ? a->tt : tp->tt;
+  Exec& ex = tp->ex;
+  cuda_check(cudaSetDevice(tp->device), "cudaSetDevice");
+  if (a && P.adapter_bytes > tp->arena_cap) {
+    if (tp->arena) cuda_check(cudaFree(tp->arena), "cudaFree");
+    tp->arena = nullptr;
+    cuda_check(cudaMalloc((void**)&tp->arena, P.adapter_bytes), "cudaMalloc(adapter arena)");
+    tp->arena_cap = P.adapter_bytes;
+  }
+  tp->ensure_events(P.groups.size());
+  // adaptive fork: pointer table (resident -> template, streamed -> arena
+  // suffix of the same layout buffer, adapter -> adapter arena)
+  ex.wptr.assign(tt.t.size(), nullptr);
+  for (int id = 0; id < tt.n_base; ++id) ex.wptr[id] = tp->dev + P.offset[id];
+  for (int id : P.adapter_layout) ex.wptr[id] = tp->arena + P.offset[id];
+  // debug preparation (outside the measured window)
+  if (tp->debug & TIDAL_DEBUG_POISON) {
+    cuda_check(poison_launch(tp->dev + P.resident_end, P.layout_bytes - P.resident_end, ex.compute),
+               "poison");
+    if (a) cuda_check(poison_launch(tp->arena, P.adapter_bytes, ex.compute), "poison");
+  }
+  if (tp->debug & TIDAL_DEBUG_SCRUB_L2) {
+    if (!tp->scrub) cuda_check(cudaMalloc(&tp->scrub, 512ull << 20), "cudaMalloc(scrub)");
+    cuda_check(scrub_launch(tp->scrub, 512ull << 20, ex.compute), "scrub");
+  }
+  if (tp->debug & (TIDAL_DEBUG_POISON | TIDAL_DEBUG_SCRUB_L2))
+    cuda_check(cudaStreamSynchronize(ex.compute), "debug prep");
+  const auto t0 = (tp->debug & (TIDAL_DEBUG_POISON | TIDAL_DEBUG_SCRUB_L2))
+                      ? std::chrono::steady_clock::now()
+                      : t_entry;
+  ex.launches = 0;
+  memcpy(ex.h_tok, host_tokens, 4ull * n_tokens);
+  cuda_check(cudaEventRecord(tp->e_start, ex.compute), "event");
+  cuda_check(cudaStreamWaitEvent(ex.copy, tp->e_start, 0), "wait");
+  // ---- copy stream: groups in traced access order, one event each ----
+  cuda_check(cudaEventRecord(tp->e_h2d0, ex.copy), "event");
+  const int skip = (tp->debug & TIDAL_DEBUG_SKIP_BARRIER) ? tp->debug_arg : -1;
+  for (size_t g = 0; g < P.groups.size(); ++g) {
+    const Group& G = P.groups[g];
+    const uint8_t* src = G.adapter ? a->host + G.offset : tp->pool + G.offset;
+    uint8_t* dst = G.adapter ? tp->arena + G.offset : tp->dev + G.offset;
+    if ((int)g == skip) {
+      sleep_kernel<<<1, 1, 0, ex.copy>>>(20000);  // fault injection: late group
+      cuda_check(cudaGetLastError(), "sleep");
+    }
+    cuda_check(cudaMemcpyAsync(dst, src, G.bytes, cudaMemcpyHostToDevice, ex.copy), "H2D group");
+    cuda_check(cudaEventRecord(tp->ev[g], ex.copy), "event");
+  }
+  cuda_check(cudaEventRecord(tp->e_h2d1, ex.copy), "event");
+  // ---- compute stream ----
+  cuda_check(cudaMemcpyAsync(ex.tok, ex.h_tok, 4ull * n_tokens, cudaMemcpyHostToDevice, ex.compute),
+             "H2D tokens");
+  if (tp->debug & 8) cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_h2d1, 0), "serial");
+  cuda_check(cudaEventRecord(tp->e_c0, ex.compute), "event");
+  RunArgs ra;
+  ra.tt = &tt;
+  ra.ops = &P.ops;
+  ra.barriers = &P.barriers;
+  ra.events = &tp->ev;
+  ra.skip_group = skip;
+  ra.S = n_tokens;
+  ra.lora_scale = a ? a->scale : 1.f;
+  ra.akey = a ? (const void*)tp->arena : nullptr;
+  ra.gen = tp->gen;
+  ra.nccl = tp->comm ? tp->comm->nccl : nullptr;
+  run_forward(ex, ra);
+  cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_h2d1, 0), "wait copies");
+  cuda_check(cudaMemcpyAsync(ex.h_key, ex.key, 8, cudaMemcpyDeviceToHost, ex.compute), "D2H key");
+  if (host_logits_out)
+    cuda_check(cudaMemcpyAsync(ex.h_logits, ex.logits, 4ull * V, cudaMemcpyDeviceToHost, ex.compute),
+               "D2H logits");
+  cuda_check(cudaEventRecord(tp->e_end, ex.compute), "event");
+  cuda_check(cudaEventSynchronize(tp->e_end), "invoke");
+  const unsigned long long key = *ex.h_key;
+  const uint32_t hi = (uint32_t)(key >> 32);
+  const uint32_t bits = (hi & 0x80000000u) ? (hi & 0x7FFFFFFFu) : ~hi;
+  float best;
+  memcpy(&best, &bits, 4);
+  *host_token_out = (int32_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu));
+  if (host_logits_out) memcpy(host_logits_out, ex.h_logits, 4ull * V);
+  const auto t1 = std::chrono::steady_clock::now();
+  if (stats) {
+    memset(stats, 0, sizeof *stats);
+    stats->ttft_host_ms = std::chrono::duration<double, std::milli>(t1 - t0).count();
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tp->e_start, tp->e_end);
+    stats->device_ms = ms;
+    cudaEventElapsedTime(&ms, tp->e_start, tp->e_h2d0);
+    stats->h2d_first_ms = ms;
+    cudaEventElapsedTime(&ms, tp->e_start, tp->e_h2d1);
+    stats->h2d_last_ms = ms;
+    cudaEventElapsedTime(&ms, tp->e_start, tp->e_c0);
+    stats->compute_first_ms = ms;
+    stats->compute_last_ms = stats->device_ms;
+    stats->bytes_streamed = P.stream_bytes;
+    stats->bytes_resident = P.resident_bytes;
+    stats->bytes_adapter = P.adapter_payload;
+    stats->n_copies = (int)P.groups.size();
+    stats->n_kernels = ex.launches;
+  }
+  if (key == 0 || std::isnan(best)) fail(TIDAL_ERR_NUMERIC, "NaN in logits (argmax undefined)");
+  TIDAL_CATCH
+}
+
+tidal_status tidal_host_alloc(uint64_t bytes, void** out) {
+  TIDAL_TRY
+  require(out != nullptr, "null argument");
+  cuda_check(cudaHostAlloc(out, bytes ? bytes : 16, cudaHostAllocPortable), "cudaHostAlloc");
+  TIDAL_CATCH
+}
+
+void tidal_host_free(void* p) {
+  if (p) cudaFreeHost(p);
+}
+
+tidal_status tidal_comm_unique_id(void* out128) {
+  TIDAL_TRY
+  require(out128 != nullptr, "null argument");
+  nccl_unique_id(out128);
+  TIDAL_CATCH
+}
+
+tidal_status tidal_comm_create(int world, int rank, const void* id, int device, tidal_comm** out) {
+  TIDAL_TRY
+  require(out && id && world >= 1 && rank >= 0 && rank < world, "bad argument");
+  auto* c = new tidal_comm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  if (world > 1) {
+    try {
+      c->nccl = nccl_comm_create(world, rank, id, device);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+  }
+  *out = c;
+  TIDAL_CATCH
+}
+
+void tidal_comm_destroy(tidal_comm* c) {
+  if (!c) return;
+  nccl_comm_destroy(c->nccl);
+  delete c;
+}
+
+tidal_status tidal_set_debug(tidal_template* tp, int flags, int arg) {
+  TIDAL_TRY
+  require(tp != nullptr, "null template");
+  tp->debug = flags;
+  tp->debug_arg = arg;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_template_checksum(tidal_template* tp, uint64_t* out) {
+  TIDAL_TRY
+  require(tp && out && !tp->dry, "bad argument");
+  cuda_check(cudaSetDevice(tp->device), "cudaSetDevice");
+  cuda_check(checksum_launch(tp->dev, tp->plan.resident_end, tp->d_sum, tp->ex.compute), "checksum");
+  unsigned long long h = 0;
+  cuda_check(cudaMemcpyAsync(&h, tp->d_sum, 8, cudaMemcpyDeviceToHost, tp->ex.compute), "D2H");
+  cuda_check(cudaStreamSynchronize(tp->ex.compute), "checksum");
+  *out = h;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_weight_ptr(const tidal_template* tp, const char* name, void** dev_out) {
+  TIDAL_TRY
+  require(tp && name && dev_out && !tp->dry, "bad argument");
+  const int id = tp->tt.find(name);
+  require(id >= 0 && id < tp->tt.n_base, std::string("unknown weight ") + name);
+  *dev_out = tp->dev + tp->plan.offset[id];
+  TIDAL_CATCH
+}
+
+// ---------------- kernel-level entry points (include/tidal_kernels.h) ----------------
+static int g_sms = 0;
+static int sms() {
+  if (!g_sms) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&g_sms, cudaDevAttrMultiProcessorCount, dev);
+  }
+  return g_sms;
+}
+
+static tidal_status sync_status(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) return set_err(TIDAL_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+  return TIDAL_OK;
+}
+
+tidal_status tidal_k_rmsnorm(const float* X, const void* g, void* Y, int S, int d, float eps) {
+  return sync_status(rmsnorm_launch(X, (const bf16*)g, (bf16*)Y, S, d, eps, 0), "rmsnorm");
+}
+
+tidal_status tidal_k_embed(const int32_t* tok, const void* E, float* X, int S, int d, int row0,
+                           int rows) {
+  return sync_status(embed_launch(tok, (const bf16*)E, X, S, d, row0, rows, 0), "embed");
+}
+
+tidal_status tidal_k_lora_shrink(const void* X, int M, int K, const void* A, void* T, int r,
+                                 float scale) {
+  const bf16* As[1] = {(const bf16*)A};
+  bf16* Ts[1] = {(bf16*)T};
+  return sync_status(lora_shrink_launch((const bf16*)X, K, M, K, As, Ts, 1, r, scale, 0), "shrink");
+}
+
+tidal_status tidal_k_attention(const void* qkv, void* O, int S, int H, int KV, int hd) {
+  return sync_status(attention_launch((const bf16*)qkv, (bf16*)O, S, H, KV, hd, 0), "attention");
+}
+
+tidal_status tidal_k_head(const float* xlast, const void* g, const void* W, int V, int d, float eps,
+                          float* logits, unsigned long long* key) {
+  cudaError_t e = cudaMemset(key, 0, 8);
+  if (e == cudaSuccess)
+    e = head_launch(xlast, (const bf16*)g, (const bf16*)W, V, d, eps, logits, key, 0, sms(), 0);
+  return sync_status(e, "head");
+}
+
+tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const int* seg_n, int nseg,
+                          void* out, int ldo, int M, int K, const void* const* T,
+                          const void* const* B, int r, const void* rope, int head_dim) {
+  TIDAL_TRY
+  require(epi >= 0 && epi <= 3 && nseg >= 1 && nseg <= 3, "bad gemm arguments");
+  GemmParams p;
+  memset(&p, 0, sizeof p);
+  auto mk = [&](CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box) {
+    require(make_tmap(m, base, rows, cols, cols * 2, box, 64), "tensor map encode failed");
+  };
+  mk(&p.a, A, M, K, 128);
+  const int mt = (M + GEMM_BM - 1) / GEMM_BM;
+  p.M = M;
+  p.K = K;
+  p.m_tiles = mt;
+  p.out = out;
+  p.ldo = ldo;
+  p.rope = (const float2*)rope;
+  p.head_dim = head_dim;
+  p.lora_r = (T && B) ? r : 0;
+  if (epi == EPI_SILU) {
+    mk(&p.b[0], W[0], seg_n[0], K, 128);
+    mk(&p.b[1], W[1], seg_n[0], K, 128);
+    if (p.lora_r) {
+      mk(&p.ta[0], T[0], M, r, 128);
+      mk(&p.ta[1], T[1], M, r, 128);
+      mk(&p.tb[0], B[0], seg_n[0], r, 128);
+      mk(&p.tb[1], B[1], seg_n[0], r, 128);
+    }
+    p.nseg = 1;
+    p.seg[0].n = seg_n[0];
+    p.seg[0].lora = p.lora_r > 0;
+    p.n_tiles[0] = (seg_n[0] + 127) / 128;
+    p.total_tiles = p.n_tiles[0] * mt;
+  } else {
+    int col = 0;
+    p.nseg = nseg;
+    for (int s = 0; s < nseg; ++s) {
+      mk(&p.b[s], W[s], seg_n[s], K, 256);
+      p.seg[s].n = seg_n[s];
+      p.seg[s].out_col = col;
+      p.seg[s].rope = (epi == EPI_ROPE) && s < 2;
+      p.seg[s].lora = p.lora_r > 0 && T[s] && B[s];
+      if (p.seg[s].lora) {
+        mk(&p.ta[s], T[s], M, r, 128);
+        mk(&p.tb[s], B[s], seg_n[s], r, 256);
+      }
+      col += seg_n[s];
+      p.n_tiles[s] = (seg_n[s] + GEMM_BN - 1) / GEMM_BN;
+      p.total_tiles += p.n_tiles[s] * mt;
+    }
+  }
+  cudaError_t e = gemm_launch(p, epi, sms(), 0);
+  tidal_status s = sync_status(e, "gemm");
+  if (s != TIDAL_OK) return s;
+  TIDAL_CATCH
+}
+
+}  // extern "C"

@@ -1,0 +1,415 @@
+// gemm_tc.cu — the dense contractions of the prefill (QKV, O, gate/up, down)
+// on 5th-gen tensor cores: tcgen05.mma with TMEM accumulators, operands staged
+// by TMA (SWIZZLE_128B) through a 4-stage mbarrier ring, warp-specialised
+// persistent CTAs (one per SM):
+//   warp 0      TMA producer (one elected lane)
+//   warp 1      TMEM allocator + MMA issuer (one elected lane)
+//   warps 2..5  epilogue: tcgen05.ld -> fused op -> smem transpose -> coalesced st.global
+// Two 256-column accumulators in TMEM let tile i's epilogue overlap tile i+1's
+// mainloop.  The LoRA delta of a targeted projection is folded in as a
+// K-extension: x W^T + (s x A^T) B^T = [x | T] [W | B]^T, i.e. ceil(r/16)
+// extra UMMA K-steps reading T [M, r] and lora_B [n, r] (zero-filled by TMA
+// beyond r), so no separate expand kernel and no extra pass over C.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace tidal {
+
+namespace {
+
+constexpr int BM = GEMM_BM, BN = GEMM_BN, BK = GEMM_BK, STAGES = GEMM_STAGES;
+constexpr int A_BYTES = BM * BK * 2;          // 16 KB
+constexpr int B_BYTES = BN * BK * 2;          // 32 KB
+constexpr int STG_ROW = 144;                  // staging row stride (bytes)
+constexpr int STG_WARP = 32 * STG_ROW;
+constexpr int OFF_A = 0;
+constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
+constexpr int OFF_STG = OFF_B + STAGES * B_BYTES;
+constexpr int OFF_BAR = OFF_STG + 4 * STG_WARP;
+constexpr int N_BARS = 2 * STAGES + 4;
+constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
+constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;   // + alignment slack
+constexpr int TMEM_COLS = 512;
+constexpr int NTHREADS = 192;
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+// Store one 32-column chunk of this thread's row (bf16) via the warp's
+// staging buffer so that global stores are row-contiguous.
+__device__ __forceinline__ void store_chunk_bf16(const float (&v)[32], uint8_t* stg, int lane,
+                                                 bf16* out, int ldo, int row0, int M, int col,
+                                                 int nvalid) {
+  uint4* st = reinterpret_cast<uint4*>(stg + lane * 80);
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    uint4 w;
+    w.x = pack_bf16x2(v[8 * k + 0], v[8 * k + 1]);
+    w.y = pack_bf16x2(v[8 * k + 2], v[8 * k + 3]);
+    w.z = pack_bf16x2(v[8 * k + 4], v[8 * k + 5]);
+    w.w = pack_bf16x2(v[8 * k + 6], v[8 * k + 7]);
+    st[k] = w;
+  }
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 4; ++it) {
+    const int r = it * 8 + (lane >> 2), ch = lane & 3;
+    const int m = row0 + r;
+    const int c = ch * 8;
+    if (m < M && c < nvalid) {
+      uint4 w = *reinterpret_cast<const uint4*>(stg + r * 80 + ch * 16);
+      bf16* dst = out + (size_t)m * ldo + col + c;
+      if (c + 8 <= nvalid) {
+        *reinterpret_cast<uint4*>(dst) = w;
+      } else {
+        const bf16* src = reinterpret_cast<const bf16*>(&w);
+        for (int e = 0; e < nvalid - c; ++e) dst[e] = src[e];
+      }
+    }
+  }
+  __syncwarp();
+}
+
+// out[m, col + j] += v[j]  (fp32 residual), coalesced through staging.
+__device__ __forceinline__ void add_chunk_f32(const float (&v)[32], uint8_t* stg, int lane,
+                                              float* out, int ldo, int row0, int M, int col,
+                                              int nvalid) {
+  float4* st = reinterpret_cast<float4*>(stg + lane * STG_ROW);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) st[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  __syncwarp();
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int r = it * 4 + (lane >> 3), ch = lane & 7;
+    const int m = row0 + r;
+    const int c = ch * 4;
+    if (m < M && c < nvalid) {
+      float4 a = *reinterpret_cast<const float4*>(stg + r * STG_ROW + ch * 16);
+      float* dst = out + (size_t)m * ldo + col + c;
+      if (c + 4 <= nvalid) {
+        float4 x = *reinterpret_cast<float4*>(dst);
+        x.x += a.x;
+        x.y += a.y;
+        x.z += a.z;
+        x.w += a.w;
+        *reinterpret_cast<float4*>(dst) = x;
+      } else {
+        const float* s = reinterpret_cast<const float*>(&a);
+        for (int e = 0; e < nvalid - c; ++e) dst[e] += s[e];
+      }
+    }
+  }
+  __syncwarp();
+}
+
+__device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  ptx::tmem_ld32(taddr, r);
+  ptx::tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+template <int EPI>
+__device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& seg, int& n0,
+                                            int& m0) {
+  int gn = tile / p.m_tiles;
+  m0 = (tile - gn * p.m_tiles) * BM;
+  seg = 0;
+  while (seg < p.nseg - 1 && gn >= p.n_tiles[seg]) {
+    gn -= p.n_tiles[seg];
+    ++seg;
+  }
+  n0 = gn * (EPI == EPI_SILU ? 128 : BN);
+}
+
+template <int EPI>
+__global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>(
+      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const uint32_t sbase = ptx::smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bar0 = sbase + OFF_BAR;
+  auto full_bar = [&](int s) { return bar0 + 8u * s; };
+  auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
+  auto tfull_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + a); };
+  auto tempty_bar = [&](int a) { return bar0 + 8u * (2 * STAGES + 2 + a); };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+
+  const int nk = (p.K + BK - 1) / BK;
+  const int nlora = p.lora_r > 0 ? (EPI == EPI_SILU ? 2 : 1) : 0;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&p.a);
+    for (int i = 0; i < 3; ++i) {
+      if (i < p.nseg || (EPI == EPI_SILU && i < 2)) {
+        ptx::prefetch_tmap(&p.b[i]);
+      }
+    }
+    for (int s = 0; s < STAGES; ++s) {
+      ptx::mbar_init(full_bar(s), 1);
+      ptx::mbar_init(empty_bar(s), 1);
+    }
+    for (int a = 0; a < 2; ++a) {
+      ptx::mbar_init(tfull_bar(a), 1);
+      ptx::mbar_init(tempty_bar(a), 128);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), TMEM_COLS);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem_base = *tmem_holder;
+
+  if (warp == 0) {
+    // ===================== TMA producer =====================
+    if (lane == 0) {
+      int stage = 0;
+      uint32_t phase = 0;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        int seg, n0, m0;
+        decode_tile<EPI>(p, tile, seg, n0, m0);
+        const bool lora = nlora > 0 && p.seg[seg].lora;
+        const int nkb = nk + (lora ? nlora : 0);
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+          const uint32_t sa = sbase + OFF_A + stage * A_BYTES;
+          const uint32_t sb = sbase + OFF_B + stage * B_BYTES;
+          const uint32_t fb = full_bar(stage);
+          if (kb < nk) {
+            ptx::mbar_expect_tx(fb, A_BYTES + B_BYTES);
+            ptx::tma_load_2d(&p.a, sa, fb, kb * BK, m0);
+            if (EPI == EPI_SILU) {
+              ptx::tma_load_2d(&p.b[0], sb, fb, kb * BK, n0);
+              ptx::tma_load_2d(&p.b[1], sb + B_BYTES / 2, fb, kb * BK, n0);
+            } else {
+              ptx::tma_load_2d(&p.b[seg], sb, fb, kb * BK, n0);
+            }
+          } else {
+            const int j = kb - nk;  // LoRA stage: EPI_SILU j=0 gate, j=1 up
+            const int t = EPI == EPI_SILU ? j : seg;
+            const int bbytes = EPI == EPI_SILU ? B_BYTES / 2 : B_BYTES;
+            ptx::mbar_expect_tx(fb, A_BYTES + bbytes);
+            ptx::tma_load_2d(&p.ta[t], sa, fb, 0, m0);
+            ptx::tma_load_2d(&p.tb[t], sb, fb, 0, n0);
+          }
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    // ===================== MMA issuer =====================
+    if (lane == 0) {
+      constexpr uint32_t IDESC = ptx::idesc_bf16(BM, BN);
+      constexpr uint32_t IDESC_HALF = ptx::idesc_bf16(BM, BN / 2);
+      const int nmma_lora = (p.lora_r + 15) / 16;
+      int stage = 0;
+      uint32_t phase = 0;
+      int acc = 0;
+      uint32_t acc_phase = 0;
+      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+        int seg, n0, m0;
+        decode_tile<EPI>(p, tile, seg, n0, m0);
+        const bool lora = nlora > 0 && p.seg[seg].lora;
+        const int nkb = nk + (lora ? nlora : 0);
+        ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
+        ptx::tc_fence_after();
+        const uint32_t d_tmem = tmem_base + acc * BN;
+        for (int kb = 0; kb < nkb; ++kb) {
+          ptx::mbar_wait(full_bar(stage), phase);
+          ptx::tc_fence_after();
+          const uint64_t adesc = ptx::desc_sw128(sbase + OFF_A + stage * A_BYTES);
+          const uint64_t bdesc = ptx::desc_sw128(sbase + OFF_B + stage * B_BYTES);
+          if (kb < nk) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              ptx::mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb | k) != 0);
+          } else if (EPI == EPI_SILU) {
+            const int j = kb - nk;
+            for (int k = 0; k < nmma_lora; ++k)
+              ptx::mma_bf16(d_tmem + j * (BN / 2), adesc + 2 * k, bdesc + 2 * k, IDESC_HALF, 1);
+          } else {
+            for (int k = 0; k < nmma_lora; ++k)
+              ptx::mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, 1);
+          }
+          ptx::mma_commit(empty_bar(stage));
+          if (++stage == STAGES) {
+            stage = 0;
+            phase ^= 1;
+          }
+        }
+        ptx::mma_commit(tfull_bar(acc));
+        if (++acc == 2) {
+          acc = 0;
+          acc_phase ^= 1;
+        }
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== epilogue (warps 2..5) =====================
+    const int q = warp & 3;  // TMEM lane quarter this warp may access
+    uint8_t* stg = smem + OFF_STG + (warp - 2) * STG_WARP;
+    int acc = 0;
+    uint32_t acc_phase = 0;
+    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      int seg, n0, m0;
+      decode_tile<EPI>(p, tile, seg, n0, m0);
+      const GemmSeg sg = p.seg[seg];
+      ptx::mbar_wait(tfull_bar(acc), acc_phase);
+      ptx::tc_fence_after();
+      const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const int row0 = m0 + q * 32;
+      const int m = row0 + lane;
+      float v[32], w[32];
+      if (EPI == EPI_SILU) {
+        const int ncols = min(128, sg.n - n0);
+#pragma unroll 1
+        for (int j = 0; j < 4; ++j) {
+          if (j * 32 >= ncols) break;
+          ld_chunk(tacc + j * 32, v);          // gate
+          ld_chunk(tacc + 128 + j * 32, w);    // up
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const float g = v[i];
+            v[i] = g / (1.0f + __expf(-g)) * w[i];
+          }
+          store_chunk_bf16(v, stg, lane, reinterpret_cast<bf16*>(p.out), p.ldo, row0, p.M,
+                           sg.out_col + n0 + j * 32, ncols - j * 32);
+        }
+      } else if (EPI == EPI_RESID) {
+        const int ncols = min(BN, sg.n - n0);
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          if (j * 32 >= ncols) break;
+          ld_chunk(tacc + j * 32, v);
+          add_chunk_f32(v, stg, lane, reinterpret_cast<float*>(p.out), p.ldo, row0, p.M,
+                        sg.out_col + n0 + j * 32, ncols - j * 32);
+        }
+      } else if (EPI == EPI_ROPE && sg.rope) {
+        const int hd = p.head_dim, half = hd >> 1;
+        const int ncols = min(BN, sg.n - n0);
+#pragma unroll 1
+        for (int h = 0; h * hd < ncols; ++h) {
+#pragma unroll 1
+          for (int j = 0; j * 32 < half; ++j) {
+            const int c1 = h * hd + j * 32, c2 = c1 + half;
+            ld_chunk(tacc + c1, v);
+            ld_chunk(tacc + c2, w);
+            if (m < p.M) {
+              const float2* cs = p.rope + (size_t)m * half + j * 32;
+#pragma unroll
+              for (int i = 0; i < 32; ++i) {
+                const float2 t = cs[i];
+                const float x1 = v[i], x2 = w[i];
+                v[i] = x1 * t.x - x2 * t.y;
+                w[i] = x2 * t.x + x1 * t.y;
+              }
+            }
+            bf16* out = reinterpret_cast<bf16*>(p.out);
+            store_chunk_bf16(v, stg, lane, out, p.ldo, row0, p.M, sg.out_col + n0 + c1, 32);
+            store_chunk_bf16(w, stg, lane, out, p.ldo, row0, p.M, sg.out_col + n0 + c2, 32);
+          }
+        }
+      } else {
+        const int ncols = min(BN, sg.n - n0);
+#pragma unroll 1
+        for (int j = 0; j < BN / 32; ++j) {
+          if (j * 32 >= ncols) break;
+          ld_chunk(tacc + j * 32, v);
+          store_chunk_bf16(v, stg, lane, reinterpret_cast<bf16*>(p.out), p.ldo, row0, p.M,
+                           sg.out_col + n0 + j * 32, ncols - j * 32);
+        }
+      }
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(tempty_bar(acc));
+      if (++acc == 2) {
+        acc = 0;
+        acc_phase ^= 1;
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+  }
+}
+
+typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*,
+                                  const cuuint64_t*, const cuuint64_t*, const cuuint32_t*,
+                                  const cuuint32_t*, CUtensorMapInterleave, CUtensorMapSwizzle,
+                                  CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+EncodeTiledFn g_encode = nullptr;
+std::once_flag g_once;
+
+template <int EPI>
+cudaError_t launch_t(const GemmParams& p, int num_sms, cudaStream_t s) {
+  static bool attr_done = false;
+  if (!attr_done) {
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    if (e != cudaSuccess) return e;
+    attr_done = true;
+  }
+  int grid = p.total_tiles < num_sms ? p.total_tiles : num_sms;
+  if (grid <= 0) return cudaSuccess;
+  gemm_tc_kernel<EPI><<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+bool tma_init() {
+  std::call_once(g_once, [] {
+    void* fn = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) ==
+            cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<EncodeTiledFn>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+               uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols) {
+  if (!tma_init()) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2, const_cast<void*>(base), dims,
+                        strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t s) {
+  switch (epi) {
+    case EPI_STORE: return launch_t<EPI_STORE>(p, num_sms, s);
+    case EPI_ROPE: return launch_t<EPI_ROPE>(p, num_sms, s);
+    case EPI_SILU: return launch_t<EPI_SILU>(p, num_sms, s);
+    case EPI_RESID: return launch_t<EPI_RESID>(p, num_sms, s);
+  }
+  return cudaErrorInvalidValue;
+}
+
+}  // namespace tidal

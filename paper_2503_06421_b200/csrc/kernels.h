@@ -1,0 +1,86 @@
+// kernels.h — device kernels of the prefill path (sm_100a), host launchers.
+#pragma once
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace tidal {
+
+using bf16 = __nv_bfloat16;
+
+// ------------------------------------------------------------------------
+// tcgen05 GEMM  C[M, N] = A[M, K] . W[N, K]^T  (+ LoRA K-extension), fused
+// epilogues.  A and W are bf16, K-major ("TN"), fed by TMA (SWIZZLE_128B)
+// into a 4-stage mbarrier ring; accumulators live in TMEM (2 x 256 columns,
+// double-buffered so the epilogue of tile i overlaps the mainloop of i+1);
+// persistent grid of one CTA per SM.
+// ------------------------------------------------------------------------
+enum GemmEpi : int {
+  EPI_STORE = 0,  // out bf16 [M, ldo] at out_col
+  EPI_ROPE = 1,   // as STORE, rotate-half RoPE on segments with rope=1 (q, k)
+  EPI_SILU = 2,   // W = [gate ; up] paired 128-row tiles: out = silu(g) * u (bf16)
+  EPI_RESID = 3   // out fp32 [M, ldo]: out += acc (residual stream)
+};
+
+constexpr int GEMM_BM = 128, GEMM_BN = 256, GEMM_BK = 64, GEMM_STAGES = 4;
+
+struct GemmSeg {
+  int n;        // rows of this weight segment (output columns)
+  int out_col;  // first output column
+  int lora;     // LoRA K-extension present for this segment
+  int rope;     // EPI_ROPE: rotate this segment
+};
+
+struct alignas(64) GemmParams {
+  CUtensorMap a;       // A [M, K], box {64, 128}
+  CUtensorMap b[3];    // W segment [n, K], box {64, 256} (EPI_SILU: b[0]=gate, b[1]=up, box {64,128})
+  CUtensorMap ta[3];   // T [M, r] (LoRA shrink output, scale folded), box {64, 128}
+  CUtensorMap tb[3];   // lora_B [n, r], box {64, 256} (EPI_SILU: {64, 128})
+  GemmSeg seg[3];
+  int nseg;
+  int M, K;
+  int lora_r;          // 0: no LoRA
+  int m_tiles;
+  int n_tiles[3];
+  int total_tiles;
+  void* out;
+  int ldo;
+  const float2* rope;  // [S, head_dim/2] (cos, sin)
+  int head_dim;
+};
+
+// Host helpers (gemm_tc.cu).
+bool tma_init();  // resolve cuTensorMapEncodeTiled through the runtime
+// 2-D bf16 tensor map: rows x cols, row stride in bytes, box {box_cols, box_rows}, SW128.
+bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+               uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols);
+cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t s);
+
+// ------------------------------------------------------------------------
+// SIMT / legacy-MMA kernels (kernels.cu, attention.cu)
+// ------------------------------------------------------------------------
+// X[s, :] = fp32(E[tok[s] - row0, :]) for tokens in [row0, row0+rows), else 0 (vocab shard).
+cudaError_t embed_launch(const int32_t* tok, const bf16* E, float* X, int S, int d, int row0,
+                         int rows, cudaStream_t s);
+// Y = bf16(g * x * rsqrt(mean(x^2) + eps)), one row per CTA.
+cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d, float eps,
+                           cudaStream_t s);
+// T_t[M, r] = bf16(scale * X[M, K] . A_t[r, K]^T), t < nt (targets sharing X).
+cudaError_t lora_shrink_launch(const bf16* X, int ldx, int M, int K, const bf16* const* A,
+                               bf16* const* T, int nt, int r, float scale, cudaStream_t s);
+// Causal GQA prefill attention over QKV [S, (H + 2 KV) hd] -> O [S, H hd].
+cudaError_t attention_launch(const bf16* qkv, bf16* O, int S, int H, int KV, int hd,
+                             cudaStream_t s);
+// Final RMSNorm of row X_last, logits[v] = W[v] . h (fp32), packed argmax key
+// (orderable(logit) << 32 | ~v) max-reduced into *key (must be preset to 0).
+cudaError_t head_launch(const float* X_last, const bf16* g, const bf16* W, int V, int d, float eps,
+                        float* logits, unsigned long long* key, int vocab_offset, int num_sms,
+                        cudaStream_t s);
+// Debug / invariants.
+cudaError_t poison_launch(void* p, size_t bytes, cudaStream_t s);           // bf16 NaN 0x7FC0
+cudaError_t checksum_launch(const void* p, size_t bytes, unsigned long long* out, cudaStream_t s);
+cudaError_t scrub_launch(void* p, size_t bytes, cudaStream_t s);
+cudaError_t nan_check_launch(const float* x, int n, int* flag, cudaStream_t s);
+
+}  // namespace tidal

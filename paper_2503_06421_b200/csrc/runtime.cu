@@ -1,0 +1,388 @@
+// runtime.cu — the op launcher: walks the canonical op sequence (plan.h R1),
+// waits on the copy-stream events of the transfer groups each op reads
+// (§5.2 "injects synchronization events"), and enqueues the
+// fused kernels for that op.  The same launcher serves the traced first run
+// (a Recorder captures first-read order as ops execute) and every invocation.
+#include <cuda_runtime.h>
+#include <sched.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <fstream>
+#include <sstream>
+
+#include "runtime.h"
+
+namespace tidal {
+
+[[noreturn]] void fail(int code, const std::string& msg) { throw Error{code, msg}; }
+
+void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) {
+    if (e == cudaErrorMemoryAllocation) fail(2, std::string(what) + ": " + cudaGetErrorString(e));
+    fail(3, std::string(what) + ": " + cudaGetErrorString(e));
+  }
+}
+
+template <typename T>
+static void dalloc(T*& p, size_t bytes) {
+  void* q = nullptr;
+  cuda_check(cudaMalloc(&q, bytes ? bytes : 16), "cudaMalloc(activations)");
+  p = reinterpret_cast<T*>(q);
+}
+
+void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int world_, int rank_,
+                int max_tok) {
+  device = dev;
+  m = shape;
+  eps = eps_;
+  theta = theta_;
+  world = world_;
+  rank = rank_;
+  max_tokens = max_tok;
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, device), "SM count");
+  if (!tma_init()) fail(3, "cuTensorMapEncodeTiled unavailable (driver too old?)");
+  int lo = 0, hi = 0;
+  cudaDeviceGetStreamPriorityRange(&lo, &hi);
+  cuda_check(cudaStreamCreateWithPriority(&compute, cudaStreamNonBlocking, lo), "stream");
+  cuda_check(cudaStreamCreateWithPriority(&copy, cudaStreamNonBlocking, hi), "stream");
+  const size_t S = (size_t)max_tokens;
+  const int hd = m.head_dim();
+  const size_t nq = (size_t)m.n_heads * hd / world, nkv = (size_t)m.n_kv_heads * hd / world;
+  dalloc(X, S * m.d_model * 4);
+  dalloc(Xn, S * m.d_model * 2);
+  dalloc(QKV, S * (nq + 2 * nkv) * 2);
+  dalloc(O, S * nq * 2);
+  dalloc(Hb, S * (size_t)(m.d_ff / world) * 2);
+  for (int t = 0; t < kNumTargets; ++t) dalloc(T[t], S * 64 * 2);
+  dalloc(logits, (size_t)m.vocab * 4);
+  dalloc(key, 64);
+  dalloc(tok, S * 4);
+  // RoPE table: angle = pos * theta^(-2i/hd), cos/sin in double, stored fp32
+  std::vector<float2> cs(S * (hd / 2));
+  for (size_t p = 0; p < S; ++p)
+    for (int i = 0; i < hd / 2; ++i) {
+      const double inv = std::pow((double)theta, -(2.0 * i) / hd);
+      const double ang = (double)p * inv;
+      cs[p * (hd / 2) + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    }
+  dalloc(rope, cs.size() * sizeof(float2));
+  cuda_check(cudaMemcpy(rope, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice),
+             "rope upload");
+  cuda_check(cudaHostAlloc((void**)&h_tok, S * 4 + 16, cudaHostAllocDefault), "pinned tokens");
+  cuda_check(cudaHostAlloc((void**)&h_logits, (size_t)m.vocab * 4 + 16, cudaHostAllocDefault),
+             "pinned logits");
+  cuda_check(cudaHostAlloc((void**)&h_key, 64, cudaHostAllocDefault), "pinned key");
+}
+
+void Exec::destroy() {
+  if (device < 0) return;
+  cudaSetDevice(device);
+  if (compute) cudaStreamSynchronize(compute);
+  if (copy) cudaStreamSynchronize(copy);
+  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  for (int t = 0; t < kNumTargets; ++t)
+    if (T[t]) cudaFree(T[t]);
+  if (h_tok) cudaFreeHost(h_tok);
+  if (h_logits) cudaFreeHost(h_logits);
+  if (h_key) cudaFreeHost(h_key);
+  if (compute) cudaStreamDestroy(compute);
+  if (copy) cudaStreamDestroy(copy);
+  device = -1;
+}
+
+static void tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
+                 uint32_t box_rows) {
+  if (!make_tmap(m, base, rows, cols, cols * 2, box_rows, 64))
+    fail(3, "cuTensorMapEncodeTiled failed (rows=" + std::to_string(rows) +
+                " cols=" + std::to_string(cols) + ")");
+}
+
+const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S, const void* akey,
+                                                   uint64_t gen) {
+  auto k = std::make_tuple(S, tt.lora_rank, tt.lora_mask, akey, gen);
+  auto it = cache.find(k);
+  if (it != cache.end()) return it->second;
+  const int L = m.n_layers, d = m.d_model, hd = m.head_dim();
+  const int nq = m.n_heads * hd / world, nkv = m.n_kv_heads * hd / world;
+  const int F = m.d_ff / world;
+  const int r = tt.lora_rank;
+  const int mt = (S + GEMM_BM - 1) / GEMM_BM;
+  std::vector<LayerLaunch> v(L);
+  auto W = [&](int id) { return wptr[id]; };
+  for (int l = 0; l < L; ++l) {
+    LayerLaunch& ll = v[l];
+    // ---- QKV + RoPE ----
+    GemmParams& q = ll.qkv;
+    memset(&q, 0, sizeof q);
+    tmap(&q.a, Xn, S, d, 128);
+    const int segn[3] = {nq, nkv, nkv};
+    const int tg[3] = {T_Q, T_K, T_V};
+    int col = 0;
+    q.lora_r = 0;
+    q.total_tiles = 0;
+    for (int s = 0; s < 3; ++s) {
+      q.seg[s].n = segn[s];
+      q.seg[s].out_col = col;
+      q.seg[s].rope = s < 2;
+      col += segn[s];
+      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, 256);
+      const int la = tt.lora_a[l][tg[s]];
+      q.seg[s].lora = la >= 0;
+      if (la >= 0) {
+        q.lora_r = r;
+        tmap(&q.ta[s], T[tg[s]], S, r, 128);
+        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, 256);
+      }
+      q.n_tiles[s] = (segn[s] + GEMM_BN - 1) / GEMM_BN;
+      q.total_tiles += q.n_tiles[s] * mt;
+    }
+    q.nseg = 3;
+    q.M = S;
+    q.K = d;
+    q.m_tiles = mt;
+    q.out = QKV;
+    q.ldo = nq + 2 * nkv;
+    q.rope = rope;
+    q.head_dim = hd;
+    // ---- O (+ residual) ----
+    GemmParams& o = ll.o;
+    memset(&o, 0, sizeof o);
+    tmap(&o.a, O, S, nq, 128);
+    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, 256);
+    o.seg[0].n = d;
+    o.seg[0].lora = tt.lora_a[l][T_O] >= 0;
+    if (o.seg[0].lora) {
+      o.lora_r = r;
+      tmap(&o.ta[0], T[T_O], S, r, 128);
+      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, 256);
+    }
+    o.nseg = 1;
+    o.M = S;
+    o.K = nq;
+    o.m_tiles = mt;
+    o.n_tiles[0] = (d + GEMM_BN - 1) / GEMM_BN;
+    o.total_tiles = o.n_tiles[0] * mt;
+    o.out = X;
+    o.ldo = d;
+    // ---- gate/up + SiLU*mul ----
+    GemmParams& g = ll.gu;
+    memset(&g, 0, sizeof g);
+    tmap(&g.a, Xn, S, d, 128);
+    tmap(&g.b[0], W(tt.proj[l][T_GATE]), F, d, 128);
+    tmap(&g.b[1], W(tt.proj[l][T_UP]), F, d, 128);
+    g.seg[0].n = F;
+    g.seg[0].lora = tt.lora_a[l][T_GATE] >= 0;
+    if (g.seg[0].lora) {
+      g.lora_r = r;
+      tmap(&g.ta[0], T[T_GATE], S, r, 128);
+      tmap(&g.ta[1], T[T_UP], S, r, 128);
+      tmap(&g.tb[0], W(tt.lora_b[l][T_GATE]), F, r, 128);
+      tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, 128);
+    }
+    g.nseg = 1;
+    g.M = S;
+    g.K = d;
+    g.m_tiles = mt;
+    g.n_tiles[0] = (F + 127) / 128;
+    g.total_tiles = g.n_tiles[0] * mt;
+    g.out = Hb;
+    g.ldo = F;
+    // ---- down (+ residual) ----
+    GemmParams& dn = ll.down;
+    memset(&dn, 0, sizeof dn);
+    tmap(&dn.a, Hb, S, F, 128);
+    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, 256);
+    dn.seg[0].n = d;
+    dn.seg[0].lora = tt.lora_a[l][T_DOWN] >= 0;
+    if (dn.seg[0].lora) {
+      dn.lora_r = r;
+      tmap(&dn.ta[0], T[T_DOWN], S, r, 128);
+      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, 256);
+    }
+    dn.nseg = 1;
+    dn.M = S;
+    dn.K = F;
+    dn.m_tiles = mt;
+    dn.n_tiles[0] = (d + GEMM_BN - 1) / GEMM_BN;
+    dn.total_tiles = dn.n_tiles[0] * mt;
+    dn.out = X;
+    dn.ldo = d;
+  }
+  if (cache.size() > 64) cache.clear();
+  return cache.emplace(k, std::move(v)).first->second;
+}
+
+enum OpKind {
+  OP_EMBED, OP_ATTN_NORM, OP_QKV, OP_ROPE, OP_ATTN, OP_O, OP_MLP_NORM, OP_GU, OP_ACT, OP_DOWN,
+  OP_FNORM, OP_HEAD, OP_ARGMAX, OP_EMBED_AR, OP_ATTN_AR, OP_MLP_AR, OP_LOGITS_AG
+};
+
+static int op_kind(const std::string& n) {
+  static const std::map<std::string, int> k = {
+      {"embed", OP_EMBED}, {"attn_norm", OP_ATTN_NORM}, {"qkv_proj", OP_QKV}, {"rope", OP_ROPE},
+      {"attention", OP_ATTN}, {"o_proj", OP_O}, {"mlp_norm", OP_MLP_NORM},
+      {"gate_up_proj", OP_GU}, {"act_mul", OP_ACT}, {"down_proj", OP_DOWN},
+      {"final_norm", OP_FNORM}, {"lm_head", OP_HEAD}, {"argmax", OP_ARGMAX},
+      {"embed_allreduce", OP_EMBED_AR}, {"attn_allreduce", OP_ATTN_AR},
+      {"mlp_allreduce", OP_MLP_AR}, {"logits_allgather", OP_LOGITS_AG}};
+  auto it = k.find(n);
+  if (it == k.end()) fail(1, "unknown op " + n);
+  return it->second;
+}
+
+// TP collectives (nccl.cu); no-ops when world == 1.
+void tp_allreduce_f32(Exec& ex, void* comm, float* buf, size_t n);
+void tp_argmax_reduce(Exec& ex, void* comm, unsigned long long* key);
+void tp_allgather_logits(Exec& ex, void* comm);
+
+void run_forward(Exec& ex, const RunArgs& a) {
+  const TensorTable& tt = *a.tt;
+  const ModelShape& m = ex.m;
+  const int S = a.S, d = m.d_model, hd = m.head_dim();
+  const int nq = m.n_heads * hd / ex.world;
+  const int F = m.d_ff / ex.world;
+  const int Vl = m.vocab / ex.world;
+  const int r = tt.lora_rank;
+  const auto& LP = ex.layer_params(tt, S, a.akey, a.gen);
+  cudaStream_t st = ex.compute;
+  int waited = -1;
+  auto K = [&](cudaError_t e, const char* what) {
+    cuda_check(e, what);
+    ++ex.launches;
+  };
+  auto shrink = [&](const bf16* X, int ldx, int Kd, int l, std::initializer_list<int> ts) {
+    const bf16* A[3];
+    bf16* T[3];
+    int n = 0;
+    for (int t : ts)
+      if (tt.lora_a[l][t] >= 0) {
+        A[n] = reinterpret_cast<const bf16*>(ex.wptr[tt.lora_a[l][t]]);
+        T[n] = ex.T[t];
+        ++n;
+      }
+    if (n) K(lora_shrink_launch(X, ldx, S, Kd, A, T, n, r, a.lora_scale, st), "lora_shrink");
+  };
+  const std::vector<Op>& ops = *a.ops;
+  for (size_t k = 0; k < ops.size(); ++k) {
+    const Op& op = ops[k];
+    if (a.rec) a.rec->op((int)k, op.reads, tt.n_base);
+    if (a.barriers && !(*a.barriers)[k].empty()) {
+      int g = -1;
+      for (int x : (*a.barriers)[k])
+        if (x != a.skip_group) g = std::max(g, x);
+      if (g > waited) {
+        cuda_check(cudaStreamWaitEvent(st, (*a.events)[g], 0), "cudaStreamWaitEvent");
+        waited = g;
+      }
+    }
+    const int l = op.layer;
+    auto Wp = [&](int id) { return reinterpret_cast<const bf16*>(ex.wptr[id]); };
+    switch (op_kind(op.name)) {
+      case OP_EMBED:
+        K(embed_launch(ex.tok, Wp(tt.embed), ex.X, S, d, ex.rank * Vl, Vl, st), "embed");
+        break;
+      case OP_EMBED_AR:
+      case OP_ATTN_AR:
+      case OP_MLP_AR:
+        tp_allreduce_f32(ex, a.nccl, ex.X, (size_t)S * d);
+        break;
+      case OP_ATTN_NORM:
+        K(rmsnorm_launch(ex.X, Wp(tt.norm1[l]), ex.Xn, S, d, ex.eps, st), "rmsnorm");
+        break;
+      case OP_QKV:
+        shrink(ex.Xn, d, d, l, {T_Q, T_K, T_V});
+        K(gemm_launch(LP[l].qkv, EPI_ROPE, ex.num_sms, st), "gemm_qkv");
+        break;
+      case OP_ROPE:  // fused into the QKV epilogue
+        break;
+      case OP_ATTN:
+        K(attention_launch(ex.QKV, ex.O, S, m.n_heads / ex.world, m.n_kv_heads / ex.world, hd, st),
+          "attention");
+        break;
+      case OP_O:
+        shrink(ex.O, nq, nq, l, {T_O});
+        if (ex.world > 1 && ex.rank != 0)
+          cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
+        K(gemm_launch(LP[l].o, EPI_RESID, ex.num_sms, st), "gemm_o");
+        break;
+      case OP_MLP_NORM:
+        K(rmsnorm_launch(ex.X, Wp(tt.norm2[l]), ex.Xn, S, d, ex.eps, st), "rmsnorm");
+        break;
+      case OP_GU:
+        shrink(ex.Xn, d, d, l, {T_GATE, T_UP});
+        K(gemm_launch(LP[l].gu, EPI_SILU, ex.num_sms, st), "gemm_gate_up");
+        break;
+      case OP_ACT:  // fused into the gate/up epilogue
+        break;
+      case OP_DOWN:
+        shrink(ex.Hb, F, F, l, {T_DOWN});
+        if (ex.world > 1 && ex.rank != 0)
+          cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
+        K(gemm_launch(LP[l].down, EPI_RESID, ex.num_sms, st), "gemm_down");
+        break;
+      case OP_FNORM:  // fused into the head kernel (fp32 last-row norm)
+        break;
+      case OP_HEAD:
+        cuda_check(cudaMemsetAsync(ex.key, 0, 8, st), "memset key");
+        K(head_launch(ex.X + (size_t)(S - 1) * d, Wp(tt.fnorm), Wp(tt.head), Vl, d, ex.eps,
+                      ex.logits + (size_t)ex.rank * Vl, ex.key, ex.rank * Vl, ex.num_sms, st),
+          "head");
+        break;
+      case OP_LOGITS_AG:
+        tp_allgather_logits(ex, a.nccl);
+        break;
+      case OP_ARGMAX:  // fused: atomicMax of packed keys in the head kernel
+        tp_argmax_reduce(ex, a.nccl, ex.key);
+        break;
+    }
+  }
+}
+
+// ---------------- NUMA binding ----------------
+static bool parse_cpulist(const std::string& s, cpu_set_t* set) {
+  CPU_ZERO(set);
+  std::stringstream ss(s);
+  std::string part;
+  bool any = false;
+  while (std::getline(ss, part, ',')) {
+    int a = 0, b = 0;
+    if (sscanf(part.c_str(), "%d-%d", &a, &b) == 2) {
+    } else if (sscanf(part.c_str(), "%d", &a) == 1) {
+      b = a;
+    } else {
+      continue;
+    }
+    for (int c = a; c <= b && c < CPU_SETSIZE; ++c) {
+      CPU_SET(c, set);
+      any = true;
+    }
+  }
+  return any;
+}
+
+NumaGuard::NumaGuard(int device) {
+  static_assert(sizeof(cpu_set_t) <= sizeof(saved), "cpu_set_t too large");
+  char bus[32] = {0};
+  if (cudaDeviceGetPCIBusId(bus, sizeof bus, device) != cudaSuccess) return;
+  for (char* c = bus; *c; ++c) *c = (char)tolower(*c);
+  std::ifstream f(std::string("/sys/bus/pci/devices/") + bus + "/local_cpulist");
+  std::string line;
+  if (!f || !std::getline(f, line)) return;
+  cpu_set_t want, avail;
+  if (!parse_cpulist(line, &want)) return;
+  if (sched_getaffinity(0, sizeof(cpu_set_t), reinterpret_cast<cpu_set_t*>(saved)) != 0) return;
+  CPU_AND(&avail, &want, reinterpret_cast<cpu_set_t*>(saved));
+  if (CPU_COUNT(&avail) == 0) return;
+  if (sched_setaffinity(0, sizeof(cpu_set_t), &avail) == 0) active = true;
+}
+
+NumaGuard::~NumaGuard() {
+  if (active) sched_setaffinity(0, sizeof(cpu_set_t), reinterpret_cast<cpu_set_t*>(saved));
+}
+
+}  // namespace tidal

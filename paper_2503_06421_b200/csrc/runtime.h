@@ -1,0 +1,102 @@
+// runtime.h — device execution context and the op launcher.
+#pragma once
+#include <cuda_runtime.h>
+
+#include <map>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "kernels.h"
+#include "plan.h"
+
+namespace tidal {
+
+struct Status {
+  int code = 0;
+  std::string msg;
+};
+struct Error {
+  int code;
+  std::string msg;
+};
+[[noreturn]] void fail(int code, const std::string& msg);
+void cuda_check(cudaError_t e, const char* what);
+
+// Per-layer launch parameters, cached per (prompt length, adapter layout).
+struct LayerLaunch {
+  GemmParams qkv, o, gu, down;
+};
+
+// Device execution context: streams, activation arena, rope table, the fork
+// pointer table (tensor id -> device address) and a launch-parameter cache.
+struct Exec {
+  int device = -1, num_sms = 148;
+  ModelShape m;
+  float eps = 1e-5f, theta = 1e4f;
+  int world = 1, rank = 0;
+  int max_tokens = 0;
+  cudaStream_t compute = nullptr, copy = nullptr;
+  // activations
+  float* X = nullptr;
+  bf16 *Xn = nullptr, *QKV = nullptr, *O = nullptr, *Hb = nullptr;
+  bf16* T[kNumTargets] = {};
+  float* logits = nullptr;
+  unsigned long long* key = nullptr;
+  int32_t* tok = nullptr;
+  float2* rope = nullptr;
+  // pinned host staging
+  int32_t* h_tok = nullptr;
+  float* h_logits = nullptr;
+  unsigned long long* h_key = nullptr;
+  // fork pointer table
+  std::vector<void*> wptr;
+  // cache: (S, lora_rank, mask, adapter arena base) -> per-layer params
+  std::map<std::tuple<int, int, uint32_t, const void*, uint64_t>, std::vector<LayerLaunch>> cache;
+  int launches = 0;
+
+  void init(int device, const ModelShape& m, float eps, float theta, int world, int rank,
+            int max_tokens);
+  void destroy();
+  const std::vector<LayerLaunch>& layer_params(const TensorTable& tt, int S, const void* akey,
+                                               uint64_t gen);
+};
+
+struct Recorder {  // lax tracing: first-read order of weights as ops execute
+  std::vector<char> seen;
+  std::vector<std::pair<int, int>> access;
+  void op(int k, const std::vector<int>& reads, int n_base) {
+    for (int id : reads)
+      if (id < n_base && !seen[id]) {
+        seen[id] = 1;
+        access.emplace_back(id, k);
+      }
+  }
+};
+
+struct RunArgs {
+  const TensorTable* tt = nullptr;
+  const std::vector<Op>* ops = nullptr;
+  const std::vector<std::vector<int>>* barriers = nullptr;  // nullable
+  const std::vector<cudaEvent_t>* events = nullptr;         // per group
+  int skip_group = -1;                                       // fault injection
+  int S = 0;
+  float lora_scale = 1.f;
+  const void* akey = nullptr;
+  uint64_t gen = 0;
+  Recorder* rec = nullptr;
+  void* nccl = nullptr;  // ncclComm_t for TP (nullable)
+};
+
+// Enqueue the forward for one prompt on exec.compute (tokens already in exec.tok).
+void run_forward(Exec& ex, const RunArgs& a);
+
+// NUMA: bind the calling thread to the CPUs local to `device` (restored by the guard).
+struct NumaGuard {
+  bool active = false;
+  unsigned char saved[128];
+  explicit NumaGuard(int device);
+  ~NumaGuard();
+};
+
+}  // namespace tidal

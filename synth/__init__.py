@@ -305,3 +305,63 @@ def prompt_fast(cfg: ModelConfig, n_tokens: int, seed: int) -> np.ndarray:
     out = np.empty(n_tokens, dtype=np.int32)
     _lib().synth_prompt(seed, cfg.vocab, n_tokens, out.ctypes.data)
     return out
+
+
+# ----------------------------------------------------------------------------
+# Tensor-parallel shards: every shard is a slice of the
+# UNSHARDED tensor, so the weights are identical at every world size.
+#   column-parallel (rows split): q, k, v, gate, up, embed, lm_head
+#   row-parallel (columns split): o, down;   norms replicated
+#   adapters (A14): q/k/v/gate/up -> A whole, B rows split;
+#                   o/down        -> A columns split, B whole
+# ----------------------------------------------------------------------------
+def _target_of(name: str) -> Optional[str]:
+    for t in TARGETS:
+        if f".{t}_proj." in name:
+            return t
+    return None
+
+
+def shard_block(spec: TensorSpec, world: int, rank: int) -> Tuple[int, int, int, int]:
+    """(row0, nrows, col0, ncols) of this rank's slice of ``spec``."""
+    if len(spec.shape) == 1:
+        return 0, 1, 0, spec.shape[0]
+    R, Cc = spec.shape
+    if world == 1:
+        return 0, R, 0, Cc
+    t = _target_of(spec.name)
+    is_a, is_b = spec.name.endswith("lora_A"), spec.name.endswith("lora_B")
+    if t in ("o", "down"):
+        if is_b:
+            return 0, R, 0, Cc
+        return 0, R, rank * Cc // world, Cc // world           # W [d, in] / A [r, in]
+    if is_a:
+        return 0, R, 0, Cc                                       # column-parallel A whole
+    return rank * R // world, R // world, 0, Cc                  # W / B / embed / head rows
+
+
+def model_inputs(cfg: ModelConfig, seed: int, world: int = 1, rank: int = 0):
+    """[(name, nbytes, None)] + fill(dst, nbytes, index) for a tidal_model whose
+    tensors are generated straight into the library's pinned pool."""
+    specs = base_tensors(cfg)
+    blocks = [shard_block(s, world, rank) for s in specs]
+    tensors = [(s.name, 2 * b[1] * b[3], None) for s, b in zip(specs, blocks)]
+
+    def fill(dst: int, nbytes: int, index: int) -> None:
+        s, (r0, nr, c0, nc) = specs[index], blocks[index]
+        assert nbytes == 2 * nr * nc
+        fill_bf16(s, NS_BASE, seed, dst, row0=r0, nrows=nr, col0=c0, ncols=nc)
+    return tensors, fill
+
+
+def adapter_fill(cfg: ModelConfig, rank: int, seed: int, slots, buf: np.ndarray,
+                 target_mask: int = 0x7F, world: int = 1, tp_rank: int = 0) -> None:
+    """Write the seeded adapter into ``buf`` (uint8 view of a pinned buffer)
+    at the canonical slots returned by tidal_adapter_layout."""
+    specs = {s.name: s for s in adapter_tensors(cfg, rank, target_mask)}
+    base = buf.ctypes.data
+    for sl in slots:
+        s = specs[sl["name"]]
+        r0, nr, c0, nc = shard_block(s, world, tp_rank)
+        assert sl["bytes"] == 2 * nr * nc, sl
+        fill_bf16(s, NS_ADAPTER, seed, base + sl["offset"], row0=r0, nrows=nr, col0=c0, ncols=nc)

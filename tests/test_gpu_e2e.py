@@ -1,0 +1,180 @@
+"""End-to-end parity of tidal_invoke_prefill against the oracle (GPU).
+
+Same seeded weights, adapter and prompt on both sides (synth); the GPU result
+must give the oracle's first token (margin rule, reading A6) and
+last-position logits within max-abs 2e-2 (BASELINE.json north_star).  Also:
+the traced first run reproduces the planner's trace byte for byte; poisoning
+the streaming arena with NaN before every invoke changes nothing (so every
+op ran after its weights landed); dropping one barrier while delaying that
+group's copy is detected; the template bytes never change (copy-on-write).
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import forward as F
+from oracle import plan as P
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+TOL = 2e-2
+MARGIN = 2 * TOL
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_06421_b200 import build
+    build.build()
+    from paper_2503_06421_b200 import tidal
+    tidal.lib()
+    return tidal
+
+
+def cfg_dict(cfg):
+    return dict(n_layers=cfg.n_layers, d_model=cfg.d_model, n_heads=cfg.n_heads,
+                n_kv_heads=cfg.n_kv_heads, d_ff=cfg.d_ff, vocab=cfg.vocab,
+                rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps,
+                tie_embeddings=cfg.tie_embeddings)
+
+
+class Rig:
+    """One synthetic model + template + (optional) adapter on cuda:0."""
+
+    def __init__(self, T, cfg, seed=0, budget=None, policy=0, max_tokens=512, trace_tokens=None):
+        self.T, self.cfg, self.seed = T, cfg, seed
+        tensors, fill = synth.model_inputs(cfg, seed)
+        self.model = T.Model(cfg_dict(cfg), tensors, f"base:{seed}", fill=fill)
+        tok = trace_tokens if trace_tokens is not None else synth.prompt(cfg, 8, seed)
+        self.trace = T.Trace(self.model, tok, device=0)
+        M = sum(s.nbytes for s in synth.base_tensors(cfg))
+        b = T.U64_MAX if budget is None else int(budget * M)
+        self.tpl = T.Template(self.model, self.trace,
+                              T.template_opts(resident_bytes=b, group_policy=policy,
+                                              max_transfers=5, max_tokens=max_tokens, device=0))
+        self.w = F.synth_weights(cfg, seed)
+
+    def adapter(self, rank, seed, mask=0x7F, scale=1.0):
+        slots, total = self.tpl.adapter_layout(rank, mask)
+        buf = self.T.PinnedBuffer(total)
+        synth.adapter_fill(self.cfg, rank, seed, slots, buf.view(), mask)
+        return self.T.Adapter(self.tpl, rank, scale, mask, buf, total, f"adapter:{seed}")
+
+
+def check(res, ref):
+    tok, logits, _ = res
+    err = float(np.abs(logits - ref["logits"]).max())
+    assert err <= TOL, err
+    top = np.sort(ref["logits"])[-2:]
+    if top[1] - top[0] > MARGIN:
+        assert tok == ref["token"]
+    assert ref["logits"][tok] >= ref["logits"].max() - MARGIN
+    return err
+
+
+@pytest.fixture(scope="module")
+def tiny(T):
+    return Rig(T, synth.config("tiny"), seed=0, budget=0.5)
+
+
+def test_traced_first_run_matches_planner_and_oracle(T, tiny):
+    cfg = tiny.cfg
+    shape = P.Shape(cfg.n_layers, cfg.d_model, cfg.n_heads, cfg.n_kv_heads, cfg.d_ff, cfg.vocab)
+    assert tiny.trace.dump() == P.trace_dump(P.trace(shape, "base:0"))
+    tok = synth.prompt(cfg, 8, 0)
+    ref = F.forward(cfg, tiny.w, tok)
+    check((tiny.trace.token, tiny.trace.logits, None), ref)
+
+
+@pytest.mark.parametrize("S", [1, 5, 16, 130, 511])
+@pytest.mark.parametrize("rank", [0, 8, 16])
+def test_tiny_invoke_matches_oracle(T, tiny, S, rank):
+    cfg = tiny.cfg
+    tok = synth.prompt(cfg, S, 100 + S)
+    a = tiny.adapter(rank, 3) if rank else None
+    aw = F.synth_adapter(cfg, rank, 3) if rank else None
+    ref = F.forward(cfg, tiny.w, tok, aw, 0x7F if rank else 0, 1.0)
+    check(tiny.tpl.invoke(tok, a), ref)
+
+
+@pytest.mark.parametrize("budget", [0.0, 0.3, 1.0])
+@pytest.mark.parametrize("policy", [0, 1, 2])
+def test_residency_and_policies_poisoned(T, budget, policy):
+    cfg = synth.config("tiny")
+    rig = Rig(T, cfg, seed=1, budget=budget, policy=policy)
+    rig.tpl.set_debug(T.DEBUG_POISON)
+    tok = synth.prompt(cfg, 16, 9)
+    a = rig.adapter(16, 4, mask=0x7F, scale=0.5)
+    ref = F.forward(cfg, rig.w, tok, F.synth_adapter(cfg, 16, 4), 0x7F, 0.5)
+    c0 = rig.tpl.checksum()
+    for _ in range(3):
+        check(rig.tpl.invoke(tok, a), ref)
+    assert rig.tpl.checksum() == c0                      # template bytes never written
+
+
+def test_partial_targets_and_scale(T, tiny):
+    cfg = tiny.cfg
+    tok = synth.prompt(cfg, 33, 5)
+    for mask in (0x07, 0x08, 0x30, 0x40, 0x31):
+        a = tiny.adapter(8, 6, mask=mask, scale=2.0)
+        ref = F.forward(cfg, tiny.w, tok, F.synth_adapter(cfg, 8, 6, mask), mask, 2.0)
+        check(tiny.tpl.invoke(tok, a), ref)
+
+
+def test_fault_injection_detected(T):
+    """Drop the barrier of one streamed group and delay its copy: with the
+    arena poisoned, the op reads NaN and the invoke fails."""
+    cfg = synth.config("tiny")
+    rig = Rig(T, cfg, seed=2, budget=0.0, policy=2)
+    tok = synth.prompt(cfg, 16, 2)
+    n_groups = sum(l.startswith("GROUP") for l in rig.tpl.plan_dump().splitlines())
+    detected = 0
+    trials = list(range(n_groups))
+    for g in trials:
+        rig.tpl.set_debug(T.DEBUG_POISON | T.DEBUG_SKIP_BARRIER, g)
+        try:
+            tk, logits, _ = rig.tpl.invoke(tok)
+            bad = not np.all(np.isfinite(logits))
+        except T.TidalError as e:
+            bad = e.code == 9
+        detected += bad
+    rig.tpl.set_debug(0)
+    assert detected == len(trials)
+    ref = F.forward(cfg, rig.w, tok)
+    check(rig.tpl.invoke(tok), ref)
+
+
+def test_resize_template(T):
+    cfg = synth.config("tiny")
+    rig = Rig(T, cfg, seed=3, budget=0.0)
+    tok = synth.prompt(cfg, 24, 3)
+    ref = F.forward(cfg, rig.w, tok)
+    rig.tpl.set_debug(T.DEBUG_POISON)
+    for b in (0, 2_000_000, T.U64_MAX, 1_000_000):
+        rig.tpl.resize(T.template_opts(resident_bytes=b))
+        check(rig.tpl.invoke(tok), ref)
+
+
+@pytest.mark.parametrize("cfg", [
+    synth.ModelConfig("gqa128", 2, 512, 4, 2, 1376, 2048, rope_theta=500000.0),
+    synth.ModelConfig("tied", 2, 256, 4, 1, 512, 1000, tie_embeddings=True),
+])
+def test_other_shapes(T, cfg):
+    rig = Rig(T, cfg, seed=4, budget=0.4)
+    rig.tpl.set_debug(T.DEBUG_POISON)
+    tok = synth.prompt(cfg, 300, 4)
+    a = rig.adapter(16, 2)
+    ref = F.forward(cfg, rig.w, tok, F.synth_adapter(cfg, 16, 2), 0x7F, 1.0)
+    check(rig.tpl.invoke(tok, a), ref)
+
+
+def test_serial_mode_same_result(T, tiny):
+    tok = synth.prompt(tiny.cfg, 16, 0)
+    t0, l0, _ = tiny.tpl.invoke(tok)
+    tiny.tpl.set_debug(T.DEBUG_SERIAL)
+    t1, l1, st = tiny.tpl.invoke(tok)
+    tiny.tpl.set_debug(0)
+    assert t0 == t1 and np.array_equal(l0, l1)
+    assert st["compute_first_ms"] >= st["h2d_last_ms"] - 1e-3

@@ -1,0 +1,201 @@
+"""Per-op parity on the GPU: each sm_100a kernel through the C-ABI
+(include/tidal_kernels.h) against the oracle's definition of the same op on
+the same seeded bf16 inputs (oracle/forward.py: rmsnorm, rope, causal
+attention, linear + LoRA, silu).  Sizes span several tiles plus ragged tails.
+
+Tolerances: outputs stored in bf16 carry one rounding (rel 2^-9) plus fp32
+accumulation-order noise; we allow |err| <= 2^-7 * max|ref| + 1e-3 for bf16
+outputs and 1e-4 relative to max|ref| for the fp32 residual output.
+"""
+import math
+
+import numpy as np
+import pytest
+
+import synth
+from oracle import forward as F
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_06421_b200 import build
+    build.build()
+    from paper_2503_06421_b200 import tidal
+    tidal.lib()
+    return tidal
+
+
+def _bf(rng, shape, scale=1.0):
+    x = (rng.standard_normal(shape) * scale).astype(np.float32)
+    return synth.bf16_bits_to_f32(synth.f32_to_bf16_bits(x)).reshape(shape)
+
+
+def _dev(a):
+    """float32 array holding bf16 values -> torch bf16 cuda tensor."""
+    return torch.from_numpy(np.ascontiguousarray(a)).to(torch.bfloat16).cuda()
+
+
+def _host(t):
+    return t.float().cpu().numpy()
+
+
+def _close_bf16(out, ref):
+    tol = 2.0 ** -7 * np.abs(ref).max() + 1e-3
+    err = np.abs(out - ref).max()
+    assert err <= tol, (err, tol)
+
+
+@pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 384, 320), (77, 256, 688), (512, 768, 1024)])
+def test_gemm_store(T, M, N, K):
+    rng = np.random.default_rng(M + N + K)
+    A, W = _bf(rng, (M, K)), _bf(rng, (N, K), 1 / math.sqrt(K))
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    T.k_gemm(0, _dev(A), [_dev(W)], [N], out, N, M, K)
+    _close_bf16(_host(out), F.linear(A, W, None, 1.0))
+
+
+@pytest.mark.parametrize("M,N,K", [(256, 512, 512), (130, 256, 1376)])
+def test_gemm_residual_fp32(T, M, N, K):
+    rng = np.random.default_rng(7)
+    A, W = _bf(rng, (M, K)), _bf(rng, (N, K), 1 / math.sqrt(K))
+    X0 = rng.standard_normal((M, N)).astype(np.float32)
+    X = torch.from_numpy(X0.copy()).cuda()
+    T.k_gemm(3, _dev(A), [_dev(W)], [N], X, N, M, K)
+    ref = X0 + F.linear(A, W, None, 1.0)
+    assert np.abs(X.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("r", [8, 16, 64])
+def test_gemm_lora_k_extension(T, r):
+    rng = np.random.default_rng(r)
+    M, N, K = 200, 512, 256
+    A, W = _bf(rng, (M, K)), _bf(rng, (N, K), 1 / math.sqrt(K))
+    Tm, B = _bf(rng, (M, r)), _bf(rng, (N, r), 0.3)
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    T.k_gemm(0, _dev(A), [_dev(W)], [N], out, N, M, K, [_dev(Tm)], [_dev(B)], r)
+    _close_bf16(_host(out), A @ W.T + Tm @ B.T)
+
+
+@pytest.mark.parametrize("Fd,lora", [(688, False), (688, True), (1024, True)])
+def test_gemm_silu_gate_up(T, Fd, lora):
+    rng = np.random.default_rng(Fd)
+    M, K, r = 150, 256, 16
+    A = _bf(rng, (M, K))
+    Wg, Wu = _bf(rng, (Fd, K), 1 / math.sqrt(K)), _bf(rng, (Fd, K), 1 / math.sqrt(K))
+    out = torch.zeros(M, Fd, dtype=torch.bfloat16, device="cuda")
+    g, u = A @ Wg.T, A @ Wu.T
+    if lora:
+        Tg, Tu = _bf(rng, (M, r)), _bf(rng, (M, r))
+        Bg, Bu = _bf(rng, (Fd, r), 0.2), _bf(rng, (Fd, r), 0.2)
+        T.k_gemm(2, _dev(A), [_dev(Wg), _dev(Wu)], [Fd], out, Fd, M, K,
+                 [_dev(Tg), _dev(Tu)], [_dev(Bg), _dev(Bu)], r)
+        g, u = g + Tg @ Bg.T, u + Tu @ Bu.T
+    else:
+        T.k_gemm(2, _dev(A), [_dev(Wg), _dev(Wu)], [Fd], out, Fd, M, K)
+    _close_bf16(_host(out), F.silu(g) * u)
+
+
+@pytest.mark.parametrize("hd,H,KV", [(64, 4, 4), (128, 4, 2)])
+def test_gemm_qkv_rope(T, hd, H, KV):
+    rng = np.random.default_rng(hd)
+    M, K = 333, 512
+    A = _bf(rng, (M, K))
+    Ws = [_bf(rng, (H * hd, K), 1 / math.sqrt(K)), _bf(rng, (KV * hd, K), 1 / math.sqrt(K)),
+          _bf(rng, (KV * hd, K), 1 / math.sqrt(K))]
+    ld = (H + 2 * KV) * hd
+    cos, sin = F.rope_cos_sin(M, hd, 1e4, np.float64)
+    cs = np.stack([cos, sin], axis=-1).astype(np.float32)
+    rope = torch.from_numpy(cs).cuda()
+    out = torch.zeros(M, ld, dtype=torch.bfloat16, device="cuda")
+    T.k_gemm(1, _dev(A), [_dev(w) for w in Ws], [H * hd, KV * hd, KV * hd], out, ld, M, K,
+             rope=rope, head_dim=hd)
+    c32, s32 = F.rope_cos_sin(M, hd, 1e4, np.float32)
+    q = F.rope((A @ Ws[0].T).reshape(M, H, hd), c32, s32).reshape(M, -1)
+    k = F.rope((A @ Ws[1].T).reshape(M, KV, hd), c32, s32).reshape(M, -1)
+    v = A @ Ws[2].T
+    _close_bf16(_host(out), np.concatenate([q, k, v], axis=1))
+
+
+@pytest.mark.parametrize("S,H,KV,hd", [(1, 4, 2, 128), (67, 4, 2, 128), (256, 2, 2, 64),
+                                        (200, 8, 2, 64), (513, 2, 1, 128)])
+def test_attention_causal_gqa(T, S, H, KV, hd):
+    rng = np.random.default_rng(S + hd)
+    qkv = _bf(rng, (S, (H + 2 * KV) * hd))
+    O = torch.zeros(S, H * hd, dtype=torch.bfloat16, device="cuda")
+    T.k_attention(_dev(qkv), O, S, H, KV, hd)
+    q = qkv[:, :H * hd].reshape(S, H, hd)
+    k = qkv[:, H * hd:(H + KV) * hd].reshape(S, KV, hd)
+    v = qkv[:, (H + KV) * hd:].reshape(S, KV, hd)
+    ref = F.causal_attention(q, k, v)
+    err = np.abs(_host(O) - ref).max()
+    assert err <= 2e-2, err
+
+
+@pytest.mark.parametrize("S,d", [(1, 256), (37, 5120), (16, 4096)])
+def test_rmsnorm(T, S, d):
+    rng = np.random.default_rng(d)
+    X = rng.standard_normal((S, d)).astype(np.float32)
+    g = _bf(rng, (d,), 0.1) + 1.0
+    g = synth.bf16_bits_to_f32(synth.f32_to_bf16_bits(g))
+    Y = torch.zeros(S, d, dtype=torch.bfloat16, device="cuda")
+    T.k_rmsnorm(torch.from_numpy(X).cuda(), _dev(g), Y, S, d, 1e-5)
+    _close_bf16(_host(Y), F.rmsnorm(X, g, 1e-5))
+
+
+def test_embed_and_vocab_shard(T):
+    rng = np.random.default_rng(3)
+    V, d, S = 64, 256, 20
+    E = _bf(rng, (V, d))
+    tok = rng.integers(0, V, S).astype(np.int32)
+    X = torch.zeros(S, d, device="cuda")
+    T.k_embed(torch.from_numpy(tok).cuda(), _dev(E), X, S, d, 0, V)
+    assert np.array_equal(X.cpu().numpy(), E[tok])
+    Xs = torch.zeros(S, d, device="cuda")
+    T.k_embed(torch.from_numpy(tok).cuda(), _dev(E[16:32]), Xs, S, d, 16, 16)
+    ref = np.where(((tok >= 16) & (tok < 32))[:, None], E[tok], 0)
+    assert np.array_equal(Xs.cpu().numpy(), ref)
+
+
+@pytest.mark.parametrize("M,K,r", [(64, 256, 8), (300, 5120, 16), (77, 688, 64)])
+def test_lora_shrink(T, M, K, r):
+    rng = np.random.default_rng(K)
+    X, A = _bf(rng, (M, K)), _bf(rng, (r, K), 1 / math.sqrt(K))
+    out = torch.zeros(M, r, dtype=torch.bfloat16, device="cuda")
+    T.k_lora_shrink(_dev(X), M, K, _dev(A), out, r, 0.5)
+    _close_bf16(_host(out), 0.5 * (X @ A.T))
+
+
+@pytest.mark.parametrize("V,d", [(1000, 256), (32000, 5120)])
+def test_head_logits_and_argmax(T, V, d):
+    rng = np.random.default_rng(V)
+    x = rng.standard_normal(d).astype(np.float32)
+    g = synth.bf16_bits_to_f32(synth.f32_to_bf16_bits(1 + 0.05 * rng.standard_normal(d).astype(np.float32)))
+    W = _bf(rng, (V, d), 1 / math.sqrt(d))
+    logits = torch.zeros(V, device="cuda")
+    key = torch.zeros(1, dtype=torch.int64, device="cuda")
+    T.k_head(torch.from_numpy(x).cuda(), _dev(g), _dev(W), V, d, 1e-5, logits, key)
+    ref = W @ F.rmsnorm(x[None], g, 1e-5)[0]
+    out = logits.cpu().numpy()
+    assert np.abs(out - ref).max() <= 1e-4 * np.abs(ref).max() + 1e-5
+    k = int(key.cpu().numpy()[0]) & 0xFFFFFFFFFFFFFFFF
+    tok = 0xFFFFFFFF - (k & 0xFFFFFFFF)
+    assert tok == int(np.argmax(out))                 # exact argmax of the kernel's own logits
+
+
+def test_head_argmax_ties_lowest_index(T):
+    V, d = 512, 256
+    W = np.zeros((V, d), np.float32)
+    W[[7, 100, 300], 0] = 1.0                          # three equal maxima
+    x = np.zeros(d, np.float32)
+    x[0] = 1.0
+    g = np.ones(d, np.float32)
+    logits = torch.zeros(V, device="cuda")
+    key = torch.zeros(1, dtype=torch.int64, device="cuda")
+    T.k_head(torch.from_numpy(x).cuda(), _dev(g), _dev(W), V, d, 1e-5, logits, key)
+    k = int(key.cpu().numpy()[0]) & 0xFFFFFFFFFFFFFFFF
+    assert 0xFFFFFFFF - (k & 0xFFFFFFFF) == 7
