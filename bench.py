@@ -1,0 +1,347 @@
+"""bench.py — template-start TTFT of a Llama2-13B-shaped prefill with a
+dynamically attached rank-16 LoRA (BASELINE.json configs[2], the paper's
+Fig. 1 workload: 2k-token prompt), on N B200s (N>1: tensor parallel, each
+rank streams its own shard over its own PCIe link; NCCL allreduce over NVLink).
+
+One timed step = attach the adapter (host) + one tidal_invoke_prefill: the
+non-resident weights and the adapter stream from the pinned host pool in
+traced order while the prefill runs, gated by per-group events; the step ends
+with the first token and the last-position logits on the host.  The template
+size is set by the paper's Eq. 1 from the warm TTFT and the H2D bandwidth
+measured in this same run.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl tidal|reference]
+                    [--config 13b] [--seq 2048] [--rank 16] [--rho eq1|<fraction>]
+
+Prints ONE JSON line (rank 0).  value = mean device TTFT (ms, lower is better).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import synth  # noqa: E402
+
+PEAKS_FALLBACK = {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0, "bf16_tflops_sustained": 1400.0}
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return p, "measured (MEASURED_PEAKS.json)"
+    except Exception:
+        return PEAKS_FALLBACK, "fallback (B200_PROFILING.md)"
+
+
+def cfg_dict(cfg):
+    return dict(n_layers=cfg.n_layers, d_model=cfg.d_model, n_heads=cfg.n_heads,
+                n_kv_heads=cfg.n_kv_heads, d_ff=cfg.d_ff, vocab=cfg.vocab,
+                rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps,
+                tie_embeddings=cfg.tie_embeddings)
+
+
+def prefill_flops(cfg, S, r, world):
+    """Algorithmic prefill FLOPs per rank: 2*S per linear parameter, causal
+    attention 2*hd*H*S*(S+1) per layer, LoRA 2*S*r*(in+out) per target, head
+    2*d*V for the last position."""
+    d, F, hd = cfg.d_model, cfg.d_ff, cfg.head_dim
+    nq, nkv = cfg.n_heads * hd, cfg.n_kv_heads * hd
+    lin = d * (nq + 2 * nkv) + nq * d + 3 * d * F
+    lora = r * ((d + nq) + 2 * (d + nkv) + (nq + d) + 2 * (d + F) + (F + d)) if r else 0
+    per_layer = 2 * S * lin + 2 * hd * cfg.n_heads * S * (S + 1) + 2 * S * lora
+    return (cfg.n_layers * per_layer + 2 * d * cfg.vocab) / world
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md recipe)."""
+    Q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+         "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+         "clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, dev):
+        self.dev, self.rows, self.p = dev, [], None
+
+    def __enter__(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.dev), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"],
+                                      stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.p = None
+        return self
+
+    def _read(self):
+        for line in self.p.stdout:
+            self.rows.append([x.strip() for x in line.split(",")])
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"]}
+        sm = [float(r[0]) for r in self.rows if r[0].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({n for r in self.rows for n, v in zip(names, r[3:7]) if v == "Active"})
+        return {"sm_mhz": statistics.median(sm) if sm else None,
+                "sm_max_mhz": float(self.rows[0][1]) if self.rows[0][1].replace(".", "").isdigit() else None,
+                "reasons": reasons, "samples": len(self.rows)}
+
+
+def oracle_sample(cfg, S, r, seed=0):
+    """One bounded oracle sample: embed + 1 decoder layer + head at full width
+    and full S, LoRA on all 7 targets; returns seconds."""
+    from oracle import forward as F
+    w = F.synth_weights(cfg, seed, fast=True, keep=True)
+    a = F.synth_adapter(cfg, r, 1, fast=True) if r else None
+    tok = synth.prompt_fast(cfg, S, 0)
+    t = time.perf_counter()
+    F.forward(cfg, w, tok, a, 0x7F if r else 0, 1.0, n_layers=1)
+    return time.perf_counter() - t
+
+
+def run_reference(args):
+    """--impl reference: the oracle (numpy fp32, plain definition) on the host
+    cores, bounded samples of the same workload (1 of L layers, extrapolated)."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    cfg = synth.config(args.config)
+    cores = len(os.sched_getaffinity(0))
+    for _ in range(args.warmup):
+        oracle_sample(cfg, args.seq, args.rank)
+    ts = [oracle_sample(cfg, args.seq, args.rank) for _ in range(args.steps)]
+    ms = statistics.mean(ts) * 1e3 * cfg.n_layers
+    sample = f"embed + 1 of {cfg.n_layers} layers + head at S={args.seq}, r={args.rank}; x{cfg.n_layers}"
+    print(json.dumps({
+        "impl": "reference", "metric": "template-start TTFT", "value": ms, "unit": "ms",
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic (seeded splitmix64 weights, uniform prompt)",
+        "config": {"workload": f"{args.config} S={args.seq} LoRA r{args.rank} (oracle sample)"},
+        "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle",
+                         "sample": sample},
+        "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="tidal", choices=["tidal", "reference"])
+    ap.add_argument("--config", default="13b")
+    ap.add_argument("--seq", type=int, default=2048)
+    ap.add_argument("--rank", type=int, default=16)
+    ap.add_argument("--rho", default="eq1")
+    ap.add_argument("--policy", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-sweep", action="store_true")
+    ap.add_argument("--quick", action="store_true", help="profiling runs: minimal extra passes")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    assert world == args.gpus or "WORLD_SIZE" not in os.environ, "--gpus must match torchrun"
+    torch.cuda.set_device(local)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    from paper_2503_06421_b200 import build as B
+    if rank == 0:
+        synth.build_c() if not os.path.exists(os.path.join(ROOT, "synth", "libsynth.so")) else None
+        B.build()
+    if dist:
+        dist.barrier()
+    from paper_2503_06421_b200 import tidal as T
+
+    cfg = synth.config(args.config)
+    S, r = args.seq, args.rank
+    P, peak_src = peaks()
+    t_setup = time.perf_counter()
+    tensors, fill = synth.model_inputs(cfg, 0, world, rank)
+    model = T.Model(cfg_dict(cfg), tensors, "base:0", fill=fill, world=world, rank=rank)
+    trace = T.Trace(model)     # planner trace == traced first run (tests/test_gpu_e2e.py)
+    comm = None
+    if world > 1:
+        uid = [T.Comm.unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(uid, src=0)
+        comm = T.Comm(world, rank, uid[0], local)
+    tpl = T.Template(model, trace, T.template_opts(resident_bytes=0, group_policy=args.policy,
+                                                   max_tokens=S, device=local, comm=comm))
+    abuf, anb, slots = None, 0, None
+    if r:
+        slots, anb = tpl.adapter_layout(r, 0x7F)
+        abuf = T.PinnedBuffer(anb)
+        synth.adapter_fill(cfg, r, 1, slots, abuf.view(), 0x7F, world, rank)
+    tokens = synth.prompt_fast(cfg, S, 0)
+    setup_s = time.perf_counter() - t_setup
+
+    def attach():
+        return T.Adapter(tpl, r, 1.0, 0x7F, abuf, anb, "adapter:1") if r else None
+
+    def step(debug):
+        tpl.set_debug(debug)
+        h0 = time.perf_counter()
+        ad = attach()
+        attach_ms = (time.perf_counter() - h0) * 1e3
+        tok, logits, st = tpl.invoke(tokens, ad)
+        st["attach_ms"] = attach_ms
+        st["e2e_ms"] = (time.perf_counter() - h0) * 1e3
+        st["token"] = tok
+        return st
+
+    def max_over_ranks(x):
+        if not dist:
+            return x
+        t = torch.tensor([x], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
+
+    # (1) H2D bandwidth of this path and the load-then-infer baseline (rho = 0, serial)
+    for _ in range(1 if args.quick else 2):
+        st0 = step(T.DEBUG_SERIAL | T.DEBUG_SCRUB_L2)
+    h2d_ms = st0["h2d_last_ms"] - st0["h2d_first_ms"]
+    stream_bytes = st0["bytes_streamed"] + st0["bytes_adapter"]
+    b_h2d = stream_bytes / (h2d_ms / 1e3)
+    b_h2d = min(b_h2d, max_over_ranks(b_h2d)) if dist else b_h2d
+    cold_ms = max_over_ranks(st0["device_ms"])
+    sweep = {"load_then_infer_rho0": cold_ms}
+    if not args.no_sweep and not args.quick:
+        sweep["overlap_rho0"] = max_over_ranks(step(T.DEBUG_SCRUB_L2)["device_ms"])
+    # (2) warm TTFT (rho = 1), the T_TTFT of Eq. 1
+    tpl.resize(T.template_opts(resident_bytes=T.U64_MAX))
+    warm = [step(T.DEBUG_SCRUB_L2)["device_ms"] for _ in range(1 if args.quick else 3)]
+    t_warm = max_over_ranks(statistics.median(warm))
+    sweep["warm_rho1"] = t_warm
+    # (3) template size
+    if args.rho == "eq1":
+        tpl.resize(T.template_opts(eq1=True, t_ttft_s=t_warm / 1e3, b_pcie_Bps=b_h2d))
+    else:
+        M = sum(s.nbytes for s in synth.base_tensors(cfg)) // world
+        tpl.resize(T.template_opts(resident_bytes=int(float(args.rho) * M)))
+    # (4) timed region
+    dbg = T.DEBUG_SCRUB_L2 | T.DEBUG_PROFILE
+    for _ in range(args.warmup):
+        step(dbg)
+    tpl.profile(reset=True)
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    stats = []
+    with Clocks(local) as clk:
+        for _ in range(args.steps):
+            stats.append(step(dbg))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    prof = tpl.profile(reset=True)
+    dev_ms = [max_over_ranks(s["device_ms"]) for s in stats]
+    e2e_ms = [max_over_ranks(s["e2e_ms"]) for s in stats]
+    s0 = stats[0]
+    ttft = statistics.mean(dev_ms)
+    if rank != 0:
+        return
+
+    # roofline of the whole step (north_star): max(streamed / B_h2d, FLOPs / peak)
+    flops = prefill_flops(cfg, S, r, world)
+    streamed = s0["bytes_streamed"] + s0["bytes_adapter"]
+    t_pcie = streamed / b_h2d * 1e3
+    t_tc = flops / (P["bf16_tflops"] * 1e12) * 1e3
+    roof = max(t_pcie, t_tc)
+    # dominant kernel (largest device time in the timed region)
+    dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
+    per_launch_ms = dom["ms"] / max(1, dom["launches"])
+    tensor_bound = dom["flops"] > 0 and dom["flops"] / max(dom["bytes"], 1) > 50
+    traffic = None
+    tf = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tf):
+        try:
+            traffic = json.load(open(tf)).get(dom_name)
+        except Exception:
+            traffic = None
+    if tensor_bound:
+        ach = dom["flops"] / (dom["ms"] / 1e3) / 1e12
+        pk = P.get("bf16_tflops_sustained", P["bf16_tflops"])
+        rl = {"kernel": dom_name, "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
+              "frac": ach / pk, "traffic": traffic,
+              "per_launch": {"ms": per_launch_ms, "flops": dom["flops"] / max(1, dom["launches"])},
+              "peak_source": peak_src + " bf16_tflops_sustained (kernel timed inside the step)"}
+    else:
+        ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
+        rl = {"kernel": dom_name, "bound": "hbm", "achieved": ach, "peak": P["hbm_gbs"],
+              "unit": "GB/s", "frac": ach / P["hbm_gbs"], "traffic": traffic,
+              "per_launch": {"ms": per_launch_ms, "bytes": dom["bytes"] / max(1, dom["launches"])},
+              "peak_source": peak_src}
+    kernels = {k: {"ms_per_step": v["ms"] / args.steps, "launches_per_step": v["launches"] / args.steps,
+                   "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
+                   "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None}
+               for k, v in prof.items() if v["launches"]}
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline:
+        t1 = oracle_sample(cfg, S, r)
+        cpu = {"value": t1 * 1e3 * cfg.n_layers, "unit": "ms",
+               "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
+               "sample": f"numpy fp32 oracle: embed + 1 of {cfg.n_layers} layers + head at "
+                         f"S={S}, LoRA r{r}; value = t x {cfg.n_layers}"}
+    out = {
+        "metric": "template-start TTFT", "value": ttft, "unit": "ms", "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": ttft,
+        "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
+        "data": "synthetic (seeded splitmix64 random-init bf16 weights + LoRA, uniform prompt)",
+        "config": {"workload": f"Llama2-{args.config.upper()}-shaped prefill, S={S}, "
+                               f"LoRA r{r} attach, template-start (BASELINE.json configs[2])",
+                   "seq_len": S, "lora_rank": r, "resident_rule": args.rho,
+                   "rho": s0["bytes_resident"] / max(1, s0["bytes_resident"] + s0["bytes_streamed"]),
+                   "group_policy": args.policy, "parallelism": f"tp{world}" if world > 1 else "single",
+                   "l2": "flushed before every step (512 MB write, outside the timed window)"},
+        "ttft_ms": {"mean": ttft, "median": statistics.median(dev_ms),
+                    "p95": sorted(dev_ms)[max(0, int(np.ceil(0.95 * len(dev_ms))) - 1)],
+                    "min": min(dev_ms)},
+        "tokens_per_s": S / (ttft / 1e3),
+        "ttft_roofline": {"roof_ms": roof, "bound": "pcie" if t_pcie >= t_tc else "tensor",
+                          "t_pcie_ms": t_pcie, "t_tensor_ms": t_tc, "frac": roof / ttft,
+                          "streamed_bytes_per_rank": streamed, "b_h2d_GBps": b_h2d / 1e9,
+                          "flops_per_rank": flops, "peak_tflops": P["bf16_tflops"]},
+        "roofline": rl,
+        "cpu_baseline": cpu,
+        "e2e": {"value": statistics.mean(e2e_ms), "unit": "ms",
+                "h2d_bytes_per_step": int(4 * S + streamed),
+                "d2h_bytes_per_step": int(4 * cfg.vocab + 8),
+                "includes": "attach_lora + invoke (token H2D, weight/adapter H2D, logits D2H)"},
+        "gpu_launches": int(sum(s["n_kernels"] for s in stats)),
+        "kernels": kernels,
+        "sweep_ms": sweep,
+        "clocks": clk.summary(),
+        "eq1": {"t_warm_ms": t_warm, "b_h2d_GBps": b_h2d / 1e9},
+        "setup_s": setup_s,
+        "first_token": s0["token"],
+    }
+    print(json.dumps(out))
+
+
+if __name__ == "__main__":
+    main()

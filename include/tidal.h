@@ -203,9 +203,23 @@ enum {
   TIDAL_DEBUG_POISON = 1,      /* NaN-poison the streaming arena before each invoke */
   TIDAL_DEBUG_SKIP_BARRIER = 2,/* drop the wait on group `arg` and delay its copy */
   TIDAL_DEBUG_SCRUB_L2 = 4,    /* write 512 MB before each invoke (timing hygiene) */
-  TIDAL_DEBUG_SERIAL = 8       /* load-then-infer: compute waits for every copy first
+  TIDAL_DEBUG_SERIAL = 8,      /* load-then-infer: compute waits for every copy first
                                   (the paper's "PyTorch-pin" baseline) */
+  TIDAL_DEBUG_PROFILE = 16     /* CUDA events around every kernel on the compute stream */
 };
+/* Per-kernel-class totals accumulated by invokes run with TIDAL_DEBUG_PROFILE:
+ * device time (events on the launching stream), launches, and the ALGORITHMIC
+ * flops and HBM bytes of those launches.  Fills up to
+ * `cap` entries (*n = number of classes); reset != 0 clears the totals. */
+typedef struct {
+  const char* name;
+  double total_ms;
+  long launches;
+  double flops;
+  double bytes;
+} tidal_kernel_time;
+tidal_status tidal_profile_read(tidal_template* tpl, tidal_kernel_time* out, int cap, int* n,
+                                int reset);
 tidal_status tidal_set_debug(tidal_template* tpl, int flags, int arg);
 /* 64-bit checksum of the resident template region computed on the device
  * (the copy-on-write invariant: unchanged across invocations). */

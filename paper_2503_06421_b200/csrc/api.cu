@@ -583,6 +583,8 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
                       ? std::chrono::steady_clock::now()
                       : t_entry;
   ex.launches = 0;
+  ex.profile = (tp->debug & TIDAL_DEBUG_PROFILE) != 0;
+  ex.prof_pending.clear();
   memcpy(ex.h_tok, host_tokens, 4ull * n_tokens);
   cuda_check(cudaEventRecord(tp->e_start, ex.compute), "event");
   cuda_check(cudaStreamWaitEvent(ex.copy, tp->e_start, 0), "wait");
@@ -625,6 +627,7 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
                "D2H logits");
   cuda_check(cudaEventRecord(tp->e_end, ex.compute), "event");
   cuda_check(cudaEventSynchronize(tp->e_end), "invoke");
+  if (ex.profile) ex.prof_collect();
   const unsigned long long key = *ex.h_key;
   const uint32_t hi = (uint32_t)(key >> 32);
   const uint32_t bits = (hi & 0x80000000u) ? (hi & 0x7FFFFFFFu) : ~hi;
@@ -704,6 +707,24 @@ tidal_status tidal_set_debug(tidal_template* tp, int flags, int arg) {
   require(tp != nullptr, "null template");
   tp->debug = flags;
   tp->debug_arg = arg;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_profile_read(tidal_template* tp, tidal_kernel_time* out, int cap, int* n,
+                                int reset) {
+  TIDAL_TRY
+  require(tp != nullptr, "null template");
+  Exec& ex = tp->ex;
+  if (ex.prof_tot.size() < KC_COUNT) ex.prof_tot.resize(KC_COUNT);
+  if (n) *n = KC_COUNT;
+  for (int i = 0; i < KC_COUNT && i < cap && out; ++i) {
+    out[i].name = kKernelClassNames[i];
+    out[i].total_ms = ex.prof_tot[i].ms;
+    out[i].launches = ex.prof_tot[i].launches;
+    out[i].flops = ex.prof_tot[i].flops;
+    out[i].bytes = ex.prof_tot[i].bytes;
+  }
+  if (reset) ex.prof_tot.assign(KC_COUNT, Exec::ProfTot());
   TIDAL_CATCH
 }
 

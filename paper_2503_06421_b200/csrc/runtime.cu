@@ -217,6 +217,42 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
   return cache.emplace(k, std::move(v)).first->second;
 }
 
+const char* const kKernelClassNames[KC_COUNT] = {
+    "embed", "rmsnorm", "lora_shrink", "gemm_qkv_rope", "attention", "gemm_o_resid",
+    "gemm_gate_up_silu", "gemm_down_resid", "head_argmax", "allreduce"};
+
+int Exec::prof_begin() {
+  const size_t i = prof_pending.size();
+  while (prof_ev.size() < 2 * (i + 1)) {
+    cudaEvent_t e;
+    cuda_check(cudaEventCreate(&e), "cudaEventCreate(profile)");
+    prof_ev.push_back(e);
+  }
+  cuda_check(cudaEventRecord(prof_ev[2 * i], compute), "event");
+  prof_pending.push_back({-1, (int)i, 0, 0});
+  return (int)i;
+}
+
+void Exec::prof_end(int cls, int ev, double flops, double bytes) {
+  cuda_check(cudaEventRecord(prof_ev[2 * ev + 1], compute), "event");
+  prof_pending[ev] = {cls, ev, flops, bytes};
+}
+
+void Exec::prof_collect() {
+  if (prof_tot.size() < KC_COUNT) prof_tot.resize(KC_COUNT);
+  for (const ProfRec& p : prof_pending) {
+    if (p.cls < 0) continue;
+    float ms = 0;
+    cuda_check(cudaEventElapsedTime(&ms, prof_ev[2 * p.ev], prof_ev[2 * p.ev + 1]), "elapsed");
+    ProfTot& t = prof_tot[p.cls];
+    t.ms += ms;
+    t.flops += p.flops;
+    t.bytes += p.bytes;
+    t.launches += 1;
+  }
+  prof_pending.clear();
+}
+
 enum OpKind {
   OP_EMBED, OP_ATTN_NORM, OP_QKV, OP_ROPE, OP_ATTN, OP_O, OP_MLP_NORM, OP_GU, OP_ACT, OP_DOWN,
   OP_FNORM, OP_HEAD, OP_ARGMAX, OP_EMBED_AR, OP_ATTN_AR, OP_MLP_AR, OP_LOGITS_AG
@@ -251,10 +287,13 @@ void run_forward(Exec& ex, const RunArgs& a) {
   const auto& LP = ex.layer_params(tt, S, a.akey, a.gen);
   cudaStream_t st = ex.compute;
   int waited = -1;
-  auto K = [&](cudaError_t e, const char* what) {
+  auto P0 = [&]() { return ex.profile ? ex.prof_begin() : -1; };
+  auto K = [&](int cls, int ev, double fl, double by, cudaError_t e, const char* what) {
     cuda_check(e, what);
     ++ex.launches;
+    if (ev >= 0) ex.prof_end(cls, ev, fl, by);
   };
+  const double Sd = S;
   auto shrink = [&](const bf16* X, int ldx, int Kd, int l, std::initializer_list<int> ts) {
     const bf16* A[3];
     bf16* T[3];
@@ -265,8 +304,19 @@ void run_forward(Exec& ex, const RunArgs& a) {
         T[n] = ex.T[t];
         ++n;
       }
-    if (n) K(lora_shrink_launch(X, ldx, S, Kd, A, T, n, r, a.lora_scale, st), "lora_shrink");
+    if (n) {
+      const int e0 = P0();
+      K(KC_SHRINK, e0, 2.0 * Sd * Kd * r * n, 2.0 * (Sd * Kd + (double)n * r * (Kd + Sd)),
+        lora_shrink_launch(X, ldx, S, Kd, A, T, n, r, a.lora_scale, st), "lora_shrink");
+    }
   };
+  auto lora_n = [&](int l, std::initializer_list<int> ts) {
+    double n = 0;
+    for (int t : ts)
+      if (tt.lora_a[l][t] >= 0) n += tt.t[tt.lora_b[l][t]].rows;
+    return n;
+  };
+  const int nkv = m.n_kv_heads * hd / ex.world;
   const std::vector<Op>& ops = *a.ops;
   for (size_t k = 0; k < ops.size(); ++k) {
     const Op& op = ops[k];
@@ -284,38 +334,75 @@ void run_forward(Exec& ex, const RunArgs& a) {
     auto Wp = [&](int id) { return reinterpret_cast<const bf16*>(ex.wptr[id]); };
     switch (op_kind(op.name)) {
       case OP_EMBED:
-        K(embed_launch(ex.tok, Wp(tt.embed), ex.X, S, d, ex.rank * Vl, Vl, st), "embed");
+        {
+          const int e0 = P0();
+          K(KC_EMBED, e0, 0, Sd * d * 6, embed_launch(ex.tok, Wp(tt.embed), ex.X, S, d, ex.rank * Vl, Vl, st),
+            "embed");
+        }
         break;
       case OP_EMBED_AR:
       case OP_ATTN_AR:
       case OP_MLP_AR:
-        tp_allreduce_f32(ex, a.nccl, ex.X, (size_t)S * d);
+        {
+          const int e0 = P0();
+          tp_allreduce_f32(ex, a.nccl, ex.X, (size_t)S * d);
+          if (e0 >= 0) ex.prof_end(KC_ALLREDUCE, e0, 0, Sd * d * 4);
+        }
         break;
       case OP_ATTN_NORM:
-        K(rmsnorm_launch(ex.X, Wp(tt.norm1[l]), ex.Xn, S, d, ex.eps, st), "rmsnorm");
+        {
+          const int e0 = P0();
+          K(KC_RMSNORM, e0, 0, Sd * d * 6 + 2.0 * d,
+            rmsnorm_launch(ex.X, Wp(tt.norm1[l]), ex.Xn, S, d, ex.eps, st), "rmsnorm");
+        }
         break;
       case OP_QKV:
         shrink(ex.Xn, d, d, l, {T_Q, T_K, T_V});
-        K(gemm_launch(LP[l].qkv, EPI_ROPE, ex.num_sms, st), "gemm_qkv");
+        {
+          const double n = nq + 2.0 * nkv;
+          const int e0 = P0();
+          K(KC_GEMM_QKV, e0, 2.0 * Sd * (n * d + r * lora_n(l, {T_Q, T_K, T_V})),
+            2.0 * (n * d + Sd * d + Sd * n), gemm_launch(LP[l].qkv, EPI_ROPE, ex.num_sms, st),
+            "gemm_qkv");
+        }
         break;
       case OP_ROPE:  // fused into the QKV epilogue
         break;
       case OP_ATTN:
-        K(attention_launch(ex.QKV, ex.O, S, m.n_heads / ex.world, m.n_kv_heads / ex.world, hd, st),
-          "attention");
+        {
+          const int e0 = P0();
+          K(KC_ATTN, e0, 2.0 * hd * ((double)m.n_heads / ex.world) * Sd * (Sd + 1),
+            2.0 * Sd * (2.0 * nq + 2.0 * nkv),
+            attention_launch(ex.QKV, ex.O, S, m.n_heads / ex.world, m.n_kv_heads / ex.world, hd, st),
+            "attention");
+        }
         break;
       case OP_O:
         shrink(ex.O, nq, nq, l, {T_O});
         if (ex.world > 1 && ex.rank != 0)
           cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
-        K(gemm_launch(LP[l].o, EPI_RESID, ex.num_sms, st), "gemm_o");
+        {
+          const int e0 = P0();
+          K(KC_GEMM_O, e0, 2.0 * Sd * d * ((double)nq + r * lora_n(l, {T_O}) / d),
+            2.0 * ((double)d * nq + Sd * nq) + 8.0 * Sd * d,
+            gemm_launch(LP[l].o, EPI_RESID, ex.num_sms, st), "gemm_o");
+        }
         break;
       case OP_MLP_NORM:
-        K(rmsnorm_launch(ex.X, Wp(tt.norm2[l]), ex.Xn, S, d, ex.eps, st), "rmsnorm");
+        {
+          const int e0 = P0();
+          K(KC_RMSNORM, e0, 0, Sd * d * 6 + 2.0 * d,
+            rmsnorm_launch(ex.X, Wp(tt.norm2[l]), ex.Xn, S, d, ex.eps, st), "rmsnorm");
+        }
         break;
       case OP_GU:
         shrink(ex.Xn, d, d, l, {T_GATE, T_UP});
-        K(gemm_launch(LP[l].gu, EPI_SILU, ex.num_sms, st), "gemm_gate_up");
+        {
+          const int e0 = P0();
+          K(KC_GEMM_GU, e0, 2.0 * Sd * (2.0 * F * d + r * lora_n(l, {T_GATE, T_UP})),
+            2.0 * (2.0 * F * d + Sd * d + Sd * F), gemm_launch(LP[l].gu, EPI_SILU, ex.num_sms, st),
+            "gemm_gate_up");
+        }
         break;
       case OP_ACT:  // fused into the gate/up epilogue
         break;
@@ -323,15 +410,24 @@ void run_forward(Exec& ex, const RunArgs& a) {
         shrink(ex.Hb, F, F, l, {T_DOWN});
         if (ex.world > 1 && ex.rank != 0)
           cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
-        K(gemm_launch(LP[l].down, EPI_RESID, ex.num_sms, st), "gemm_down");
+        {
+          const int e0 = P0();
+          K(KC_GEMM_DOWN, e0, 2.0 * Sd * ((double)d * F + r * lora_n(l, {T_DOWN})),
+            2.0 * ((double)d * F + Sd * F) + 8.0 * Sd * d,
+            gemm_launch(LP[l].down, EPI_RESID, ex.num_sms, st), "gemm_down");
+        }
         break;
       case OP_FNORM:  // fused into the head kernel (fp32 last-row norm)
         break;
       case OP_HEAD:
         cuda_check(cudaMemsetAsync(ex.key, 0, 8, st), "memset key");
-        K(head_launch(ex.X + (size_t)(S - 1) * d, Wp(tt.fnorm), Wp(tt.head), Vl, d, ex.eps,
-                      ex.logits + (size_t)ex.rank * Vl, ex.key, ex.rank * Vl, ex.num_sms, st),
-          "head");
+        {
+          const int e0 = P0();
+          K(KC_HEAD, e0, 2.0 * Vl * d, 2.0 * Vl * d + 4.0 * Vl,
+            head_launch(ex.X + (size_t)(S - 1) * d, Wp(tt.fnorm), Wp(tt.head), Vl, d, ex.eps,
+                        ex.logits + (size_t)ex.rank * Vl, ex.key, ex.rank * Vl, ex.num_sms, st),
+            "head");
+        }
         break;
       case OP_LOGITS_AG:
         tp_allgather_logits(ex, a.nccl);

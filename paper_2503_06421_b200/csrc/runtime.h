@@ -54,6 +54,24 @@ struct Exec {
   // cache: (S, lora_rank, mask, adapter arena base) -> per-layer params
   std::map<std::tuple<int, int, uint32_t, const void*, uint64_t>, std::vector<LayerLaunch>> cache;
   int launches = 0;
+  // per-kernel-class timing (TIDAL_DEBUG_PROFILE): event pairs on the compute
+  // stream around every launch, plus each launch's algorithmic flops/bytes
+  bool profile = false;
+  std::vector<cudaEvent_t> prof_ev;
+  struct ProfRec {
+    int cls;
+    int ev;
+    double flops, bytes;
+  };
+  std::vector<ProfRec> prof_pending;
+  struct ProfTot {
+    double ms = 0, flops = 0, bytes = 0;
+    long launches = 0;
+  };
+  std::vector<ProfTot> prof_tot;
+  int prof_begin();                               // returns event-pair index, records start
+  void prof_end(int cls, int ev, double flops, double bytes);
+  void prof_collect();                            // after the stream synchronised
 
   void init(int device, const ModelShape& m, float eps, float theta, int world, int rank,
             int max_tokens);
@@ -61,6 +79,12 @@ struct Exec {
   const std::vector<LayerLaunch>& layer_params(const TensorTable& tt, int S, const void* akey,
                                                uint64_t gen);
 };
+
+enum KernelClass {
+  KC_EMBED, KC_RMSNORM, KC_SHRINK, KC_GEMM_QKV, KC_ATTN, KC_GEMM_O, KC_GEMM_GU, KC_GEMM_DOWN,
+  KC_HEAD, KC_ALLREDUCE, KC_COUNT
+};
+extern const char* const kKernelClassNames[KC_COUNT];
 
 struct Recorder {  // lax tracing: first-read order of weights as ops execute
   std::vector<char> seen;

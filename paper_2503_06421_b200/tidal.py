@@ -19,7 +19,7 @@ OK = 0
 ERR_NAMES = {0: "OK", 1: "INVALID", 2: "OOM", 3: "CUDA", 4: "NCCL", 5: "STRUCTURE",
              6: "RESIDENCY", 7: "COW", 8: "BUFSZ", 9: "NUMERIC"}
 GROUPS_PER_LAYER, GROUPS_MAX_TRANSFERS, GROUPS_PER_TENSOR = 0, 1, 2
-DEBUG_POISON, DEBUG_SKIP_BARRIER, DEBUG_SCRUB_L2, DEBUG_SERIAL = 1, 2, 4, 8
+DEBUG_POISON, DEBUG_SKIP_BARRIER, DEBUG_SCRUB_L2, DEBUG_SERIAL, DEBUG_PROFILE = 1, 2, 4, 8, 16
 U64_MAX = (1 << 64) - 1
 
 
@@ -67,6 +67,11 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class KernelTime(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("total_ms", C.c_double), ("launches", C.c_long),
+                ("flops", C.c_double), ("bytes", C.c_double)]
+
+
 FILL_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
 VP = C.c_void_p
 
@@ -96,6 +101,8 @@ SIGNATURES = [
     ("tidal_comm_destroy", None, [VP]),
     ("tidal_set_debug", C.c_int, [VP, C.c_int, C.c_int]),
     ("tidal_template_checksum", C.c_int, [VP, C.POINTER(C.c_uint64)]),
+    ("tidal_profile_read", C.c_int, [VP, C.POINTER(KernelTime), C.c_int, C.POINTER(C.c_int),
+                                     C.c_int]),
     ("tidal_weight_ptr", C.c_int, [VP, C.c_char_p, C.POINTER(VP)]),
     ("tidal_k_rmsnorm", C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_float]),
     ("tidal_k_embed", C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_int, C.c_int]),
@@ -256,6 +263,13 @@ class Template:
 
     def set_debug(self, flags: int, arg: int = -1) -> None:
         _check(lib().tidal_set_debug(self.h, flags, arg))
+
+    def profile(self, reset: bool = True) -> dict:
+        n = C.c_int(0)
+        arr = (KernelTime * 32)()
+        _check(lib().tidal_profile_read(self.h, arr, 32, C.byref(n), int(reset)))
+        return {k.name.decode(): {"ms": k.total_ms, "launches": k.launches, "flops": k.flops,
+                                  "bytes": k.bytes} for k in arr[:n.value]}
 
     def checksum(self) -> int:
         v = C.c_uint64(0)

@@ -129,9 +129,18 @@ def test_fault_injection_detected(T):
     cfg = synth.config("tiny")
     rig = Rig(T, cfg, seed=2, budget=0.0, policy=2)
     tok = synth.prompt(cfg, 16, 2)
-    n_groups = sum(l.startswith("GROUP") for l in rig.tpl.plan_dump().splitlines())
+    # The copy stream is FIFO, so a wait on group g also covers every earlier
+    # group: the binding barriers are the ones that raise the waited maximum.
+    # Dropping one of those must be detected.
+    waited, trials = -1, []
+    for l in rig.tpl.plan_dump().splitlines():
+        if l.startswith("BARRIER"):
+            g = max(int(x) for x in l.split()[2].split(","))
+            if g > waited:
+                trials.append(g)
+                waited = g
+    assert len(trials) >= 10
     detected = 0
-    trials = list(range(n_groups))
     for g in trials:
         rig.tpl.set_debug(T.DEBUG_POISON | T.DEBUG_SKIP_BARRIER, g)
         try:
