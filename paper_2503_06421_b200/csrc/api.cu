@@ -171,6 +171,7 @@ tidal_status tidal_model_create(const tidal_model_config* cfg, const tidal_host_
   const int hd = m.head_dim();
   require(hd == 64 || hd == 128, "head_dim must be 64 or 128");
   require(m.d_model % 64 == 0 && m.d_ff % 8 == 0, "d_model % 64, d_ff % 8 required");
+  require(m.d_model <= 8192, "d_model <= 8192 (RMSNorm keeps a row in registers)");
   require(m.n_kv_heads % world == 0 && m.d_ff % world == 0 && m.vocab % world == 0,
           "model does not shard evenly over world");
   require((m.d_ff / world) % 8 == 0, "d_ff/world must be a multiple of 8");
@@ -340,7 +341,9 @@ static void warm_kernels(tidal_template* tp) {
   const bf16* A[1] = {ex.Xn};
   bf16* T[1] = {ex.T[0]};
   for (int r : {8, 16, 32, 64})
-    cuda_check(lora_shrink_launch(ex.Xn, 64, 1, 64, A, T, 1, r, 1.f, ex.compute), "warm shrink");
+    cuda_check(lora_shrink_launch(ex.Xn, 64, 1, 64, A, T, 1, r, 1.f, ex.num_sms, ex.shrink_ws,
+                                  ex.shrink_tickets, ex.compute),
+               "warm shrink");
   cuda_check(cudaStreamSynchronize(ex.compute), "warm run");
   ex.cache.clear();
 }
@@ -779,7 +782,17 @@ tidal_status tidal_k_lora_shrink(const void* X, int M, int K, const void* A, voi
                                  float scale) {
   const bf16* As[1] = {(const bf16*)A};
   bf16* Ts[1] = {(bf16*)T};
-  return sync_status(lora_shrink_launch((const bf16*)X, K, M, K, As, Ts, 1, r, scale, 0), "shrink");
+  float* ws = nullptr;
+  unsigned int* tk = nullptr;
+  cudaError_t e = cudaMalloc(&ws, (size_t)SHRINK_MAX_KSPLIT * M * r * 4 + 16);
+  if (e == cudaSuccess) e = cudaMalloc(&tk, ((M + 63) / 64 + 1) * 4);
+  if (e == cudaSuccess) e = cudaMemset(tk, 0, ((M + 63) / 64 + 1) * 4);
+  if (e == cudaSuccess)
+    e = lora_shrink_launch((const bf16*)X, K, M, K, As, Ts, 1, r, scale, sms(), ws, tk, 0);
+  tidal_status st = sync_status(e, "shrink");
+  cudaFree(ws);
+  cudaFree(tk);
+  return st;
 }
 
 tidal_status tidal_k_attention(const void* qkv, void* O, int S, int H, int KV, int hd) {

@@ -87,25 +87,36 @@ __device__ __forceinline__ void add_chunk_f32(const float (&v)[32], uint8_t* stg
 #pragma unroll
   for (int k = 0; k < 8; ++k) st[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
   __syncwarp();
+  const int ch = lane & 7, c = ch * 4;
+  if (c + 4 <= nvalid) {
+    // issue all 8 residual loads before any store (one memory latency per chunk)
+    float4 x[8];
 #pragma unroll
-  for (int it = 0; it < 8; ++it) {
-    const int r = it * 4 + (lane >> 3), ch = lane & 7;
-    const int m = row0 + r;
-    const int c = ch * 4;
-    if (m < M && c < nvalid) {
-      float4 a = *reinterpret_cast<const float4*>(stg + r * STG_ROW + ch * 16);
-      float* dst = out + (size_t)m * ldo + col + c;
-      if (c + 4 <= nvalid) {
-        float4 x = *reinterpret_cast<float4*>(dst);
-        x.x += a.x;
-        x.y += a.y;
-        x.z += a.z;
-        x.w += a.w;
-        *reinterpret_cast<float4*>(dst) = x;
-      } else {
-        const float* s = reinterpret_cast<const float*>(&a);
-        for (int e = 0; e < nvalid - c; ++e) dst[e] += s[e];
+    for (int it = 0; it < 8; ++it) {
+      const int m = row0 + it * 4 + (lane >> 3);
+      if (m < M) x[it] = __ldcg(reinterpret_cast<const float4*>(out + (size_t)m * ldo + col + c));
+    }
+#pragma unroll
+    for (int it = 0; it < 8; ++it) {
+      const int r = it * 4 + (lane >> 3);
+      const int m = row0 + r;
+      if (m < M) {
+        const float4 a = *reinterpret_cast<const float4*>(stg + r * STG_ROW + ch * 16);
+        x[it].x += a.x;
+        x[it].y += a.y;
+        x[it].z += a.z;
+        x[it].w += a.w;
+        *reinterpret_cast<float4*>(out + (size_t)m * ldo + col + c) = x[it];
       }
+    }
+  } else if (c < nvalid) {
+    for (int it = 0; it < 8; ++it) {
+      const int r = it * 4 + (lane >> 3);
+      const int m = row0 + r;
+      if (m >= M) continue;
+      const float* s = reinterpret_cast<const float*>(stg + r * STG_ROW + ch * 16);
+      float* dst = out + (size_t)m * ldo + col + c;
+      for (int e = 0; e < nvalid - c; ++e) dst[e] += s[e];
     }
   }
   __syncwarp();

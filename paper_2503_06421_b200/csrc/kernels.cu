@@ -58,7 +58,7 @@ __global__ void embed_kernel(const int32_t* __restrict__ tok, const bf16* __rest
 }
 
 // ---------------- RMSNorm ----------------
-constexpr int NORM_THREADS = 256;
+constexpr int NORM_THREADS = 256, NORM_VEC = 8;
 __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const float* __restrict__ X,
                                                                const bf16* __restrict__ g,
                                                                bf16* __restrict__ Y, int d,
@@ -66,136 +66,33 @@ __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const float* __re
   __shared__ float red[32];
   const float4* x = reinterpret_cast<const float4*>(X + (size_t)blockIdx.x * d);
   const int n4 = d >> 2;
+  // the row stays in registers: one HBM read of X (d <= 4 * 256 * NORM_VEC)
+  float4 v[NORM_VEC];
   float ss = 0.f;
-  for (int i = threadIdx.x; i < n4; i += NORM_THREADS) {
-    float4 v = x[i];
-    ss += v.x * v.x + v.y * v.y + v.z * v.z + v.w * v.w;
+#pragma unroll
+  for (int j = 0; j < NORM_VEC; ++j) {
+    const int i = threadIdx.x + j * NORM_THREADS;
+    v[j] = i < n4 ? x[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss += v[j].x * v[j].x + v[j].y * v[j].y + v[j].z * v[j].z + v[j].w * v[j].w;
   }
   ss = block_sum<NORM_THREADS>(ss, red);
   const float inv = rsqrtf(ss / (float)d + eps);
   uint2* y = reinterpret_cast<uint2*>(Y + (size_t)blockIdx.x * d);
   const uint2* g2 = reinterpret_cast<const uint2*>(g);
-  for (int i = threadIdx.x; i < n4; i += NORM_THREADS) {
-    float4 v = x[i];
+#pragma unroll
+  for (int j = 0; j < NORM_VEC; ++j) {
+    const int i = threadIdx.x + j * NORM_THREADS;
+    if (i >= n4) break;
+    const float4 vv = v[j];
     uint2 gw = g2[i];
     const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gw);
     float2 g01 = __bfloat1622float2(gh[0]), g23 = __bfloat1622float2(gh[1]);
-    __nv_bfloat162 r0 = __floats2bfloat162_rn(v.x * inv * g01.x, v.y * inv * g01.y);
-    __nv_bfloat162 r1 = __floats2bfloat162_rn(v.z * inv * g23.x, v.w * inv * g23.y);
+    __nv_bfloat162 r0 = __floats2bfloat162_rn(vv.x * inv * g01.x, vv.y * inv * g01.y);
+    __nv_bfloat162 r1 = __floats2bfloat162_rn(vv.z * inv * g23.x, vv.w * inv * g23.y);
     uint2 o;
     o.x = *reinterpret_cast<uint32_t*>(&r0);
     o.y = *reinterpret_cast<uint32_t*>(&r1);
     y[i] = o;
-  }
-}
-
-// ---------------- LoRA shrink: T = scale * X A^T (mma.sync m16n8k16) ----------------
-// CTA = 64 rows x one target; 4 warps x 16 rows; K in steps of 32 through a
-// 2-stage cp.async ring.  r <= 64.
-constexpr int SH_BM = 64, SH_BK = 32, SH_LD = 40;  // smem row stride (elements), conflict-free
-
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
-  const int n = valid ? 16 : 0;
-  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem), "r"(n)
-               : "memory");
-}
-__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
-template <int N>
-__device__ __forceinline__ void cp_wait() {
-  asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
-}
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(p);
-  asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
-               : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
-               : "r"(s));
-}
-__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], const void* p) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(p);
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
-               : "=r"(r[0]), "=r"(r[1])
-               : "r"(s));
-}
-__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4],
-                                         const uint32_t (&b)[2]) {
-  asm volatile(
-      "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
-      "{%8,%9}, {%0,%1,%2,%3};"
-      : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
-}
-
-struct ShrinkArgs {
-  const bf16* A[3];
-  bf16* T[3];
-};
-
-template <int R>
-__global__ void __launch_bounds__(128) lora_shrink_kernel(const bf16* __restrict__ X, int ldx, int M,
-                                                          int K, ShrinkArgs args, float scale) {
-  __shared__ __align__(16) bf16 xs[2][SH_BM * SH_LD];
-  __shared__ __align__(16) bf16 as[2][R * SH_LD];
-  const int t = blockIdx.y;
-  const bf16* __restrict__ A = args.A[t];
-  const int m0 = blockIdx.x * SH_BM;
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  float acc[R / 8][4];
-#pragma unroll
-  for (int i = 0; i < R / 8; ++i) acc[i][0] = acc[i][1] = acc[i][2] = acc[i][3] = 0.f;
-  const int nk = (K + SH_BK - 1) / SH_BK;
-  auto load = [&](int kb, int buf) {
-    const int k0 = kb * SH_BK;
-    for (int c = threadIdx.x; c < SH_BM * 4; c += 128) {
-      const int r = c >> 2, ch = c & 3;
-      const int m = m0 + r, k = k0 + ch * 8;
-      const bool ok = m < M && k < K;
-      cp_async16(&xs[buf][r * SH_LD + ch * 8], ok ? X + (size_t)m * ldx + k : X, ok);
-    }
-    for (int c = threadIdx.x; c < R * 4; c += 128) {
-      const int r = c >> 2, ch = c & 3;
-      const int k = k0 + ch * 8;
-      const bool ok = k < K;
-      cp_async16(&as[buf][r * SH_LD + ch * 8], ok ? A + (size_t)r * K + k : A, ok);
-    }
-    cp_commit();
-  };
-  load(0, 0);
-  for (int kb = 0; kb < nk; ++kb) {
-    const int buf = kb & 1;
-    if (kb + 1 < nk) {
-      load(kb + 1, buf ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
-    __syncthreads();
-#pragma unroll
-    for (int kk = 0; kk < SH_BK / 16; ++kk) {
-      uint32_t a[4];
-      const int ar = warp * 16 + (lane & 15), ac = kk * 16 + (lane >> 4) * 8;
-      ldsm_x4(a, &xs[buf][ar * SH_LD + ac]);
-#pragma unroll
-      for (int nt = 0; nt < R / 8; ++nt) {
-        uint32_t b[2];
-        const int br = nt * 8 + (lane & 7), bc = kk * 16 + ((lane >> 3) & 1) * 8;
-        ldsm_x2(b, &as[buf][br * SH_LD + bc]);
-        mma16816(acc[nt], a, b);
-      }
-    }
-    __syncthreads();
-  }
-  bf16* T = args.T[t];
-  const int r0 = m0 + warp * 16 + (lane >> 2);
-#pragma unroll
-  for (int nt = 0; nt < R / 8; ++nt) {
-    const int c = nt * 8 + 2 * (lane & 3);
-    if (r0 < M)
-      *reinterpret_cast<__nv_bfloat162*>(T + (size_t)r0 * R + c) =
-          __floats2bfloat162_rn(acc[nt][0] * scale, acc[nt][1] * scale);
-    if (r0 + 8 < M)
-      *reinterpret_cast<__nv_bfloat162*>(T + (size_t)(r0 + 8) * R + c) =
-          __floats2bfloat162_rn(acc[nt][2] * scale, acc[nt][3] * scale);
   }
 }
 
@@ -299,24 +196,6 @@ cudaError_t embed_launch(const int32_t* tok, const bf16* E, float* X, int S, int
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d, float eps,
                            cudaStream_t s) {
   rmsnorm_kernel<<<S, NORM_THREADS, 0, s>>>(X, g, Y, d, eps);
-  return cudaGetLastError();
-}
-
-cudaError_t lora_shrink_launch(const bf16* X, int ldx, int M, int K, const bf16* const* A,
-                               bf16* const* T, int nt, int r, float scale, cudaStream_t s) {
-  ShrinkArgs a{};
-  for (int i = 0; i < nt && i < 3; ++i) {
-    a.A[i] = A[i];
-    a.T[i] = T[i];
-  }
-  dim3 grid((M + SH_BM - 1) / SH_BM, nt);
-  switch (r) {
-    case 8: lora_shrink_kernel<8><<<grid, 128, 0, s>>>(X, ldx, M, K, a, scale); break;
-    case 16: lora_shrink_kernel<16><<<grid, 128, 0, s>>>(X, ldx, M, K, a, scale); break;
-    case 32: lora_shrink_kernel<32><<<grid, 128, 0, s>>>(X, ldx, M, K, a, scale); break;
-    case 64: lora_shrink_kernel<64><<<grid, 128, 0, s>>>(X, ldx, M, K, a, scale); break;
-    default: return cudaErrorInvalidValue;
-  }
   return cudaGetLastError();
 }
 

@@ -60,6 +60,9 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   dalloc(logits, (size_t)m.vocab * 4);
   dalloc(key, 64);
   dalloc(tok, S * 4);
+  dalloc(shrink_ws, (size_t)SHRINK_MAX_KSPLIT * S * 3 * 64 * 4);
+  dalloc(shrink_tickets, ((S + 63) / 64 + 1) * 4);
+  cuda_check(cudaMemset(shrink_tickets, 0, ((S + 63) / 64 + 1) * 4), "memset tickets");
   // RoPE table: angle = pos * theta^(-2i/hd), cos/sin in double, stored fp32
   std::vector<float2> cs(S * (hd / 2));
   for (size_t p = 0; p < S; ++p)
@@ -82,7 +85,7 @@ void Exec::destroy() {
   cudaSetDevice(device);
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
-  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope};
+  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, shrink_ws, shrink_tickets};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int t = 0; t < kNumTargets; ++t)
@@ -307,7 +310,9 @@ void run_forward(Exec& ex, const RunArgs& a) {
     if (n) {
       const int e0 = P0();
       K(KC_SHRINK, e0, 2.0 * Sd * Kd * r * n, 2.0 * (Sd * Kd + (double)n * r * (Kd + Sd)),
-        lora_shrink_launch(X, ldx, S, Kd, A, T, n, r, a.lora_scale, st), "lora_shrink");
+        lora_shrink_launch(X, ldx, S, Kd, A, T, n, r, a.lora_scale, ex.num_sms,
+                           ex.shrink_ws, ex.shrink_tickets, st),
+        "lora_shrink");
     }
   };
   auto lora_n = [&](int l, std::initializer_list<int> ts) {

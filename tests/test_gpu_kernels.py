@@ -161,7 +161,8 @@ def test_embed_and_vocab_shard(T):
     assert np.array_equal(Xs.cpu().numpy(), ref)
 
 
-@pytest.mark.parametrize("M,K,r", [(64, 256, 8), (300, 5120, 16), (77, 688, 64)])
+@pytest.mark.parametrize("M,K,r", [(64, 256, 8), (300, 5120, 16), (77, 688, 64), (2048, 13824, 16),
+                                   (1, 64, 32)])
 def test_lora_shrink(T, M, K, r):
     rng = np.random.default_rng(K)
     X, A = _bf(rng, (M, K)), _bf(rng, (r, K), 1 / math.sqrt(K))
