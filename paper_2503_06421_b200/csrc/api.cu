@@ -7,6 +7,8 @@
 #include <cmath>
 #include <cstring>
 #include <deque>
+#include <map>
+#include <memory>
 #include <string>
 #include <thread>
 #include <vector>
@@ -87,7 +89,17 @@ struct tidal_comm {
   int world = 1, rank = 0, device = 0;
 };
 
+// Plan of the template with an adapter of (rank, mask) attached.  Depends only
+// on the template (layout, resident prefix, generation) and (rank, mask), not on
+// the adapter's bytes, so attaching a new adapter of a known shape is O(1).
+struct AdapterPlan {
+  TensorTable tt;
+  Plan plan;
+  uint64_t gen = 0;
+};
+
 struct tidal_template {
+  std::map<std::pair<int, uint32_t>, std::shared_ptr<AdapterPlan>> aplans;
   ModelShape shape;
   float theta = 1e4f, eps = 1e-5f;
   int world = 1, rank = 0;
@@ -123,9 +135,7 @@ struct tidal_template {
 
 struct tidal_adapter {
   tidal_template* tpl = nullptr;
-  TensorTable tt;
-  Plan plan;
-  uint64_t plan_gen = 0;
+  std::shared_ptr<AdapterPlan> ap;
   int rank = 0;
   float scale = 1.f;
   uint32_t mask = 0;
@@ -341,9 +351,12 @@ static void warm_kernels(tidal_template* tp) {
   const bf16* A[1] = {ex.Xn};
   bf16* T[1] = {ex.T[0]};
   for (int r : {8, 16, 32, 64})
-    cuda_check(lora_shrink_launch(ex.Xn, 64, 1, 64, A, T, 1, r, 1.f, ex.num_sms, ex.shrink_ws,
-                                  ex.shrink_tickets, ex.compute),
-               "warm shrink");
+    for (int nt = 1; nt <= 3; ++nt) {
+      const bf16* A3[3] = {ex.Xn, ex.Xn, ex.Xn};
+      bf16* T3[3] = {ex.T[0], ex.T[1], ex.T[2]};
+      cuda_check(lora_shrink_launch(ex.Xn, 64, 1, 64, A3, T3, nt, r, 1.f, ex.compute),
+                 "warm shrink");
+    }
   cuda_check(cudaStreamSynchronize(ex.compute), "warm run");
   ex.cache.clear();
 }
@@ -488,17 +501,27 @@ tidal_status tidal_adapter_layout(const tidal_template* tp, int rank, uint32_t m
   TIDAL_CATCH
 }
 
+static std::shared_ptr<AdapterPlan> get_adapter_plan(tidal_template* tp, int rank, uint32_t mask) {
+  auto& slot = tp->aplans[{rank, mask}];
+  if (!slot || slot->gen != tp->gen) {
+    auto ap = std::make_shared<AdapterPlan>();
+    adapter_table(tp, rank, mask, ap->tt, "adapter");
+    ap->plan = make_plan(ap->tt, tp->tr, tp->choice);
+    ap->gen = tp->gen;
+    slot = ap;
+  }
+  return slot;
+}
+
 tidal_status tidal_attach_lora(tidal_template* tp, const tidal_lora_desc* d, tidal_adapter** out) {
   TIDAL_TRY
   require(tp && d && out, "null argument");
   auto* a = new tidal_adapter();
   try {
-    adapter_table(tp, d->rank, d->target_mask, a->tt, d->checkpoint ? d->checkpoint : "adapter");
-    a->plan = make_plan(a->tt, tp->tr, tp->choice);
-    a->plan_gen = tp->gen;
-    require(d->bytes == a->plan.adapter_bytes,
+    a->ap = get_adapter_plan(tp, d->rank, d->target_mask);
+    require(d->bytes == a->ap->plan.adapter_bytes,
             "adapter buffer is " + std::to_string(d->bytes) + " B, layout needs " +
-                std::to_string(a->plan.adapter_bytes),
+                std::to_string(a->ap->plan.adapter_bytes),
             TIDAL_ERR_STRUCTURE);
     require(d->host_pinned != nullptr || tp->dry, "adapter needs a pinned host buffer");
   } catch (...) {
@@ -523,12 +546,10 @@ tidal_status tidal_plan_dump(const tidal_template* tp, const tidal_adapter* a, c
   require(tp != nullptr, "null template");
   if (a) {
     require(a->tpl == tp, "adapter attached to another template");
-    if (a->plan_gen != tp->gen) {
-      auto* ma = const_cast<tidal_adapter*>(a);
-      ma->plan = make_plan(ma->tt, tp->tr, tp->choice);
-      ma->plan_gen = tp->gen;
-    }
-    dump_copy(plan_dump(a->tt, a->plan), buf, cap, needed);
+    auto* ma = const_cast<tidal_adapter*>(a);
+    if (ma->ap->gen != tp->gen)
+      ma->ap = get_adapter_plan(const_cast<tidal_template*>(tp), ma->rank, ma->mask);
+    dump_copy(plan_dump(ma->ap->tt, ma->ap->plan), buf, cap, needed);
   } else {
     dump_copy(plan_dump(tp->tt, tp->plan), buf, cap, needed);
   }
@@ -549,13 +570,11 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
   auto* a = const_cast<tidal_adapter*>(ca);
   if (a) {
     require(a->tpl == tp, "adapter attached to another template");
-    if (a->plan_gen != tp->gen) {
-      a->plan = make_plan(a->tt, tp->tr, tp->choice);
-      a->plan_gen = tp->gen;
-    }
+    if (a->ap->gen != tp->gen) a->ap = get_adapter_plan(tp, a->rank, a->mask);
   }
-  const Plan& P = a ? a->plan : tp->plan;
-  const TensorTable& tt = a ? a->tt : tp->tt;
+  const std::shared_ptr<AdapterPlan> hold = a ? a->ap : nullptr;
+  const Plan& P = a ? hold->plan : tp->plan;
+  const TensorTable& tt = a ? hold->tt : tp->tt;
   Exec& ex = tp->ex;
   cuda_check(cudaSetDevice(tp->device), "cudaSetDevice");
   if (a && P.adapter_bytes > tp->arena_cap) {
@@ -782,17 +801,8 @@ tidal_status tidal_k_lora_shrink(const void* X, int M, int K, const void* A, voi
                                  float scale) {
   const bf16* As[1] = {(const bf16*)A};
   bf16* Ts[1] = {(bf16*)T};
-  float* ws = nullptr;
-  unsigned int* tk = nullptr;
-  cudaError_t e = cudaMalloc(&ws, (size_t)SHRINK_MAX_KSPLIT * M * r * 4 + 16);
-  if (e == cudaSuccess) e = cudaMalloc(&tk, ((M + 63) / 64 + 1) * 4);
-  if (e == cudaSuccess) e = cudaMemset(tk, 0, ((M + 63) / 64 + 1) * 4);
-  if (e == cudaSuccess)
-    e = lora_shrink_launch((const bf16*)X, K, M, K, As, Ts, 1, r, scale, sms(), ws, tk, 0);
-  tidal_status st = sync_status(e, "shrink");
-  cudaFree(ws);
-  cudaFree(tk);
-  return st;
+  return sync_status(lora_shrink_launch((const bf16*)X, K, M, K, As, Ts, 1, r, scale, 0),
+                     "shrink");
 }
 
 tidal_status tidal_k_attention(const void* qkv, void* O, int S, int H, int KV, int hd) {
@@ -811,9 +821,15 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
                           void* out, int ldo, int M, int K, const void* const* T,
                           const void* const* B, int r, const void* rope, int head_dim) {
   TIDAL_TRY
+  const int bn_req = epi >> 8;
+  epi &= 0xFF;
   require(epi >= 0 && epi <= 3 && nseg >= 1 && nseg <= 3, "bad gemm arguments");
   GemmParams p;
   memset(&p, 0, sizeof p);
+  p.bn = bn_req ? bn_req : gemm_pick_bn(epi, M, seg_n, epi == EPI_SILU ? 1 : nseg, sms());
+  require(p.bn == 256 || p.bn == 192 || p.bn == 128, "bn must be 256, 192 or 128");
+  if (epi == EPI_SILU) p.bn = 128;
+  if (epi == EPI_ROPE && p.bn == 192) p.bn = 256;
   auto mk = [&](CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box) {
     require(make_tmap(m, base, rows, cols, cols * 2, box, 64), "tensor map encode failed");
   };
@@ -845,17 +861,17 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
     int col = 0;
     p.nseg = nseg;
     for (int s = 0; s < nseg; ++s) {
-      mk(&p.b[s], W[s], seg_n[s], K, 256);
+      mk(&p.b[s], W[s], seg_n[s], K, p.bn);
       p.seg[s].n = seg_n[s];
       p.seg[s].out_col = col;
       p.seg[s].rope = (epi == EPI_ROPE) && s < 2;
       p.seg[s].lora = p.lora_r > 0 && T[s] && B[s];
       if (p.seg[s].lora) {
         mk(&p.ta[s], T[s], M, r, 128);
-        mk(&p.tb[s], B[s], seg_n[s], r, 256);
+        mk(&p.tb[s], B[s], seg_n[s], r, p.bn);
       }
       col += seg_n[s];
-      p.n_tiles[s] = (seg_n[s] + GEMM_BN - 1) / GEMM_BN;
+      p.n_tiles[s] = (seg_n[s] + p.bn - 1) / p.bn;
       p.total_tiles += p.n_tiles[s] * mt;
     }
   }

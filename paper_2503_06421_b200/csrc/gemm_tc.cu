@@ -130,7 +130,7 @@ __device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
-template <int EPI>
+template <int EPI, int BNT>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& seg, int& n0,
                                             int& m0) {
   int gn = tile / p.m_tiles;
@@ -140,11 +140,13 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
     gn -= p.n_tiles[seg];
     ++seg;
   }
-  n0 = gn * (EPI == EPI_SILU ? 128 : BN);
+  n0 = gn * (EPI == EPI_SILU ? 128 : BNT);
 }
 
-template <int EPI>
+template <int EPI, int BNT>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
+  constexpr int BNX = EPI == EPI_SILU ? 256 : BNT;  // MMA N = accumulator columns
+  constexpr int BBYTES = BNX * BK * 2;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -190,7 +192,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       uint32_t phase = 0;
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
         int seg, n0, m0;
-        decode_tile<EPI>(p, tile, seg, n0, m0);
+        decode_tile<EPI, BNT>(p, tile, seg, n0, m0);
         const bool lora = nlora > 0 && p.seg[seg].lora;
         const int nkb = nk + (lora ? nlora : 0);
         for (int kb = 0; kb < nkb; ++kb) {
@@ -199,7 +201,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           const uint32_t sb = sbase + OFF_B + stage * B_BYTES;
           const uint32_t fb = full_bar(stage);
           if (kb < nk) {
-            ptx::mbar_expect_tx(fb, A_BYTES + B_BYTES);
+            ptx::mbar_expect_tx(fb, A_BYTES + BBYTES);
             ptx::tma_load_2d(&p.a, sa, fb, kb * BK, m0);
             if (EPI == EPI_SILU) {
               ptx::tma_load_2d(&p.b[0], sb, fb, kb * BK, n0);
@@ -210,7 +212,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           } else {
             const int j = kb - nk;  // LoRA stage: EPI_SILU j=0 gate, j=1 up
             const int t = EPI == EPI_SILU ? j : seg;
-            const int bbytes = EPI == EPI_SILU ? B_BYTES / 2 : B_BYTES;
+            const int bbytes = EPI == EPI_SILU ? B_BYTES / 2 : BBYTES;
             ptx::mbar_expect_tx(fb, A_BYTES + bbytes);
             ptx::tma_load_2d(&p.ta[t], sa, fb, 0, m0);
             ptx::tma_load_2d(&p.tb[t], sb, fb, 0, n0);
@@ -226,7 +228,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
   } else if (warp == 1) {
     // ===================== MMA issuer =====================
     if (lane == 0) {
-      constexpr uint32_t IDESC = ptx::idesc_bf16(BM, BN);
+      constexpr uint32_t IDESC = ptx::idesc_bf16(BM, BNX);
       constexpr uint32_t IDESC_HALF = ptx::idesc_bf16(BM, BN / 2);
       const int nmma_lora = (p.lora_r + 15) / 16;
       int stage = 0;
@@ -235,12 +237,12 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       uint32_t acc_phase = 0;
       for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
         int seg, n0, m0;
-        decode_tile<EPI>(p, tile, seg, n0, m0);
+        decode_tile<EPI, BNT>(p, tile, seg, n0, m0);
         const bool lora = nlora > 0 && p.seg[seg].lora;
         const int nkb = nk + (lora ? nlora : 0);
         ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         ptx::tc_fence_after();
-        const uint32_t d_tmem = tmem_base + acc * BN;
+        const uint32_t d_tmem = tmem_base + acc * BNX;
         for (int kb = 0; kb < nkb; ++kb) {
           ptx::mbar_wait(full_bar(stage), phase);
           ptx::tc_fence_after();
@@ -280,11 +282,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     uint32_t acc_phase = 0;
     for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
       int seg, n0, m0;
-      decode_tile<EPI>(p, tile, seg, n0, m0);
+      decode_tile<EPI, BNT>(p, tile, seg, n0, m0);
       const GemmSeg sg = p.seg[seg];
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
       ptx::tc_fence_after();
-      const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BN;
+      const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNX;
       const int row0 = m0 + q * 32;
       const int m = row0 + lane;
       float v[32], w[32];
@@ -304,9 +306,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
                            sg.out_col + n0 + j * 32, ncols - j * 32);
         }
       } else if (EPI == EPI_RESID) {
-        const int ncols = min(BN, sg.n - n0);
+        const int ncols = min(BNT, sg.n - n0);
 #pragma unroll 1
-        for (int j = 0; j < BN / 32; ++j) {
+        for (int j = 0; j < BNT / 32; ++j) {
           if (j * 32 >= ncols) break;
           ld_chunk(tacc + j * 32, v);
           add_chunk_f32(v, stg, lane, reinterpret_cast<float*>(p.out), p.ldo, row0, p.M,
@@ -314,7 +316,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
         }
       } else if (EPI == EPI_ROPE && sg.rope) {
         const int hd = p.head_dim, half = hd >> 1;
-        const int ncols = min(BN, sg.n - n0);
+        const int ncols = min(BNT, sg.n - n0);
 #pragma unroll 1
         for (int h = 0; h * hd < ncols; ++h) {
 #pragma unroll 1
@@ -338,9 +340,9 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           }
         }
       } else {
-        const int ncols = min(BN, sg.n - n0);
+        const int ncols = min(BNT, sg.n - n0);
 #pragma unroll 1
-        for (int j = 0; j < BN / 32; ++j) {
+        for (int j = 0; j < BNT / 32; ++j) {
           if (j * 32 >= ncols) break;
           ld_chunk(tacc + j * 32, v);
           store_chunk_bf16(v, stg, lane, reinterpret_cast<bf16*>(p.out), p.ldo, row0, p.M,
@@ -370,22 +372,43 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 EncodeTiledFn g_encode = nullptr;
 std::once_flag g_once;
 
-template <int EPI>
+template <int EPI, int BNT>
 cudaError_t launch_t(const GemmParams& p, int num_sms, cudaStream_t s) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI, BNT>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
   int grid = p.total_tiles < num_sms ? p.total_tiles : num_sms;
   if (grid <= 0) return cudaSuccess;
-  gemm_tc_kernel<EPI><<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
+  gemm_tc_kernel<EPI, BNT><<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
   return cudaGetLastError();
 }
 
 }  // namespace
+
+int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms) {
+  if (epi == EPI_SILU) return 128;
+  const int mt = (M + BM - 1) / BM;
+  static const int cands[] = {256, 192, 128};
+  int best = 256;
+  double best_cost = 1e30;
+  for (int bn : cands) {
+    if (epi == EPI_ROPE && bn == 192) continue;  // RoPE tiles must hold whole heads
+    long tiles = 0;
+    for (int s = 0; s < nseg; ++s) tiles += (long)mt * ((seg_n[s] + bn - 1) / bn);
+    const long waves = (tiles + num_sms - 1) / num_sms;
+    // 128-wide tiles pay ~15% more per MAC (A-operand smem traffic per MMA doubles)
+    const double cost = (double)waves * bn * (bn == 128 ? 1.15 : 1.0);
+    if (cost < best_cost - 1e-9) {
+      best_cost = cost;
+      best = bn;
+    }
+  }
+  return best;
+}
 
 bool tma_init() {
   std::call_once(g_once, [] {
@@ -415,10 +438,18 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
 
 cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t s) {
   switch (epi) {
-    case EPI_STORE: return launch_t<EPI_STORE>(p, num_sms, s);
-    case EPI_ROPE: return launch_t<EPI_ROPE>(p, num_sms, s);
-    case EPI_SILU: return launch_t<EPI_SILU>(p, num_sms, s);
-    case EPI_RESID: return launch_t<EPI_RESID>(p, num_sms, s);
+    case EPI_STORE:
+      if (p.bn == 192) return launch_t<EPI_STORE, 192>(p, num_sms, s);
+      if (p.bn == 128) return launch_t<EPI_STORE, 128>(p, num_sms, s);
+      return launch_t<EPI_STORE, 256>(p, num_sms, s);
+    case EPI_ROPE:
+      if (p.bn == 128) return launch_t<EPI_ROPE, 128>(p, num_sms, s);
+      return launch_t<EPI_ROPE, 256>(p, num_sms, s);
+    case EPI_SILU: return launch_t<EPI_SILU, 128>(p, num_sms, s);
+    case EPI_RESID:
+      if (p.bn == 192) return launch_t<EPI_RESID, 192>(p, num_sms, s);
+      if (p.bn == 128) return launch_t<EPI_RESID, 128>(p, num_sms, s);
+      return launch_t<EPI_RESID, 256>(p, num_sms, s);
   }
   return cudaErrorInvalidValue;
 }

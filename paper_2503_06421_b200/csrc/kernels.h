@@ -48,7 +48,12 @@ struct alignas(64) GemmParams {
   int ldo;
   const float2* rope;  // [S, head_dim/2] (cos, sin)
   int head_dim;
+  int bn;              // N tile: 256 | 192 | 128 (EPI_SILU: 128 output cols = 256 acc cols)
 };
+
+// N-tile width minimising (waves x tile width) on num_sms SMs; the W/lora_B
+// tensor maps must use box rows = the returned value (128 for EPI_SILU).
+int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms);
 
 // Host helpers (gemm_tc.cu).
 bool tma_init();  // resolve cuTensorMapEncodeTiled through the runtime
@@ -67,13 +72,9 @@ cudaError_t embed_launch(const int32_t* tok, const bf16* E, float* X, int S, int
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d, float eps,
                            cudaStream_t s);
 // T_t[M, r] = bf16(scale * X[M, K] . A_t[r, K]^T), t < nt <= 3 (targets sharing X).
-// Split-K over CTAs: ws holds SHRINK_MAX_KSPLIT * M * nt * r floats, tickets
-// ceil(M/64) zero-initialised counters (self-cleaning).
-constexpr int SHRINK_MAX_KSPLIT = 16;
-int shrink_ksplit(int M, int K, int num_sms);
+// One read of X for all targets; intra-CTA split-K, deterministic reduction.
 cudaError_t lora_shrink_launch(const bf16* X, int ldx, int M, int K, const bf16* const* A,
-                               bf16* const* T, int nt, int r, float scale, int num_sms,
-                               float* ws, unsigned int* tickets, cudaStream_t s);
+                               bf16* const* T, int nt, int r, float scale, cudaStream_t s);
 // Causal GQA prefill attention over QKV [S, (H + 2 KV) hd] -> O [S, H hd].
 cudaError_t attention_launch(const bf16* qkv, bf16* O, int S, int H, int KV, int hd,
                              cudaStream_t s);

@@ -60,9 +60,6 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   dalloc(logits, (size_t)m.vocab * 4);
   dalloc(key, 64);
   dalloc(tok, S * 4);
-  dalloc(shrink_ws, (size_t)SHRINK_MAX_KSPLIT * S * 3 * 64 * 4);
-  dalloc(shrink_tickets, ((S + 63) / 64 + 1) * 4);
-  cuda_check(cudaMemset(shrink_tickets, 0, ((S + 63) / 64 + 1) * 4), "memset tickets");
   // RoPE table: angle = pos * theta^(-2i/hd), cos/sin in double, stored fp32
   std::vector<float2> cs(S * (hd / 2));
   for (size_t p = 0; p < S; ++p)
@@ -85,7 +82,7 @@ void Exec::destroy() {
   cudaSetDevice(device);
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
-  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, shrink_ws, shrink_tickets};
+  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int t = 0; t < kNumTargets; ++t)
@@ -128,20 +125,21 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     int col = 0;
     q.lora_r = 0;
     q.total_tiles = 0;
+    q.bn = gemm_pick_bn(EPI_ROPE, S, segn, 3, num_sms);
     for (int s = 0; s < 3; ++s) {
       q.seg[s].n = segn[s];
       q.seg[s].out_col = col;
       q.seg[s].rope = s < 2;
       col += segn[s];
-      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, 256);
+      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, q.bn);
       const int la = tt.lora_a[l][tg[s]];
       q.seg[s].lora = la >= 0;
       if (la >= 0) {
         q.lora_r = r;
         tmap(&q.ta[s], T[tg[s]], S, r, 128);
-        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, 256);
+        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, q.bn);
       }
-      q.n_tiles[s] = (segn[s] + GEMM_BN - 1) / GEMM_BN;
+      q.n_tiles[s] = (segn[s] + q.bn - 1) / q.bn;
       q.total_tiles += q.n_tiles[s] * mt;
     }
     q.nseg = 3;
@@ -155,20 +153,21 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     // ---- O (+ residual) ----
     GemmParams& o = ll.o;
     memset(&o, 0, sizeof o);
+    o.bn = gemm_pick_bn(EPI_RESID, S, &d, 1, num_sms);
     tmap(&o.a, O, S, nq, 128);
-    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, 256);
+    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, o.bn);
     o.seg[0].n = d;
     o.seg[0].lora = tt.lora_a[l][T_O] >= 0;
     if (o.seg[0].lora) {
       o.lora_r = r;
       tmap(&o.ta[0], T[T_O], S, r, 128);
-      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, 256);
+      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, o.bn);
     }
     o.nseg = 1;
     o.M = S;
     o.K = nq;
     o.m_tiles = mt;
-    o.n_tiles[0] = (d + GEMM_BN - 1) / GEMM_BN;
+    o.n_tiles[0] = (d + o.bn - 1) / o.bn;
     o.total_tiles = o.n_tiles[0] * mt;
     o.out = X;
     o.ldo = d;
@@ -188,6 +187,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
       tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, 128);
     }
     g.nseg = 1;
+    g.bn = 128;
     g.M = S;
     g.K = d;
     g.m_tiles = mt;
@@ -198,20 +198,21 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     // ---- down (+ residual) ----
     GemmParams& dn = ll.down;
     memset(&dn, 0, sizeof dn);
+    dn.bn = gemm_pick_bn(EPI_RESID, S, &d, 1, num_sms);
     tmap(&dn.a, Hb, S, F, 128);
-    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, 256);
+    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, dn.bn);
     dn.seg[0].n = d;
     dn.seg[0].lora = tt.lora_a[l][T_DOWN] >= 0;
     if (dn.seg[0].lora) {
       dn.lora_r = r;
       tmap(&dn.ta[0], T[T_DOWN], S, r, 128);
-      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, 256);
+      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, dn.bn);
     }
     dn.nseg = 1;
     dn.M = S;
     dn.K = F;
     dn.m_tiles = mt;
-    dn.n_tiles[0] = (d + GEMM_BN - 1) / GEMM_BN;
+    dn.n_tiles[0] = (d + dn.bn - 1) / dn.bn;
     dn.total_tiles = dn.n_tiles[0] * mt;
     dn.out = X;
     dn.ldo = d;
@@ -310,8 +311,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
     if (n) {
       const int e0 = P0();
       K(KC_SHRINK, e0, 2.0 * Sd * Kd * r * n, 2.0 * (Sd * Kd + (double)n * r * (Kd + Sd)),
-        lora_shrink_launch(X, ldx, S, Kd, A, T, n, r, a.lora_scale, ex.num_sms,
-                           ex.shrink_ws, ex.shrink_tickets, st),
+        lora_shrink_launch(X, ldx, S, Kd, A, T, n, r, a.lora_scale, st),
         "lora_shrink");
     }
   };

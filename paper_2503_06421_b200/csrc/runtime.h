@@ -45,8 +45,6 @@ struct Exec {
   unsigned long long* key = nullptr;
   int32_t* tok = nullptr;
   float2* rope = nullptr;
-  float* shrink_ws = nullptr;
-  unsigned int* shrink_tickets = nullptr;
   // pinned host staging
   int32_t* h_tok = nullptr;
   float* h_logits = nullptr;

@@ -1,11 +1,12 @@
 // shrink.cu — LoRA shrink T_t = scale * X A_t^T for the targets that share X
 // (q,k,v share Xn; gate,up share Xn; o reads O; down reads H).
-// A skinny product (r <= 64 per target, <= 3 targets): its cost is one read
-// of X [M, K], so the kernel reads X ONCE for all targets and splits K across
-// CTAs to put ~4 CTAs on every SM.  Each CTA (64 rows x K/ksplit) accumulates
-// with mma.sync m16n8k16 from a 2-stage cp.async ring, writes an fp32 partial
-// to a workspace, and the last CTA of each row tile (atomic ticket) reduces
-// the partials in a fixed order (deterministic) and stores bf16 T.
+// A skinny product (r <= 64 per target, <= 3 targets): its cost is one HBM
+// read of X [M, K], so the kernel reads X once for all targets.  CTA = 16 rows
+// x all targets; its 8 warps each own a K slice (intra-CTA split-K: every warp
+// streams its own X/A tiles through a private 2-stage cp.async ring and runs
+// mma.sync m16n8k16), then the 8 partials are summed through shared memory in
+// a fixed order (deterministic) and stored as bf16.  No workspace, no atomics,
+// one launch; ceil(M/16) CTAs (128 at S=2048).
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -16,10 +17,12 @@
 namespace tidal {
 namespace {
 
-constexpr int BM = 64, BK = 32, LD = 40, NTH = 128;
+constexpr int BM = 16, BK = 32, LD = 40;
+// warps per CTA (K slices): 8, or 4 for r = 64 so the rings fit in shared memory
+template <int R>
+constexpr int nwarps() { return R >= 64 ? 4 : 8; }
 
-__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, bool valid) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(smem);
+__device__ __forceinline__ void cp_async16(uint32_t s, const void* gmem, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem),
                "r"(valid ? 16 : 0)
                : "memory");
@@ -29,14 +32,12 @@ template <int N>
 __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
-__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], const void* p) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(p);
+__device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t s) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x4.shared.b16 {%0,%1,%2,%3}, [%4];"
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(s));
 }
-__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], const void* p) {
-  const uint32_t s = (uint32_t)__cvta_generic_to_shared(p);
+__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], uint32_t s) {
   asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
                : "=r"(r[0]), "=r"(r[1])
                : "r"(s));
@@ -56,39 +57,41 @@ struct Args {
 };
 
 template <int R>
-__global__ void __launch_bounds__(NTH) shrink_kernel(const bf16* __restrict__ X, int ldx, int M,
+__global__ void __launch_bounds__(nwarps<R>() * 32) shrink_kernel(const bf16* __restrict__ X, int ldx, int M,
                                                      int K, Args args, int nt, float scale,
-                                                     int kchunk, float* __restrict__ ws,
-                                                     unsigned int* __restrict__ tickets) {
-  extern __shared__ __align__(16) bf16 sm[];
-  bf16* xs = sm;                           // [2][BM*LD]
-  bf16* as = sm + 2 * BM * LD;             // [2][3*R*LD]
+                                                     int kslice) {
+  constexpr int NW = nwarps<R>(), NTH = NW * 32;
+  extern __shared__ __align__(16) uint8_t sm[];
   const int RT = nt * R;
-  const int m0 = blockIdx.x * BM;
-  const int ks = blockIdx.y, nks = gridDim.y;
-  const int kbeg = ks * kchunk, kend = min(K, kbeg + kchunk);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM;
+  // warp-private ring: [2 stages][(BM + RT) rows][LD]
+  const int wstride = 2 * (BM + RT) * LD * 2;  // bytes
+  const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(sm) + warp * wstride;
+  const int kbeg = warp * kslice, kend = min(K, kbeg + kslice);
+  const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   float acc[3][R / 8][4];
 #pragma unroll
   for (int t = 0; t < 3; ++t)
 #pragma unroll
     for (int i = 0; i < R / 8; ++i) acc[t][i][0] = acc[t][i][1] = acc[t][i][2] = acc[t][i][3] = 0.f;
-  const int nk = (kend - kbeg + BK - 1) / BK;
   auto load = [&](int kb, int buf) {
     const int k0 = kbeg + kb * BK;
-    for (int c = threadIdx.x; c < BM * 4; c += NTH) {
+    const uint32_t sb = wbase + buf * (BM + RT) * LD * 2;
+    for (int c = lane; c < (BM + RT) * 4; c += 32) {
       const int r = c >> 2, ch = c & 3;
-      const int m = m0 + r, k = k0 + ch * 8;
-      const bool ok = m < M && k < kend;
-      cp_async16(xs + buf * BM * LD + r * LD + ch * 8, ok ? X + (size_t)m * ldx + k : X, ok);
-    }
-    for (int c = threadIdx.x; c < RT * 4; c += NTH) {
-      const int r = c >> 2, ch = c & 3;
-      const int t = r / R, rr = r - t * R;
       const int k = k0 + ch * 8;
-      const bool ok = k < kend;
-      const bf16* A = args.A[t];
-      cp_async16(as + buf * 3 * R * LD + r * LD + ch * 8, ok ? A + (size_t)rr * K + k : A, ok);
+      const uint32_t dst = sb + (r * LD + ch * 8) * 2;
+      if (r < BM) {
+        const int m = m0 + r;
+        const bool ok = m < M && k < kend;
+        cp_async16(dst, ok ? X + (size_t)m * ldx + k : X, ok);
+      } else {
+        const int ra = r - BM, t = ra / R, rr = ra - t * R;
+        const bool ok = k < kend;
+        const bf16* A = args.A[t];
+        cp_async16(dst, ok ? A + (size_t)rr * K + k : A, ok);
+      }
     }
     cp_commit();
   };
@@ -101,103 +104,93 @@ __global__ void __launch_bounds__(NTH) shrink_kernel(const bf16* __restrict__ X,
     } else {
       cp_wait<0>();
     }
-    __syncthreads();
-    const bf16* xb = xs + buf * BM * LD;
-    const bf16* ab = as + buf * 3 * R * LD;
+    __syncwarp();
+    const uint32_t sb = wbase + buf * (BM + RT) * LD * 2;
 #pragma unroll
     for (int kk = 0; kk < BK / 16; ++kk) {
       uint32_t a[4];
-      ldsm_x4(a, xb + (warp * 16 + (lane & 15)) * LD + kk * 16 + (lane >> 4) * 8);
+      ldsm_x4(a, sb + ((lane & 15) * LD + kk * 16 + (lane >> 4) * 8) * 2);
 #pragma unroll
       for (int t = 0; t < 3; ++t) {
         if (t >= nt) break;
 #pragma unroll
         for (int n = 0; n < R / 8; ++n) {
           uint32_t b[2];
-          ldsm_x2(b, ab + (t * R + n * 8 + (lane & 7)) * LD + kk * 16 + ((lane >> 3) & 1) * 8);
+          ldsm_x2(b, sb + ((BM + t * R + n * 8 + (lane & 7)) * LD + kk * 16 +
+                           ((lane >> 3) & 1) * 8) * 2);
           mma16816(acc[t][n], a, b);
         }
       }
     }
-    __syncthreads();
+    __syncwarp();
   }
-  // fp32 partial -> workspace [nks][M][RT]
-  const int r0 = m0 + warp * 16 + (lane >> 2);
-  float* w = ws + (size_t)ks * M * RT;
+  // cross-warp reduction through shared memory (reuses the rings)
+  __syncthreads();
+  float* red = reinterpret_cast<float*>(sm);  // [NW][BM][RT]
+  const int r0 = lane >> 2;
 #pragma unroll
   for (int t = 0; t < 3; ++t) {
     if (t >= nt) break;
 #pragma unroll
     for (int n = 0; n < R / 8; ++n) {
       const int c = t * R + n * 8 + 2 * (lane & 3);
-      if (r0 < M) *reinterpret_cast<float2*>(w + (size_t)r0 * RT + c) = make_float2(acc[t][n][0], acc[t][n][1]);
-      if (r0 + 8 < M)
-        *reinterpret_cast<float2*>(w + (size_t)(r0 + 8) * RT + c) = make_float2(acc[t][n][2], acc[t][n][3]);
+      float* p = red + (size_t)warp * BM * RT;
+      p[r0 * RT + c] = acc[t][n][0];
+      p[r0 * RT + c + 1] = acc[t][n][1];
+      p[(r0 + 8) * RT + c] = acc[t][n][2];
+      p[(r0 + 8) * RT + c + 1] = acc[t][n][3];
     }
   }
-  __threadfence();
   __syncthreads();
-  __shared__ unsigned int last;
-  if (threadIdx.x == 0) last = atomicAdd(&tickets[blockIdx.x], 1u) == (unsigned)(nks - 1);
-  __syncthreads();
-  if (!last) return;
-  __threadfence();
-  const int rows = min(BM, M - m0);
-  for (int e = threadIdx.x; e < rows * RT; e += NTH) {
+  for (int e = threadIdx.x; e < BM * RT; e += NTH) {
     const int rr = e / RT, c = e - rr * RT;
-    const size_t off = (size_t)(m0 + rr) * RT + c;
+    const int m = m0 + rr;
+    if (m >= M) continue;
     float s = 0.f;
-    for (int k = 0; k < nks; ++k) s += __ldcg(ws + (size_t)k * M * RT + off);
+#pragma unroll
+    for (int w = 0; w < NW; ++w) s += red[(size_t)w * BM * RT + e];
     const int t = c / R;
-    args.T[t][(size_t)(m0 + rr) * R + (c - t * R)] = __float2bfloat16_rn(s * scale);
+    args.T[t][(size_t)m * R + (c - t * R)] = __float2bfloat16_rn(s * scale);
   }
-  if (threadIdx.x == 0) tickets[blockIdx.x] = 0;  // self-cleaning for the next launch
 }
 
 template <int R>
 cudaError_t launch(const bf16* X, int ldx, int M, int K, const Args& a, int nt, float scale,
-                   int ksplit, float* ws, unsigned int* tickets, cudaStream_t s) {
-  const int smem = (2 * BM * LD + 2 * 3 * R * LD) * 2;
+                   cudaStream_t s) {
+  constexpr int NW = nwarps<R>(), NTH = NW * 32;
+  const int ring = NW * 2 * (BM + 3 * R) * LD * 2;
+  const int redb = NW * BM * 3 * R * 4;
+  const int smem = ring > redb ? ring : redb;
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(shrink_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  int kchunk = (K + ksplit - 1) / ksplit;
-  kchunk = (kchunk + BK - 1) / BK * BK;
-  const int nks = (K + kchunk - 1) / kchunk;
-  dim3 grid((M + BM - 1) / BM, nks);
-  shrink_kernel<R><<<grid, NTH, smem, s>>>(X, ldx, M, K, a, nt, scale, kchunk, ws, tickets);
+  int kslice = (K + NW - 1) / NW;
+  kslice = (kslice + BK - 1) / BK * BK;
+  const int need_ring = NW * 2 * (BM + nt * R) * LD * 2;
+  const int need_red = NW * BM * nt * R * 4;
+  const int need = need_ring > need_red ? need_ring : need_red;
+  shrink_kernel<R><<<(M + BM - 1) / BM, NTH, need, s>>>(X, ldx, M, K, a, nt, scale, kslice);
   return cudaGetLastError();
 }
 
 }  // namespace
 
-int shrink_ksplit(int M, int K, int num_sms) {
-  const int mt = (M + BM - 1) / BM;
-  int ks = (4 * num_sms + mt - 1) / mt;
-  const int kmax = (K + 255) / 256;   // at least 256 K per CTA
-  if (ks > kmax) ks = kmax;
-  if (ks > SHRINK_MAX_KSPLIT) ks = SHRINK_MAX_KSPLIT;
-  return ks < 1 ? 1 : ks;
-}
-
 cudaError_t lora_shrink_launch(const bf16* X, int ldx, int M, int K, const bf16* const* A,
-                               bf16* const* T, int nt, int r, float scale, int num_sms,
-                               float* ws, unsigned int* tickets, cudaStream_t s) {
+                               bf16* const* T, int nt, int r, float scale, cudaStream_t s) {
   if (nt < 1 || nt > 3) return cudaErrorInvalidValue;
   Args a{};
   for (int i = 0; i < nt; ++i) {
     a.A[i] = A[i];
     a.T[i] = T[i];
   }
-  const int ks = shrink_ksplit(M, K, num_sms);
   switch (r) {
-    case 8: return launch<8>(X, ldx, M, K, a, nt, scale, ks, ws, tickets, s);
-    case 16: return launch<16>(X, ldx, M, K, a, nt, scale, ks, ws, tickets, s);
-    case 32: return launch<32>(X, ldx, M, K, a, nt, scale, ks, ws, tickets, s);
-    case 64: return launch<64>(X, ldx, M, K, a, nt, scale, ks, ws, tickets, s);
+    case 8: return launch<8>(X, ldx, M, K, a, nt, scale, s);
+    case 16: return launch<16>(X, ldx, M, K, a, nt, scale, s);
+    case 32: return launch<32>(X, ldx, M, K, a, nt, scale, s);
+    case 64: return launch<64>(X, ldx, M, K, a, nt, scale, s);
   }
   return cudaErrorInvalidValue;
 }

@@ -70,6 +70,28 @@ def test_gemm_residual_fp32(T, M, N, K):
     assert np.abs(X.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("bn", [128, 192, 256])
+@pytest.mark.parametrize("epi", [0, 3])
+def test_gemm_tile_widths(T, bn, epi):
+    """Every N-tile width the runtime may pick (gemm_pick_bn), with a ragged
+    N tail (N = 5*bn - 64) and LoRA, for the store and residual epilogues."""
+    rng = np.random.default_rng(bn + epi)
+    M, K, r = 260, 512, 16
+    N = 5 * bn - 64
+    A, W = _bf(rng, (M, K)), _bf(rng, (N, K), 1 / math.sqrt(K))
+    Tm, B = _bf(rng, (M, r)), _bf(rng, (N, r), 0.3)
+    ref = A @ W.T + Tm @ B.T
+    if epi == 0:
+        out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+        T.k_gemm(epi | (bn << 8), _dev(A), [_dev(W)], [N], out, N, M, K, [_dev(Tm)], [_dev(B)], r)
+        _close_bf16(_host(out), ref)
+    else:
+        X0 = rng.standard_normal((M, N)).astype(np.float32)
+        X = torch.from_numpy(X0.copy()).cuda()
+        T.k_gemm(epi | (bn << 8), _dev(A), [_dev(W)], [N], X, N, M, K, [_dev(Tm)], [_dev(B)], r)
+        assert np.abs(X.cpu().numpy() - (X0 + ref)).max() <= 2e-4 * np.abs(X0 + ref).max()
+
+
 @pytest.mark.parametrize("r", [8, 16, 64])
 def test_gemm_lora_k_extension(T, r):
     rng = np.random.default_rng(r)
