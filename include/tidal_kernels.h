@@ -27,6 +27,10 @@ tidal_status tidal_k_lora_shrink(const void* X, int M, int K, const void* A, voi
                                  float scale);
 /* O[S,H*hd] = causal GQA attention over QKV[S,(H+2KV)*hd]; hd in {64,128}. */
 tidal_status tidal_k_attention(const void* qkv, void* O, int S, int H, int KV, int hd);
+/* The tcgen05 attention used for hd = 128: Q, K from qkv[S,(H+2KV)*128]; V given
+ * transposed, vt[KV*128][vt_ld] (vt_ld >= S, multiple of 8). */
+tidal_status tidal_k_attention_tc(const void* qkv, const void* vt, int vt_ld, void* O, int S, int H,
+                                  int KV);
 /* logits[V] = W[V,d] . RMSNorm(xlast; g), *key = packed argmax (see tidal.h). */
 tidal_status tidal_k_head(const float* xlast, const void* g, const void* W, int V, int d, float eps,
                           float* logits, unsigned long long* key);

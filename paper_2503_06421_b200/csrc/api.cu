@@ -809,6 +809,18 @@ tidal_status tidal_k_attention(const void* qkv, void* O, int S, int H, int KV, i
   return sync_status(attention_launch((const bf16*)qkv, (bf16*)O, S, H, KV, hd, 0), "attention");
 }
 
+tidal_status tidal_k_attention_tc(const void* qkv, const void* vt, int vt_ld, void* O, int S, int H,
+                                  int KV) {
+  TIDAL_TRY
+  AttnParams p;
+  memset(&p, 0, sizeof p);
+  require(attn_tc_params(&p, (const bf16*)qkv, (const bf16*)vt, vt_ld, (bf16*)O, S, H, KV),
+          "attention tensor maps");
+  tidal_status s = sync_status(attn_tc_launch(p, 0), "attention_tc");
+  if (s != TIDAL_OK) return s;
+  TIDAL_CATCH
+}
+
 tidal_status tidal_k_head(const float* xlast, const void* g, const void* W, int V, int d, float eps,
                           float* logits, unsigned long long* key) {
   cudaError_t e = cudaMemset(key, 0, 8);

@@ -1,0 +1,263 @@
+// attn_tc.cu — causal GQA prefill attention on 5th-gen tensor cores (hd = 128).
+//   O_h = softmax(Q_h K_g^T / sqrt(hd) + causal) V_g,   g = h / (H / KV)
+// CTA = 128 queries of one head; warp-specialised like the GEMM:
+//   warp 0      TMA: Q once, then K / V^T tiles of 128 keys (2-stage ring)
+//   warp 1      tcgen05.mma: S_j = Q K_j^T into TMEM (double-buffered, so
+//               S_{j+1} runs while softmax works on S_j), then O += P_j V_j
+//   warps 2..5  softmax, one query row per thread (TMEM lane = row): row max,
+//               P = exp2(S*scale - m) rounded to bf16 into a SWIZZLE_128B smem
+//               tile (the A operand of the PV MMA), running row sum in fp32.
+//               O lives in TMEM for the whole CTA; it is rescaled only when a
+//               row max grows by more than 2^8 (exact: O and l share the same
+//               stale max, P <= 256 cannot overflow), then O / l -> bf16.
+// V is consumed as V^T [hd][S] (written transposed by the QKV GEMM epilogue),
+// so both MMAs read K-major operands.
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace tidal {
+namespace {
+
+constexpr int HD = 128, BQ = 128, BKV = 128;
+constexpr int TILE = 128 * 128 * 2;  // 32 KB: any 128 x 128 bf16 tile (two 64-wide K-blocks)
+constexpr int HALF = TILE / 2;
+constexpr int OFF_Q = 0, OFF_K = OFF_Q + TILE, OFF_V = OFF_K + 2 * TILE, OFF_P = OFF_V + 2 * TILE;
+constexpr int OFF_BAR = OFF_P + TILE;
+constexpr int N_BARS = 10;
+constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
+constexpr int SMEM = OFF_TMEM + 16 + 1024;
+constexpr int NTH = 192;
+constexpr uint32_t COL_S0 = 0, COL_O = 256;
+
+__device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
+  __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
+  return *reinterpret_cast<uint32_t*>(&v);
+}
+
+__global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
+                                             ~uintptr_t(1023));
+  const uint32_t sb = ptx::smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bars = sb + OFF_BAR;
+  const uint32_t q_full = bars, p_full = bars + 8, pv_done = bars + 16;
+  auto kv_full = [&](int s) { return bars + 24 + 8u * s; };
+  auto kv_empty = [&](int s) { return bars + 40 + 8u * s; };
+  auto s_full = [&](int s) { return bars + 56 + 8u * s; };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+
+  const int nq = (p.S + BQ - 1) / BQ;
+  const int qt = nq - 1 - (int)blockIdx.x;  // heavy (late) query tiles first
+  const int h = blockIdx.y;
+  const int g = h / (p.H / p.KV);
+  const int q0 = qt * BQ;
+  const int nkv = qt + 1;                   // causal: key tiles 0..qt (BQ == BKV)
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&p.qkv);
+    ptx::prefetch_tmap(&p.vt);
+    ptx::mbar_init(q_full, 1);
+    ptx::mbar_init(p_full, 128);
+    ptx::mbar_init(pv_done, 1);
+    for (int s = 0; s < 2; ++s) {
+      ptx::mbar_init(kv_full(s), 1);
+      ptx::mbar_init(kv_empty(s), 1);
+      ptx::mbar_init(s_full(s), 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const int qc = h * HD, kc = (p.H + g) * HD, vr = g * HD;
+      ptx::mbar_expect_tx(q_full, TILE);
+      ptx::tma_load_2d(&p.qkv, sb + OFF_Q, q_full, qc, q0);
+      ptx::tma_load_2d(&p.qkv, sb + OFF_Q + HALF, q_full, qc + 64, q0);
+      for (int j = 0; j < nkv; ++j) {
+        const int s = j & 1;
+        ptx::mbar_wait(kv_empty(s), ((j >> 1) & 1) ^ 1);
+        const uint32_t fb = kv_full(s);
+        ptx::mbar_expect_tx(fb, 2 * TILE);
+        const uint32_t ks = sb + OFF_K + s * TILE, vs = sb + OFF_V + s * TILE;
+        ptx::tma_load_2d(&p.qkv, ks, fb, kc, j * BKV);
+        ptx::tma_load_2d(&p.qkv, ks + HALF, fb, kc + 64, j * BKV);
+        ptx::tma_load_2d(&p.vt, vs, fb, j * BKV, vr);
+        ptx::tma_load_2d(&p.vt, vs + HALF, fb, j * BKV + 64, vr);
+      }
+    }
+    __syncwarp();
+  } else if (warp == 1) {
+    if (lane == 0) {
+      constexpr uint32_t IDESC = ptx::idesc_bf16(128, 128);
+      ptx::mbar_wait(q_full, 0);
+      auto issue_s = [&](int j) {
+        const int s = j & 1;
+        ptx::mbar_wait(kv_full(s), (j >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t ks = sb + OFF_K + s * TILE;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * HALF;
+          ptx::mma_bf16(tmem + COL_S0 + s * 128, ptx::desc_sw128(sb + OFF_Q + off) + 2 * (kk & 3),
+                        ptx::desc_sw128(ks + off) + 2 * (kk & 3), IDESC, kk > 0);
+        }
+        ptx::mma_commit(s_full(s));
+      };
+      issue_s(0);
+      for (int j = 0; j < nkv; ++j) {
+        if (j + 1 < nkv) issue_s(j + 1);
+        ptx::mbar_wait(p_full, j & 1);
+        ptx::tc_fence_after();
+        const uint32_t vs = sb + OFF_V + (j & 1) * TILE;
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * HALF;
+          ptx::mma_bf16(tmem + COL_O, ptx::desc_sw128(sb + OFF_P + off) + 2 * (kk & 3),
+                        ptx::desc_sw128(vs + off) + 2 * (kk & 3), IDESC, (j | kk) != 0);
+        }
+        ptx::mma_commit(kv_empty(j & 1));
+        ptx::mma_commit(pv_done);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ===================== softmax warps =====================
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const int qi = q0 + row;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    uint8_t* Ps = smem + OFF_P;
+    float m_used = -INFINITY, l = 0.f;
+    for (int j = 0; j < nkv; ++j) {
+      ptx::mbar_wait(s_full(j & 1), (j >> 1) & 1);
+      ptx::tc_fence_after();
+      float v[128];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(tmem + lane_base + COL_S0 + (j & 1) * 128 + c * 32, r);
+        ptx::tmem_ld_wait();
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]) * p.scale_log2;
+      }
+      if (j == qt) {  // diagonal tile: causal mask
+#pragma unroll
+        for (int i = 0; i < 128; ++i)
+          if (j * BKV + i > qi) v[i] = -INFINITY;
+      }
+      float mx = m_used;
+#pragma unroll
+      for (int i = 0; i < 128; ++i) mx = fmaxf(mx, v[i]);
+      const bool need = mx > m_used + 8.f;
+      if (j > 0) ptx::mbar_wait(pv_done, (j - 1) & 1);  // P buffer free, O settled
+      if (j > 0 && __any_sync(0xffffffffu, need)) {
+        ptx::tc_fence_after();
+        const float corr = need ? exp2f(m_used - mx) : 1.f;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          const uint32_t ta = tmem + lane_base + COL_O + c * 32;
+          ptx::tmem_ld32(ta, r);
+          ptx::tmem_ld_wait();
+#pragma unroll
+          for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
+          ptx::tmem_st32(ta, r);
+        }
+        ptx::tmem_st_wait();
+        l *= corr;
+      }
+      if (need) m_used = mx;
+      // P = exp2(v - m) -> bf16, SWIZZLE_128B K-major tile (two 64-key blocks)
+#pragma unroll
+      for (int c = 0; c < 16; ++c) {
+        float e[8];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          e[i] = exp2f(v[c * 8 + i] - m_used);
+          l += e[i];
+        }
+        uint4 w;
+        w.x = pack_bf16x2(e[0], e[1]);
+        w.y = pack_bf16x2(e[2], e[3]);
+        w.z = pack_bf16x2(e[4], e[5]);
+        w.w = pack_bf16x2(e[6], e[7]);
+        const int blk = c >> 3, ch = c & 7;
+        *reinterpret_cast<uint4*>(Ps + blk * HALF + row * 128 + ((ch ^ (row & 7)) << 4)) = w;
+      }
+      ptx::fence_proxy_async_smem();
+      ptx::tc_fence_before();
+      ptx::mbar_arrive(p_full);
+    }
+    // epilogue: O / l -> bf16
+    ptx::mbar_wait(pv_done, (nkv - 1) & 1);
+    ptx::tc_fence_after();
+    const float inv = 1.f / l;
+    bf16* out = p.out + (size_t)qi * p.ldo + h * HD;
+#pragma unroll 1
+    for (int c = 0; c < 4; ++c) {
+      uint32_t r[32];
+      ptx::tmem_ld32(tmem + lane_base + COL_O + c * 32, r);
+      ptx::tmem_ld_wait();
+      if (qi < p.S) {
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          uint4 w;
+          w.x = pack_bf16x2(__uint_as_float(r[8 * k + 0]) * inv, __uint_as_float(r[8 * k + 1]) * inv);
+          w.y = pack_bf16x2(__uint_as_float(r[8 * k + 2]) * inv, __uint_as_float(r[8 * k + 3]) * inv);
+          w.z = pack_bf16x2(__uint_as_float(r[8 * k + 4]) * inv, __uint_as_float(r[8 * k + 5]) * inv);
+          w.w = pack_bf16x2(__uint_as_float(r[8 * k + 6]) * inv, __uint_as_float(r[8 * k + 7]) * inv);
+          *reinterpret_cast<uint4*>(out + c * 32 + k * 8) = w;
+        }
+      }
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
+}  // namespace
+
+bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, bf16* out, int S,
+                    int H, int KV) {
+  const int ld = (H + 2 * KV) * HD;
+  if (!make_tmap(&p->qkv, qkv, S, ld, (uint64_t)ld * 2, 128, 64)) return false;
+  if (!make_tmap(&p->vt, vt, (uint64_t)KV * HD, S, (uint64_t)vt_ld * 2, 128, 64)) return false;
+  p->S = S;
+  p->H = H;
+  p->KV = KV;
+  p->scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
+  p->out = out;
+  p->ldo = H * HD;
+  return true;
+}
+
+cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e =
+        cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  dim3 grid((p.S + BQ - 1) / BQ, p.H);
+  attn_tc_kernel<<<grid, NTH, SMEM, s>>>(p);
+  return cudaGetLastError();
+}
+
+}  // namespace tidal

@@ -347,6 +347,14 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           ld_chunk(tacc + j * 32, v);
           store_chunk_bf16(v, stg, lane, reinterpret_cast<bf16*>(p.out), p.ldo, row0, p.M,
                            sg.out_col + n0 + j * 32, ncols - j * 32);
+          if (EPI == EPI_ROPE && sg.vt && m < p.M) {
+            // V^T for the tcgen05 attention: lanes are consecutive tokens -> coalesced
+            bf16* dst = p.vt + (size_t)(n0 + j * 32) * p.vt_ld + m;
+            const int nv = min(32, ncols - j * 32);
+#pragma unroll
+            for (int i = 0; i < 32; ++i)
+              if (i < nv) dst[(size_t)i * p.vt_ld] = __float2bfloat16_rn(v[i]);
+          }
         }
       }
       ptx::tc_fence_before();

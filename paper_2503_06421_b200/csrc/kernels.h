@@ -30,6 +30,7 @@ struct GemmSeg {
   int out_col;  // first output column
   int lora;     // LoRA K-extension present for this segment
   int rope;     // EPI_ROPE: rotate this segment
+  int vt;       // EPI_ROPE: also store this segment transposed into GemmParams::vt
 };
 
 struct alignas(64) GemmParams {
@@ -49,7 +50,23 @@ struct alignas(64) GemmParams {
   const float2* rope;  // [S, head_dim/2] (cos, sin)
   int head_dim;
   int bn;              // N tile: 256 | 192 | 128 (EPI_SILU: 128 output cols = 256 acc cols)
+  bf16* vt;            // V^T [n_vt][vt_ld] for the tcgen05 attention (segments with vt=1)
+  int vt_ld;
 };
+
+// tcgen05 causal attention (hd = 128): Q/K from QKV [S, (H+2KV)*128], V from
+// V^T [KV*128][vt_ld] (written by the QKV epilogue).
+struct alignas(64) AttnParams {
+  CUtensorMap qkv;  // box {64, 128}
+  CUtensorMap vt;   // box {64 keys, 128 rows}
+  int S, H, KV;
+  float scale_log2;
+  bf16* out;
+  int ldo;
+};
+bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, bf16* out, int S,
+                    int H, int KV);
+cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s);
 
 // N-tile width minimising (waves x tile width) on num_sms SMs; the W/lora_B
 // tensor maps must use box rows = the returned value (128 for EPI_SILU).

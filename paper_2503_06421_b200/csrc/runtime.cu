@@ -60,6 +60,8 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   dalloc(logits, (size_t)m.vocab * 4);
   dalloc(key, 64);
   dalloc(tok, S * 4);
+  vt_ld = (int)((S + 63) / 64 * 64);
+  dalloc(Vt, nkv * (size_t)vt_ld * 2);
   // RoPE table: angle = pos * theta^(-2i/hd), cos/sin in double, stored fp32
   std::vector<float2> cs(S * (hd / 2));
   for (size_t p = 0; p < S; ++p)
@@ -82,7 +84,7 @@ void Exec::destroy() {
   cudaSetDevice(device);
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
-  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope};
+  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int t = 0; t < kNumTargets; ++t)
@@ -143,6 +145,9 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
       q.total_tiles += q.n_tiles[s] * mt;
     }
     q.nseg = 3;
+    q.seg[2].vt = hd == 128;  // V^T for the tcgen05 attention
+    q.vt = Vt;
+    q.vt_ld = vt_ld;
     q.M = S;
     q.K = d;
     q.m_tiles = mt;
@@ -255,6 +260,18 @@ void Exec::prof_collect() {
     t.launches += 1;
   }
   prof_pending.clear();
+}
+
+cudaError_t Exec::attention_tc(int S, cudaStream_t s) {
+  auto it = attn_cache.find(S);
+  if (it == attn_cache.end()) {
+    AttnParams p;
+    memset(&p, 0, sizeof p);
+    if (!attn_tc_params(&p, QKV, Vt, vt_ld, O, S, m.n_heads / world, m.n_kv_heads / world))
+      fail(3, "attention tensor maps");
+    it = attn_cache.emplace(S, p).first;
+  }
+  return attn_tc_launch(it->second, s);
 }
 
 enum OpKind {
@@ -378,7 +395,9 @@ void run_forward(Exec& ex, const RunArgs& a) {
           const int e0 = P0();
           K(KC_ATTN, e0, 2.0 * hd * ((double)m.n_heads / ex.world) * Sd * (Sd + 1),
             2.0 * Sd * (2.0 * nq + 2.0 * nkv),
-            attention_launch(ex.QKV, ex.O, S, m.n_heads / ex.world, m.n_kv_heads / ex.world, hd, st),
+            hd == 128 ? ex.attention_tc(S, st)
+                      : attention_launch(ex.QKV, ex.O, S, m.n_heads / ex.world,
+                                         m.n_kv_heads / ex.world, hd, st),
             "attention");
         }
         break;

@@ -45,6 +45,9 @@ struct Exec {
   unsigned long long* key = nullptr;
   int32_t* tok = nullptr;
   float2* rope = nullptr;
+  bf16* Vt = nullptr;  // V^T [KV*hd][vt_ld] (tcgen05 attention, hd = 128)
+  int vt_ld = 0;
+  std::map<int, AttnParams> attn_cache;  // per prompt length
   // pinned host staging
   int32_t* h_tok = nullptr;
   float* h_logits = nullptr;
@@ -78,6 +81,7 @@ struct Exec {
   void destroy();
   const std::vector<LayerLaunch>& layer_params(const TensorTable& tt, int S, const void* akey,
                                                uint64_t gen);
+  cudaError_t attention_tc(int S, cudaStream_t s);
 };
 
 enum KernelClass {

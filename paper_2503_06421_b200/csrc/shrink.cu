@@ -1,12 +1,13 @@
 // shrink.cu — LoRA shrink T_t = scale * X A_t^T for the targets that share X
 // (q,k,v share Xn; gate,up share Xn; o reads O; down reads H).
-// A skinny product (r <= 64 per target, <= 3 targets): its cost is one HBM
-// read of X [M, K], so the kernel reads X once for all targets.  CTA = 16 rows
-// x all targets; its 8 warps each own a K slice (intra-CTA split-K: every warp
-// streams its own X/A tiles through a private 2-stage cp.async ring and runs
-// mma.sync m16n8k16), then the 8 partials are summed through shared memory in
-// a fixed order (deterministic) and stored as bf16.  No workspace, no atomics,
-// one launch; ceil(M/16) CTAs (128 at S=2048).
+// A skinny product (r <= 64 per target, <= 3 targets) whose cost is moving X
+// (once, from HBM) and A (from L2, once per CTA), so it is latency-bound unless
+// enough bytes are in flight: CTA = 16 rows x all targets, its warps each own
+// a K slice (intra-CTA split-K) and stream X/A tiles of 64 K-columns through a
+// private STG-deep cp.async ring (~100+ KB in flight per SM), mma.sync
+// m16n8k16 accumulates, and the per-warp partials are summed through shared
+// memory in a fixed order (deterministic) and stored as bf16.  One launch, no
+// workspace, ceil(M/16) CTAs.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -17,10 +18,13 @@
 namespace tidal {
 namespace {
 
-constexpr int BM = 16, BK = 32, LD = 40;
-// warps per CTA (K slices): 8, or 4 for r = 64 so the rings fit in shared memory
+constexpr int BM = 16, BK = 64, LD = BK + 8;  // smem row stride (elements): conflict-free ldmatrix
+
 template <int R>
-constexpr int nwarps() { return R >= 64 ? 4 : 8; }
+struct Cfg {
+  static constexpr int NW = R >= 64 ? 2 : 4;               // warps (K slices) per CTA
+  static constexpr int STG = R >= 32 ? 3 : (R >= 16 ? 4 : 6);  // ring depth per warp
+};
 
 __device__ __forceinline__ void cp_async16(uint32_t s, const void* gmem, bool valid) {
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(s), "l"(gmem),
@@ -37,18 +41,13 @@ __device__ __forceinline__ void ldsm_x4(uint32_t (&r)[4], uint32_t s) {
                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
                : "r"(s));
 }
-__device__ __forceinline__ void ldsm_x2(uint32_t (&r)[2], uint32_t s) {
-  asm volatile("ldmatrix.sync.aligned.m8n8.x2.shared.b16 {%0,%1}, [%2];"
-               : "=r"(r[0]), "=r"(r[1])
-               : "r"(s));
-}
-__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4],
-                                         const uint32_t (&b)[2]) {
+__device__ __forceinline__ void mma16816(float (&c)[4], const uint32_t (&a)[4], uint32_t b0,
+                                         uint32_t b1) {
   asm volatile(
       "mma.sync.aligned.m16n8k16.row.col.f32.bf16.bf16.f32 {%0,%1,%2,%3}, {%4,%5,%6,%7}, "
       "{%8,%9}, {%0,%1,%2,%3};"
       : "+f"(c[0]), "+f"(c[1]), "+f"(c[2]), "+f"(c[3])
-      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b[0]), "r"(b[1]));
+      : "r"(a[0]), "r"(a[1]), "r"(a[2]), "r"(a[3]), "r"(b0), "r"(b1));
 }
 
 struct Args {
@@ -57,17 +56,16 @@ struct Args {
 };
 
 template <int R>
-__global__ void __launch_bounds__(nwarps<R>() * 32) shrink_kernel(const bf16* __restrict__ X, int ldx, int M,
-                                                     int K, Args args, int nt, float scale,
-                                                     int kslice) {
-  constexpr int NW = nwarps<R>(), NTH = NW * 32;
+__global__ void __launch_bounds__(Cfg<R>::NW * 32) shrink_kernel(const bf16* __restrict__ X,
+                                                                 int ldx, int M, int K, Args args,
+                                                                 int nt, float scale, int kslice) {
+  constexpr int NW = Cfg<R>::NW, STG = Cfg<R>::STG, NTH = NW * 32;
   extern __shared__ __align__(16) uint8_t sm[];
   const int RT = nt * R;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.x * BM;
-  // warp-private ring: [2 stages][(BM + RT) rows][LD]
-  const int wstride = 2 * (BM + RT) * LD * 2;  // bytes
-  const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(sm) + warp * wstride;
+  const int stage_bytes = (BM + RT) * LD * 2;
+  const uint32_t wbase = (uint32_t)__cvta_generic_to_shared(sm) + warp * STG * stage_bytes;
   const int kbeg = warp * kslice, kend = min(K, kbeg + kslice);
   const int nk = kend > kbeg ? (kend - kbeg + BK - 1) / BK : 0;
   float acc[3][R / 8][4];
@@ -75,37 +73,35 @@ __global__ void __launch_bounds__(nwarps<R>() * 32) shrink_kernel(const bf16* __
   for (int t = 0; t < 3; ++t)
 #pragma unroll
     for (int i = 0; i < R / 8; ++i) acc[t][i][0] = acc[t][i][1] = acc[t][i][2] = acc[t][i][3] = 0.f;
-  auto load = [&](int kb, int buf) {
-    const int k0 = kbeg + kb * BK;
-    const uint32_t sb = wbase + buf * (BM + RT) * LD * 2;
-    for (int c = lane; c < (BM + RT) * 4; c += 32) {
-      const int r = c >> 2, ch = c & 3;
-      const int k = k0 + ch * 8;
-      const uint32_t dst = sb + (r * LD + ch * 8) * 2;
-      if (r < BM) {
-        const int m = m0 + r;
-        const bool ok = m < M && k < kend;
-        cp_async16(dst, ok ? X + (size_t)m * ldx + k : X, ok);
-      } else {
-        const int ra = r - BM, t = ra / R, rr = ra - t * R;
-        const bool ok = k < kend;
-        const bf16* A = args.A[t];
-        cp_async16(dst, ok ? A + (size_t)rr * K + k : A, ok);
+  auto load = [&](int kb) {
+    if (kb < nk) {
+      const int k0 = kbeg + kb * BK;
+      const uint32_t sb = wbase + (kb % STG) * stage_bytes;
+      for (int c = lane; c < (BM + RT) * 8; c += 32) {
+        const int r = c >> 3, ch = c & 7;
+        const int k = k0 + ch * 8;
+        const uint32_t dst = sb + (r * LD + ch * 8) * 2;
+        if (r < BM) {
+          const int m = m0 + r;
+          const bool ok = m < M && k < kend;
+          cp_async16(dst, ok ? X + (size_t)m * ldx + k : X, ok);
+        } else {
+          const int ra = r - BM, t = ra / R, rr = ra - t * R;
+          const bool ok = k < kend;
+          const bf16* A = args.A[t];
+          cp_async16(dst, ok ? A + (size_t)rr * K + k : A, ok);
+        }
       }
     }
-    cp_commit();
+    cp_commit();  // always commit: uniform group accounting
   };
-  if (nk > 0) load(0, 0);
+#pragma unroll
+  for (int s = 0; s < STG - 1; ++s) load(s);
   for (int kb = 0; kb < nk; ++kb) {
-    const int buf = kb & 1;
-    if (kb + 1 < nk) {
-      load(kb + 1, buf ^ 1);
-      cp_wait<1>();
-    } else {
-      cp_wait<0>();
-    }
+    load(kb + STG - 1);
+    cp_wait<STG - 1>();
     __syncwarp();
-    const uint32_t sb = wbase + buf * (BM + RT) * LD * 2;
+    const uint32_t sb = wbase + (kb % STG) * stage_bytes;
 #pragma unroll
     for (int kk = 0; kk < BK / 16; ++kk) {
       uint32_t a[4];
@@ -114,16 +110,26 @@ __global__ void __launch_bounds__(nwarps<R>() * 32) shrink_kernel(const bf16* __
       for (int t = 0; t < 3; ++t) {
         if (t >= nt) break;
 #pragma unroll
-        for (int n = 0; n < R / 8; ++n) {
-          uint32_t b[2];
-          ldsm_x2(b, sb + ((BM + t * R + n * 8 + (lane & 7)) * LD + kk * 16 +
-                           ((lane >> 3) & 1) * 8) * 2);
-          mma16816(acc[t][n], a, b);
+        for (int n = 0; n < R / 8; n += 2) {
+          if (R == 8) {
+            uint32_t b[4];
+            // x4 over one 8-row n-tile: k lo/hi for this kk (matrices 2,3 unused)
+            ldsm_x4(b, sb + ((BM + t * R + (lane & 7)) * LD + kk * 16 + ((lane >> 3) & 1) * 8) * 2);
+            mma16816(acc[t][0], a, b[0], b[1]);
+          } else {
+            uint32_t b[4];
+            // x4: n-tiles n and n+1, k lo/hi
+            ldsm_x4(b, sb + ((BM + t * R + n * 8 + (lane & 7) + ((lane >> 4) << 3)) * LD + kk * 16 +
+                             ((lane >> 3) & 1) * 8) * 2);
+            mma16816(acc[t][n], a, b[0], b[1]);
+            mma16816(acc[t][n + 1], a, b[2], b[3]);
+          }
         }
       }
     }
     __syncwarp();
   }
+  cp_wait<0>();
   // cross-warp reduction through shared memory (reuses the rings)
   __syncthreads();
   float* red = reinterpret_cast<float*>(sm);  // [NW][BM][RT]
@@ -157,22 +163,21 @@ __global__ void __launch_bounds__(nwarps<R>() * 32) shrink_kernel(const bf16* __
 template <int R>
 cudaError_t launch(const bf16* X, int ldx, int M, int K, const Args& a, int nt, float scale,
                    cudaStream_t s) {
-  constexpr int NW = nwarps<R>(), NTH = NW * 32;
-  const int ring = NW * 2 * (BM + 3 * R) * LD * 2;
-  const int redb = NW * BM * 3 * R * 4;
-  const int smem = ring > redb ? ring : redb;
+  constexpr int NW = Cfg<R>::NW, STG = Cfg<R>::STG;
   static bool attr = false;
   if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(shrink_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+    const int maxb = NW * STG * (BM + 3 * R) * LD * 2;
+    cudaError_t e =
+        cudaFuncSetAttribute(shrink_kernel<R>, cudaFuncAttributeMaxDynamicSharedMemorySize, maxb);
     if (e != cudaSuccess) return e;
     attr = true;
   }
   int kslice = (K + NW - 1) / NW;
   kslice = (kslice + BK - 1) / BK * BK;
-  const int need_ring = NW * 2 * (BM + nt * R) * LD * 2;
-  const int need_red = NW * BM * nt * R * 4;
-  const int need = need_ring > need_red ? need_ring : need_red;
-  shrink_kernel<R><<<(M + BM - 1) / BM, NTH, need, s>>>(X, ldx, M, K, a, nt, scale, kslice);
+  const int ring = NW * STG * (BM + nt * R) * LD * 2;
+  const int redb = NW * BM * nt * R * 4;
+  const int need = ring > redb ? ring : redb;
+  shrink_kernel<R><<<(M + BM - 1) / BM, NW * 32, need, s>>>(X, ldx, M, K, a, nt, scale, kslice);
   return cudaGetLastError();
 }
 

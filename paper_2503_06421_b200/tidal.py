@@ -109,6 +109,7 @@ SIGNATURES = [
     ("tidal_k_lora_shrink", C.c_int, [VP, C.c_int, C.c_int, VP, VP, C.c_int, C.c_float]),
     ("tidal_k_attention", C.c_int, [VP, VP, C.c_int, C.c_int, C.c_int, C.c_int]),
     ("tidal_k_head", C.c_int, [VP, VP, VP, C.c_int, C.c_int, C.c_float, VP, VP]),
+    ("tidal_k_attention_tc", C.c_int, [VP, VP, C.c_int, VP, C.c_int, C.c_int, C.c_int]),
     ("tidal_k_gemm", C.c_int, [C.c_int, VP, C.POINTER(VP), C.POINTER(C.c_int), C.c_int, VP,
                                C.c_int, C.c_int, C.c_int, C.POINTER(VP), C.POINTER(VP), C.c_int,
                                VP, C.c_int]),
@@ -355,6 +356,10 @@ def k_lora_shrink(X, M, K, A, T, r, scale):
 
 def k_attention(qkv, O, S, H, KV, hd):
     _check(lib().tidal_k_attention(_ptr(qkv), _ptr(O), S, H, KV, hd))
+
+
+def k_attention_tc(qkv, vt, vt_ld, O, S, H, KV):
+    _check(lib().tidal_k_attention_tc(_ptr(qkv), _ptr(vt), vt_ld, _ptr(O), S, H, KV))
 
 
 def k_head(xlast, g, W, V, d, eps, logits, key):

@@ -158,6 +158,42 @@ def test_attention_causal_gqa(T, S, H, KV, hd):
     assert err <= 2e-2, err
 
 
+@pytest.mark.parametrize("S,H,KV", [(1, 2, 1), (128, 2, 2), (300, 4, 2), (1000, 3, 1), (2048, 2, 2)])
+def test_attention_tcgen05(T, S, H, KV):
+    """The tcgen05/TMEM attention (hd = 128) against the oracle; V passed
+    transposed as the QKV epilogue writes it."""
+    hd = 128
+    rng = np.random.default_rng(S * 7 + H)
+    qkv = _bf(rng, (S, (H + 2 * KV) * hd))
+    q = qkv[:, :H * hd].reshape(S, H, hd)
+    k = qkv[:, H * hd:(H + KV) * hd].reshape(S, KV, hd)
+    v = qkv[:, (H + KV) * hd:].reshape(S, KV, hd)
+    vt_ld = (S + 63) // 64 * 64
+    vt = np.zeros((KV * hd, vt_ld), np.float32)
+    vt[:, :S] = v.reshape(S, KV * hd).T
+    O = torch.zeros(S, H * hd, dtype=torch.bfloat16, device="cuda")
+    T.k_attention_tc(_dev(qkv), _dev(vt), vt_ld, O, S, H, KV)
+    ref = F.causal_attention(q, k, v)
+    err = np.abs(_host(O) - ref).max()
+    assert err <= 2e-2, err
+
+
+def test_attention_tcgen05_large_logits(T):
+    """Scores spanning > 2^8 in exp2 units exercise the lazy O rescale."""
+    S, H, KV, hd = 512, 1, 1, 128
+    rng = np.random.default_rng(11)
+    qkv = _bf(rng, (S, 3 * hd))
+    qkv[:, :hd] *= 4.0                               # sharp, growing maxima
+    qkv[:, hd:2 * hd] *= np.linspace(0.2, 4.0, S)[:, None]
+    qkv = synth.bf16_bits_to_f32(synth.f32_to_bf16_bits(qkv)).reshape(qkv.shape)
+    q, k, v = qkv[:, :hd].reshape(S, 1, hd), qkv[:, hd:2 * hd].reshape(S, 1, hd), qkv[:, 2 * hd:].reshape(S, 1, hd)
+    vt = np.ascontiguousarray(v.reshape(S, hd).T)
+    O = torch.zeros(S, hd, dtype=torch.bfloat16, device="cuda")
+    T.k_attention_tc(_dev(qkv), _dev(vt), S, O, S, H, KV)
+    ref = F.causal_attention(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64))
+    assert np.abs(_host(O) - ref).max() <= 2e-2
+
+
 @pytest.mark.parametrize("S,d", [(1, 256), (37, 5120), (16, 4096)])
 def test_rmsnorm(T, S, d):
     rng = np.random.default_rng(d)
