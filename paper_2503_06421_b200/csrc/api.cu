@@ -801,8 +801,16 @@ tidal_status tidal_k_lora_shrink(const void* X, int M, int K, const void* A, voi
                                  float scale) {
   const bf16* As[1] = {(const bf16*)A};
   bf16* Ts[1] = {(bf16*)T};
-  return sync_status(lora_shrink_launch((const bf16*)X, K, M, K, As, Ts, 1, r, scale, 0),
-                     "shrink");
+  TIDAL_TRY
+  float* ws = nullptr;
+  cuda_check(cudaMalloc(&ws, (size_t)SHRINK_MAX_SPLIT * M * r * 4 + 16), "cudaMalloc(ws)");
+  ShrinkPlan sp;
+  const bool ok = shrink_plan(&sp, (const bf16*)X, M, K, As, Ts, 1, r, ws, sms());
+  tidal_status st = ok ? sync_status(shrink_run(sp, scale, sms(), 0), "shrink")
+                       : set_err(TIDAL_ERR_INVALID, "shrink tensor maps");
+  cudaFree(ws);
+  return st;
+  TIDAL_CATCH
 }
 
 tidal_status tidal_k_attention(const void* qkv, void* O, int S, int H, int KV, int hd) {

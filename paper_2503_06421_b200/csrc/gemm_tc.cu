@@ -130,9 +130,42 @@ __device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
   for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// out[ks][m, col + j] = v[j]  (fp32 split-K partial), coalesced through staging.
+__device__ __forceinline__ void store_chunk_f32(const float (&v)[32], uint8_t* stg, int lane,
+                                                float* out, int ldo, int row0, int M, int col,
+                                                int nvalid) {
+  float4* st = reinterpret_cast<float4*>(stg + lane * STG_ROW);
+#pragma unroll
+  for (int k = 0; k < 8; ++k) st[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
+  __syncwarp();
+  const int ch = lane & 7, c = ch * 4;
+#pragma unroll
+  for (int it = 0; it < 8; ++it) {
+    const int r = it * 4 + (lane >> 3);
+    const int m = row0 + r;
+    if (m < M && c < nvalid) {
+      const float4 a = *reinterpret_cast<const float4*>(stg + r * STG_ROW + ch * 16);
+      float* dst = out + (size_t)m * ldo + col + c;
+      if (c + 4 <= nvalid) {
+        *reinterpret_cast<float4*>(dst) = a;
+      } else {
+        const float* s = reinterpret_cast<const float*>(&a);
+        for (int e = 0; e < nvalid - c; ++e) dst[e] = s[e];
+      }
+    }
+  }
+  __syncwarp();
+}
+
 template <int EPI, int BNT>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& seg, int& n0,
                                             int& m0) {
+  if (EPI == EPI_PARTIAL) {  // tile = ks * m_tiles + m
+    seg = 0;
+    n0 = 0;
+    m0 = (tile % p.m_tiles) * BM;
+    return;
+  }
   int gn = tile / p.m_tiles;
   m0 = (tile - gn * p.m_tiles) * BM;
   seg = 0;
@@ -194,13 +227,23 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
         int seg, n0, m0;
         decode_tile<EPI, BNT>(p, tile, seg, n0, m0);
         const bool lora = nlora > 0 && p.seg[seg].lora;
-        const int nkb = nk + (lora ? nlora : 0);
-        for (int kb = 0; kb < nkb; ++kb) {
+        int kb0 = 0, nkb = nk + (lora ? nlora : 0);
+        if (EPI == EPI_PARTIAL) {
+          const int ks = tile / p.m_tiles;
+          kb0 = ks * p.kblocks_per_split;
+          nkb = min(nk, kb0 + p.kblocks_per_split);
+        }
+        for (int kb = kb0; kb < nkb; ++kb) {
           ptx::mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + OFF_A + stage * A_BYTES;
           const uint32_t sb = sbase + OFF_B + stage * B_BYTES;
           const uint32_t fb = full_bar(stage);
-          if (kb < nk) {
+          if (EPI == EPI_PARTIAL) {
+            ptx::mbar_expect_tx(fb, A_BYTES + p.nseg * p.src_rows * BK * 2);
+            ptx::tma_load_2d(&p.a, sa, fb, kb * BK, m0);
+            for (int s = 0; s < p.nseg; ++s)
+              ptx::tma_load_2d(&p.b[s], sb + s * p.src_rows * BK * 2, fb, kb * BK, 0);
+          } else if (kb < nk) {
             ptx::mbar_expect_tx(fb, A_BYTES + BBYTES);
             ptx::tma_load_2d(&p.a, sa, fb, kb * BK, m0);
             if (EPI == EPI_SILU) {
@@ -239,19 +282,24 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
         int seg, n0, m0;
         decode_tile<EPI, BNT>(p, tile, seg, n0, m0);
         const bool lora = nlora > 0 && p.seg[seg].lora;
-        const int nkb = nk + (lora ? nlora : 0);
+        int kb0 = 0, nkb = nk + (lora ? nlora : 0);
+        if (EPI == EPI_PARTIAL) {
+          const int ks = tile / p.m_tiles;
+          kb0 = ks * p.kblocks_per_split;
+          nkb = min(nk, kb0 + p.kblocks_per_split);
+        }
         ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BNX;
-        for (int kb = 0; kb < nkb; ++kb) {
+        for (int kb = kb0; kb < nkb; ++kb) {
           ptx::mbar_wait(full_bar(stage), phase);
           ptx::tc_fence_after();
           const uint64_t adesc = ptx::desc_sw128(sbase + OFF_A + stage * A_BYTES);
           const uint64_t bdesc = ptx::desc_sw128(sbase + OFF_B + stage * B_BYTES);
-          if (kb < nk) {
+          if (EPI == EPI_PARTIAL || kb < nk) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              ptx::mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, (kb | k) != 0);
+              ptx::mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, ((kb - kb0) | k) != 0);
           } else if (EPI == EPI_SILU) {
             const int j = kb - nk;
             for (int k = 0; k < nmma_lora; ++k)
@@ -290,7 +338,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       const int row0 = m0 + q * 32;
       const int m = row0 + lane;
       float v[32], w[32];
-      if (EPI == EPI_SILU) {
+      if (EPI == EPI_PARTIAL) {
+        const int ks = tile / p.m_tiles;
+        const int ncols = p.nseg * p.src_rows;
+        float* out = reinterpret_cast<float*>(p.out) + (size_t)ks * p.M * p.ldo;
+#pragma unroll 1
+        for (int j = 0; j * 32 < ncols; ++j) {
+          ld_chunk(tacc + j * 32, v);
+          store_chunk_f32(v, stg, lane, out, p.ldo, row0, p.M, j * 32, ncols - j * 32);
+        }
+      } else if (EPI == EPI_SILU) {
         const int ncols = min(128, sg.n - n0);
 #pragma unroll 1
         for (int j = 0; j < 4; ++j) {
@@ -458,8 +515,74 @@ cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t 
       if (p.bn == 192) return launch_t<EPI_RESID, 192>(p, num_sms, s);
       if (p.bn == 128) return launch_t<EPI_RESID, 128>(p, num_sms, s);
       return launch_t<EPI_RESID, 256>(p, num_sms, s);
+    case EPI_PARTIAL:
+      if (p.bn == 64) return launch_t<EPI_PARTIAL, 64>(p, num_sms, s);
+      if (p.bn == 128) return launch_t<EPI_PARTIAL, 128>(p, num_sms, s);
+      return launch_t<EPI_PARTIAL, 192>(p, num_sms, s);
   }
   return cudaErrorInvalidValue;
+}
+
+}  // namespace tidal
+
+// ---------------------------------------------------------------------------
+// LoRA shrink on tensor cores: split-K EPI_PARTIAL GEMM + fixed-order reduce.
+// ---------------------------------------------------------------------------
+namespace tidal {
+namespace {
+__global__ void shrink_reduce_kernel(const float* __restrict__ ws, int ksplit, int M, int RT, int r,
+                                     bf16* T0, bf16* T1, bf16* T2, float scale) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= M * RT) return;
+  float s = 0.f;
+  for (int k = 0; k < ksplit; ++k) s += __ldcs(ws + (size_t)k * M * RT + e);
+  const int m = e / RT, c = e - m * RT, t = c / r;
+  bf16* T = t == 0 ? T0 : (t == 1 ? T1 : T2);
+  T[(size_t)m * r + (c - t * r)] = __float2bfloat16_rn(s * scale);
+}
+}  // namespace
+
+bool shrink_plan(ShrinkPlan* sp, const bf16* X, int M, int K, const bf16* const* A, bf16* const* T,
+                 int nt, int r, float* ws, int num_sms) {
+  memset(sp, 0, sizeof *sp);
+  GemmParams& g = sp->g;
+  const int RT = nt * r;
+  if (nt < 1 || nt > 3 || RT > 192 || r % 8) return false;
+  g.bn = RT <= 64 ? 64 : (RT <= 128 ? 128 : 192);
+  if (!make_tmap(&g.a, X, M, K, (uint64_t)K * 2, 128, 64)) return false;
+  for (int s = 0; s < nt; ++s)
+    if (!make_tmap(&g.b[s], A[s], r, K, (uint64_t)K * 2, r, 64)) return false;
+  g.nseg = nt;
+  g.src_rows = r;
+  g.M = M;
+  g.K = K;
+  g.m_tiles = (M + BM - 1) / BM;
+  g.n_tiles[0] = 1;
+  g.seg[0].n = RT;
+  const int nk = (K + BK - 1) / BK;
+  int ks = num_sms / g.m_tiles;
+  ks = ks < 1 ? 1 : (ks > SHRINK_MAX_SPLIT ? SHRINK_MAX_SPLIT : ks);
+  g.kblocks_per_split = (nk + ks - 1) / ks;
+  g.ksplit = (nk + g.kblocks_per_split - 1) / g.kblocks_per_split;  // every split non-empty
+  g.total_tiles = g.m_tiles * g.ksplit;
+  g.out = ws;
+  g.ldo = RT;
+  sp->M = M;
+  sp->RT = RT;
+  sp->r = r;
+  sp->nt = nt;
+  for (int s = 0; s < nt; ++s) sp->T[s] = T[s];
+  sp->ws = ws;
+  return true;
+}
+
+cudaError_t shrink_run(const ShrinkPlan& sp, float scale, int num_sms, cudaStream_t s) {
+  cudaError_t e = gemm_launch(sp.g, EPI_PARTIAL, num_sms, s);
+  if (e != cudaSuccess) return e;
+  const int n = sp.M * sp.RT;
+  shrink_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(sp.ws, sp.g.ksplit, sp.M, sp.RT, sp.r,
+                                                       sp.T[0], sp.T[1], sp.T[2], scale);
+  return cudaGetLastError();
 }
 
 }  // namespace tidal

@@ -20,7 +20,9 @@ enum GemmEpi : int {
   EPI_STORE = 0,  // out bf16 [M, ldo] at out_col
   EPI_ROPE = 1,   // as STORE, rotate-half RoPE on segments with rope=1 (q, k)
   EPI_SILU = 2,   // W = [gate ; up] paired 128-row tiles: out = silu(g) * u (bf16)
-  EPI_RESID = 3   // out fp32 [M, ldo]: out += acc (residual stream)
+  EPI_RESID = 3,  // out fp32 [M, ldo]: out += acc (residual stream)
+  EPI_PARTIAL = 4 // split-K partial sums: out fp32 [ksplit][M][ldo] = acc; the B tile
+                  // stacks nseg sources of src_rows rows each (LoRA shrink: A_q;A_k;A_v)
 };
 
 constexpr int GEMM_BM = 128, GEMM_BN = 256, GEMM_BK = 64, GEMM_STAGES = 4;
@@ -52,7 +54,21 @@ struct alignas(64) GemmParams {
   int bn;              // N tile: 256 | 192 | 128 (EPI_SILU: 128 output cols = 256 acc cols)
   bf16* vt;            // V^T [n_vt][vt_ld] for the tcgen05 attention (segments with vt=1)
   int vt_ld;
+  int ksplit, kblocks_per_split, src_rows;  // EPI_PARTIAL
 };
+
+// LoRA shrink on tensor cores: T_t = bf16(scale * X A_t^T) for nt targets
+// sharing X, as a split-K EPI_PARTIAL GEMM into ws plus a fixed-order reduce.
+struct ShrinkPlan {
+  GemmParams g;
+  int M, RT, r, nt;
+  bf16* T[3];
+  float* ws;
+};
+bool shrink_plan(ShrinkPlan* sp, const bf16* X, int M, int K, const bf16* const* A, bf16* const* T,
+                 int nt, int r, float* ws, int num_sms);
+cudaError_t shrink_run(const ShrinkPlan& sp, float scale, int num_sms, cudaStream_t s);
+constexpr int SHRINK_MAX_SPLIT = 16;
 
 // tcgen05 causal attention (hd = 128): Q/K from QKV [S, (H+2KV)*128], V from
 // V^T [KV*128][vt_ld] (written by the QKV epilogue).

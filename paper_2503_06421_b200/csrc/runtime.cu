@@ -60,6 +60,7 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   dalloc(logits, (size_t)m.vocab * 4);
   dalloc(key, 64);
   dalloc(tok, S * 4);
+  dalloc(shrink_ws, (size_t)SHRINK_MAX_SPLIT * S * 192 * 4);
   vt_ld = (int)((S + 63) / 64 * 64);
   dalloc(Vt, nkv * (size_t)vt_ld * 2);
   // RoPE table: angle = pos * theta^(-2i/hd), cos/sin in double, stored fp32
@@ -84,7 +85,7 @@ void Exec::destroy() {
   cudaSetDevice(device);
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
-  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt};
+  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int t = 0; t < kNumTargets; ++t)
@@ -221,6 +222,27 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     dn.total_tiles = dn.n_tiles[0] * mt;
     dn.out = X;
     dn.ldo = d;
+    // ---- LoRA shrinks (T = s x A^T) for the targets sharing each input ----
+    if (r) {
+      const std::initializer_list<int> groups[4] = {{T_Q, T_K, T_V}, {T_O}, {T_GATE, T_UP}, {T_DOWN}};
+      const bf16* inputs[4] = {Xn, O, Xn, Hb};
+      const int kdim[4] = {d, nq, d, F};
+      for (int gi = 0; gi < 4; ++gi) {
+        const bf16* A[3];
+        bf16* Tt[3];
+        int n = 0;
+        for (int t : groups[gi])
+          if (tt.lora_a[l][t] >= 0) {
+            A[n] = reinterpret_cast<const bf16*>(W(tt.lora_a[l][t]));
+            Tt[n] = T[t];
+            ++n;
+          }
+        if (!n) continue;
+        if (!shrink_plan(&ll.sh[gi], inputs[gi], S, kdim[gi], A, Tt, n, r, shrink_ws, num_sms))
+          fail(3, "shrink tensor maps");
+        ll.has_sh[gi] = 1;
+      }
+    }
   }
   if (cache.size() > 64) cache.clear();
   return cache.emplace(k, std::move(v)).first->second;
@@ -315,22 +337,16 @@ void run_forward(Exec& ex, const RunArgs& a) {
     if (ev >= 0) ex.prof_end(cls, ev, fl, by);
   };
   const double Sd = S;
-  auto shrink = [&](const bf16* X, int ldx, int Kd, int l, std::initializer_list<int> ts) {
-    const bf16* A[3];
-    bf16* T[3];
-    int n = 0;
-    for (int t : ts)
-      if (tt.lora_a[l][t] >= 0) {
-        A[n] = reinterpret_cast<const bf16*>(ex.wptr[tt.lora_a[l][t]]);
-        T[n] = ex.T[t];
-        ++n;
-      }
-    if (n) {
-      const int e0 = P0();
-      K(KC_SHRINK, e0, 2.0 * Sd * Kd * r * n, 2.0 * (Sd * Kd + (double)n * r * (Kd + Sd)),
-        lora_shrink_launch(X, ldx, S, Kd, A, T, n, r, a.lora_scale, st),
-        "lora_shrink");
-    }
+  // LoRA shrink gi (0 qkv, 1 o, 2 gate_up, 3 down): split-K tcgen05 GEMM + reduce
+  auto shrink = [&](const bf16* X, int ldx, int Kd, int l, int gi) {
+    (void)X;
+    (void)ldx;
+    if (!LP[l].has_sh[gi]) return;
+    const ShrinkPlan& sp = LP[l].sh[gi];
+    const int e0 = P0();
+    K(KC_SHRINK, e0, 2.0 * Sd * Kd * sp.RT, 2.0 * (Sd * Kd + (double)sp.RT * (Kd + Sd)),
+      shrink_run(sp, a.lora_scale, ex.num_sms, st), "lora_shrink");
+    ++ex.launches;  // shrink_run launches two kernels (GEMM + reduce)
   };
   auto lora_n = [&](int l, std::initializer_list<int> ts) {
     double n = 0;
@@ -379,7 +395,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_QKV:
-        shrink(ex.Xn, d, d, l, {T_Q, T_K, T_V});
+        shrink(ex.Xn, d, d, l, 0);
         {
           const double n = nq + 2.0 * nkv;
           const int e0 = P0();
@@ -402,7 +418,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_O:
-        shrink(ex.O, nq, nq, l, {T_O});
+        shrink(ex.O, nq, nq, l, 1);
         if (ex.world > 1 && ex.rank != 0)
           cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
         {
@@ -420,7 +436,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_GU:
-        shrink(ex.Xn, d, d, l, {T_GATE, T_UP});
+        shrink(ex.Xn, d, d, l, 2);
         {
           const int e0 = P0();
           K(KC_GEMM_GU, e0, 2.0 * Sd * (2.0 * F * d + r * lora_n(l, {T_GATE, T_UP})),
@@ -431,7 +447,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_ACT:  // fused into the gate/up epilogue
         break;
       case OP_DOWN:
-        shrink(ex.Hb, F, F, l, {T_DOWN});
+        shrink(ex.Hb, F, F, l, 3);
         if (ex.world > 1 && ex.rank != 0)
           cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
         {

@@ -26,6 +26,8 @@ void cuda_check(cudaError_t e, const char* what);
 // Per-layer launch parameters, cached per (prompt length, adapter layout).
 struct LayerLaunch {
   GemmParams qkv, o, gu, down;
+  ShrinkPlan sh[4];  // LoRA shrink feeding qkv / o / gate_up / down
+  int has_sh[4] = {0, 0, 0, 0};
 };
 
 // Device execution context: streams, activation arena, rope table, the fork
@@ -45,6 +47,7 @@ struct Exec {
   unsigned long long* key = nullptr;
   int32_t* tok = nullptr;
   float2* rope = nullptr;
+  float* shrink_ws = nullptr;  // split-K partials of the LoRA shrink
   bf16* Vt = nullptr;  // V^T [KV*hd][vt_ld] (tcgen05 attention, hd = 128)
   int vt_ld = 0;
   std::map<int, AttnParams> attn_cache;  // per prompt length
