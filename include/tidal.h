@@ -205,7 +205,8 @@ enum {
   TIDAL_DEBUG_SCRUB_L2 = 4,    /* write 512 MB before each invoke (timing hygiene) */
   TIDAL_DEBUG_SERIAL = 8,      /* load-then-infer: compute waits for every copy first
                                   (the paper's "PyTorch-pin" baseline) */
-  TIDAL_DEBUG_PROFILE = 16     /* CUDA events around every kernel on the compute stream */
+  TIDAL_DEBUG_PROFILE = 16,    /* CUDA events around every kernel on the compute stream */
+  TIDAL_DEBUG_PROFILE_GEMM = 32 /* events around the tensor-core GEMMs only (low overhead) */
 };
 /* Per-kernel-class totals accumulated by invokes run with TIDAL_DEBUG_PROFILE:
  * device time (events on the launching stream), launches, and the ALGORITHMIC

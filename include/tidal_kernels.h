@@ -38,8 +38,9 @@ tidal_status tidal_k_head(const float* xlast, const void* g, const void* W, int 
  * epi: 0 store bf16, 1 store bf16 with RoPE on segments 0,1 (rope = float2
  * [M, head_dim/2] cos/sin), 2 SiLU(W_0 part) * (W_1 part) with seg_n[0] = F,
  * 3 fp32 out += acc.  T/B nullable (no LoRA).  K % 8 == 0, seg_n % 8 == 0.
- * Bits 8.. of epi optionally force the N-tile width (128, 192 or 256);
- * 0 lets the library pick it as the runtime does (gemm_pick_bn). */
+ * Bits 8-16 of epi optionally force the N-tile width (128, 192 or 256) and
+ * bits 20-21 the CTA group (1 single-SM, 2 CTA pair with cta_group::2);
+ * 0 lets the library pick them as the runtime does. */
 tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const int* seg_n, int nseg,
                           void* out, int ldo, int M, int K, const void* const* T,
                           const void* const* B, int r, const void* rope, int head_dim);

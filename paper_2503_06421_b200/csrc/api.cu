@@ -605,7 +605,8 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
                       ? std::chrono::steady_clock::now()
                       : t_entry;
   ex.launches = 0;
-  ex.profile = (tp->debug & TIDAL_DEBUG_PROFILE) != 0;
+  ex.profile = (tp->debug & (TIDAL_DEBUG_PROFILE | TIDAL_DEBUG_PROFILE_GEMM)) != 0;
+  ex.profile_all = (tp->debug & TIDAL_DEBUG_PROFILE) != 0;
   ex.prof_pending.clear();
   memcpy(ex.h_tok, host_tokens, 4ull * n_tokens);
   cuda_check(cudaEventRecord(tp->e_start, ex.compute), "event");
@@ -841,7 +842,8 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
                           void* out, int ldo, int M, int K, const void* const* T,
                           const void* const* B, int r, const void* rope, int head_dim) {
   TIDAL_TRY
-  const int bn_req = epi >> 8;
+  const int cg_req = (epi >> 20) & 0x3;  // bits 20-21: CTA group (0 = auto)
+  const int bn_req = (epi >> 8) & 0x1FF;  // bits 8-16: N tile (0 = auto)
   epi &= 0xFF;
   require(epi >= 0 && epi <= 3 && nseg >= 1 && nseg <= 3, "bad gemm arguments");
   GemmParams p;
@@ -850,11 +852,14 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
   require(p.bn == 256 || p.bn == 192 || p.bn == 128, "bn must be 256, 192 or 128");
   if (epi == EPI_SILU) p.bn = 128;
   if (epi == EPI_ROPE && p.bn == 192) p.bn = 256;
+  p.cg = cg_req ? cg_req : gemm_pick_cg(M);
+  require(p.cg == 1 || p.cg == 2, "cg must be 1 or 2");
+  const int bbox = gemm_b_box(epi, p.bn, p.cg), tbbox = gemm_tb_box(epi, p.bn, p.cg);
   auto mk = [&](CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box) {
     require(make_tmap(m, base, rows, cols, cols * 2, box, 64), "tensor map encode failed");
   };
   mk(&p.a, A, M, K, 128);
-  const int mt = (M + GEMM_BM - 1) / GEMM_BM;
+  const int mt = (M + GEMM_BM * p.cg - 1) / (GEMM_BM * p.cg);
   p.M = M;
   p.K = K;
   p.m_tiles = mt;
@@ -869,8 +874,8 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
     if (p.lora_r) {
       mk(&p.ta[0], T[0], M, r, 128);
       mk(&p.ta[1], T[1], M, r, 128);
-      mk(&p.tb[0], B[0], seg_n[0], r, 128);
-      mk(&p.tb[1], B[1], seg_n[0], r, 128);
+      mk(&p.tb[0], B[0], seg_n[0], r, tbbox);
+      mk(&p.tb[1], B[1], seg_n[0], r, tbbox);
     }
     p.nseg = 1;
     p.seg[0].n = seg_n[0];
@@ -881,14 +886,14 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
     int col = 0;
     p.nseg = nseg;
     for (int s = 0; s < nseg; ++s) {
-      mk(&p.b[s], W[s], seg_n[s], K, p.bn);
+      mk(&p.b[s], W[s], seg_n[s], K, bbox);
       p.seg[s].n = seg_n[s];
       p.seg[s].out_col = col;
       p.seg[s].rope = (epi == EPI_ROPE) && s < 2;
       p.seg[s].lora = p.lora_r > 0 && T[s] && B[s];
       if (p.seg[s].lora) {
         mk(&p.ta[s], T[s], M, r, 128);
-        mk(&p.tb[s], B[s], seg_n[s], r, p.bn);
+        mk(&p.tb[s], B[s], seg_n[s], r, tbbox);
       }
       col += seg_n[s];
       p.n_tiles[s] = (seg_n[s] + p.bn - 1) / p.bn;

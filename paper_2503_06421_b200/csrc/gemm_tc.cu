@@ -1,24 +1,29 @@
 // gemm_tc.cu — the dense contractions of the prefill (QKV, O, gate/up, down)
 // on 5th-gen tensor cores: tcgen05.mma with TMEM accumulators, operands staged
 // by TMA (SWIZZLE_128B) through a 4-stage mbarrier ring, warp-specialised
-// persistent CTAs (one per SM):
+// persistent CTAs:
 //   warp 0      TMA producer (one elected lane)
 //   warp 1      TMEM allocator + MMA issuer (one elected lane)
 //   warps 2..5  epilogue: tcgen05.ld -> fused op -> smem transpose -> coalesced st.global
-// Two 256-column accumulators in TMEM let tile i's epilogue overlap tile i+1's
-// mainloop.  The LoRA delta of a targeted projection is folded in as a
-// K-extension: x W^T + (s x A^T) B^T = [x | T] [W | B]^T, i.e. ceil(r/16)
-// extra UMMA K-steps reading T [M, r] and lora_B [n, r] (zero-filled by TMA
-// beyond r), so no separate expand kernel and no extra pass over C.
+// CG = 2 (the default for M > 128): a CTA pair on the two SMs of a TPC runs
+// one 256 x BN tile with tcgen05.mma.cta_group::2 — each CTA stages its 128
+// rows of A and its BN/2 rows of B, so per-SM shared-memory operand traffic
+// halves; the leader CTA issues the MMA and commits to both CTAs' barriers.
+// Two accumulators in TMEM let tile i's epilogue overlap tile i+1's mainloop.
+// The LoRA delta of a targeted projection is folded in as a K-extension:
+// x W^T + (s x A^T) B^T = [x | T] [W | B]^T, i.e. ceil(r/16) extra UMMA
+// K-steps reading T [M, r] and lora_B [n, r] (zero-filled by TMA beyond r).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdio>
+#include <cstring>
 #include <mutex>
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "ptx2.cuh"
 
 namespace tidal {
 
@@ -26,7 +31,8 @@ namespace {
 
 constexpr int BM = GEMM_BM, BN = GEMM_BN, BK = GEMM_BK, STAGES = GEMM_STAGES;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
-constexpr int B_BYTES = BN * BK * 2;          // 32 KB
+constexpr int B_BYTES = BN * BK * 2;          // 32 KB (stage slot; a CTA uses <= this)
+constexpr int ROW_BYTES = BK * 2;             // one 64-element K row = 128 B
 constexpr int STG_ROW = 144;                  // staging row stride (bytes)
 constexpr int STG_WARP = 32 * STG_ROW;
 constexpr int OFF_A = 0;
@@ -122,15 +128,7 @@ __device__ __forceinline__ void add_chunk_f32(const float (&v)[32], uint8_t* stg
   __syncwarp();
 }
 
-__device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
-  uint32_t r[32];
-  ptx::tmem_ld32(taddr, r);
-  ptx::tmem_ld_wait();
-#pragma unroll
-  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
-}
-
-// out[ks][m, col + j] = v[j]  (fp32 split-K partial), coalesced through staging.
+// out[m, col + j] = v[j]  (fp32 split-K partial), coalesced through staging.
 __device__ __forceinline__ void store_chunk_f32(const float (&v)[32], uint8_t* stg, int lane,
                                                 float* out, int ldo, int row0, int M, int col,
                                                 int nvalid) {
@@ -157,7 +155,18 @@ __device__ __forceinline__ void store_chunk_f32(const float (&v)[32], uint8_t* s
   __syncwarp();
 }
 
-template <int EPI, int BNT>
+__device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
+  uint32_t r[32];
+  ptx::tmem_ld32(taddr, r);
+  ptx::tmem_ld_wait();
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// tile -> (segment, first output column within the segment, first row of the
+// cluster tile).  Cluster tiles are n-major so concurrently running tiles share
+// the same weight panel (read from HBM once, then from L2).
+template <int EPI, int BNT, int CG>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& seg, int& n0,
                                             int& m0) {
   if (EPI == EPI_PARTIAL) {  // tile = ks * m_tiles + m
@@ -167,7 +176,7 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
     return;
   }
   int gn = tile / p.m_tiles;
-  m0 = (tile - gn * p.m_tiles) * BM;
+  m0 = (tile - gn * p.m_tiles) * (BM * CG);
   seg = 0;
   while (seg < p.nseg - 1 && gn >= p.n_tiles[seg]) {
     gn -= p.n_tiles[seg];
@@ -176,15 +185,20 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
   n0 = gn * (EPI == EPI_SILU ? 128 : BNT);
 }
 
-template <int EPI, int BNT>
+template <int EPI, int BNT, int CG>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
   constexpr int BNX = EPI == EPI_SILU ? 256 : BNT;  // MMA N = accumulator columns
-  constexpr int BBYTES = BNX * BK * 2;
+  constexpr int BROWS = BNX / CG;                   // B rows staged by this CTA
+  constexpr int BBYTES = BROWS * ROW_BYTES;
+  constexpr int SILU_LORA_ROWS = 128 / CG;          // per-CTA rows of a gate/up LoRA-B box
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>(
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const uint32_t sbase = ptx::smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = CG == 2 ? (int)ptx::cluster_rank() : 0;
+  const int unit = CG == 2 ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
+  const int nunits = CG == 2 ? (int)gridDim.x >> 1 : (int)gridDim.x;
   const uint32_t bar0 = sbase + OFF_BAR;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
@@ -197,40 +211,51 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&p.a);
-    for (int i = 0; i < 3; ++i) {
-      if (i < p.nseg || (EPI == EPI_SILU && i < 2)) {
-        ptx::prefetch_tmap(&p.b[i]);
-      }
-    }
+    for (int i = 0; i < 3; ++i)
+      if (i < p.nseg || (EPI == EPI_SILU && i < 2)) ptx::prefetch_tmap(&p.b[i]);
     for (int s = 0; s < STAGES; ++s) {
-      ptx::mbar_init(full_bar(s), 1);
+      ptx::mbar_init(full_bar(s), CG);  // leader expect_tx + peer arrive
       ptx::mbar_init(empty_bar(s), 1);
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(tfull_bar(a), 1);
-      ptx::mbar_init(tempty_bar(a), 128);
+      ptx::mbar_init(tempty_bar(a), 128 * CG);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), TMEM_COLS);
+  if (warp == 1) {
+    if (CG == 2)
+      ptx::tmem_alloc_pair(ptx::smem_u32(tmem_holder), TMEM_COLS);
+    else
+      ptx::tmem_alloc(ptx::smem_u32(tmem_holder), TMEM_COLS);
+  }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
 
   if (warp == 0) {
-    // ===================== TMA producer =====================
+    // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
+      auto tma = [&](const CUtensorMap* m, uint32_t dst, uint32_t fb, int c0, int c1) {
+        if (CG == 2)
+          ptx::tma_load_2d_pair(m, dst, fb, c0, c1);
+        else
+          ptx::tma_load_2d(m, dst, fb, c0, c1);
+      };
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < p.total_tiles; tile += nunits) {
         int seg, n0, m0;
-        decode_tile<EPI, BNT>(p, tile, seg, n0, m0);
+        decode_tile<EPI, BNT, CG>(p, tile, seg, n0, m0);
+        const int ma = m0 + rank * BM;  // this CTA's A rows
         const bool lora = nlora > 0 && p.seg[seg].lora;
         int kb0 = 0, nkb = nk + (lora ? nlora : 0);
         if (EPI == EPI_PARTIAL) {
-          const int ks = tile / p.m_tiles;
-          kb0 = ks * p.kblocks_per_split;
+          kb0 = (tile / p.m_tiles) * p.kblocks_per_split;
           nkb = min(nk, kb0 + p.kblocks_per_split);
         }
         for (int kb = kb0; kb < nkb; ++kb) {
@@ -238,27 +263,41 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           const uint32_t sa = sbase + OFF_A + stage * A_BYTES;
           const uint32_t sb = sbase + OFF_B + stage * B_BYTES;
           const uint32_t fb = full_bar(stage);
+          int bytes;  // this CTA's bytes for the stage
           if (EPI == EPI_PARTIAL) {
-            ptx::mbar_expect_tx(fb, A_BYTES + p.nseg * p.src_rows * BK * 2);
-            ptx::tma_load_2d(&p.a, sa, fb, kb * BK, m0);
-            for (int s = 0; s < p.nseg; ++s)
-              ptx::tma_load_2d(&p.b[s], sb + s * p.src_rows * BK * 2, fb, kb * BK, 0);
+            bytes = A_BYTES + p.nseg * p.src_rows * ROW_BYTES;
           } else if (kb < nk) {
-            ptx::mbar_expect_tx(fb, A_BYTES + BBYTES);
-            ptx::tma_load_2d(&p.a, sa, fb, kb * BK, m0);
+            bytes = A_BYTES + BBYTES;
+          } else {
+            bytes = A_BYTES + (EPI == EPI_SILU ? SILU_LORA_ROWS : BROWS) * ROW_BYTES;
+          }
+          if (rank == 0)
+            ptx::mbar_expect_tx(fb, bytes * CG);
+          else
+            ptx::mbar_arrive_leader(fb);
+          if (EPI == EPI_PARTIAL) {
+            tma(&p.a, sa, fb, kb * BK, ma);
+            for (int s = 0; s < p.nseg; ++s)
+              tma(&p.b[s], sb + s * p.src_rows * ROW_BYTES, fb, kb * BK, 0);
+          } else if (kb < nk) {
+            tma(&p.a, sa, fb, kb * BK, ma);
             if (EPI == EPI_SILU) {
-              ptx::tma_load_2d(&p.b[0], sb, fb, kb * BK, n0);
-              ptx::tma_load_2d(&p.b[1], sb + B_BYTES / 2, fb, kb * BK, n0);
+              if (CG == 2) {
+                tma(&p.b[rank], sb, fb, kb * BK, n0);  // rank 0: gate rows, rank 1: up rows
+              } else {
+                tma(&p.b[0], sb, fb, kb * BK, n0);
+                tma(&p.b[1], sb + 128 * ROW_BYTES, fb, kb * BK, n0);
+              }
             } else {
-              ptx::tma_load_2d(&p.b[seg], sb, fb, kb * BK, n0);
+              tma(&p.b[seg], sb, fb, kb * BK, n0 + rank * BROWS);
             }
           } else {
             const int j = kb - nk;  // LoRA stage: EPI_SILU j=0 gate, j=1 up
-            const int t = EPI == EPI_SILU ? j : seg;
-            const int bbytes = EPI == EPI_SILU ? B_BYTES / 2 : BBYTES;
-            ptx::mbar_expect_tx(fb, A_BYTES + bbytes);
-            ptx::tma_load_2d(&p.ta[t], sa, fb, 0, m0);
-            ptx::tma_load_2d(&p.tb[t], sb, fb, 0, n0);
+            tma(&p.ta[EPI == EPI_SILU ? j : seg], sa, fb, 0, ma);
+            if (EPI == EPI_SILU)
+              tma(&p.tb[j], sb, fb, 0, n0 + rank * SILU_LORA_ROWS);
+            else
+              tma(&p.tb[seg], sb, fb, 0, n0 + rank * BROWS);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -269,23 +308,34 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     }
     __syncwarp();
   } else if (warp == 1) {
-    // ===================== MMA issuer =====================
-    if (lane == 0) {
-      constexpr uint32_t IDESC = ptx::idesc_bf16(BM, BNX);
-      constexpr uint32_t IDESC_HALF = ptx::idesc_bf16(BM, BN / 2);
+    // ===================== MMA issuer (leader CTA) =====================
+    if (lane == 0 && rank == 0) {
+      constexpr uint32_t IDESC = ptx::idesc_bf16(BM * CG, BNX);
+      constexpr uint32_t IDESC_HALF = ptx::idesc_bf16(BM * CG, 128);
       const int nmma_lora = (p.lora_r + 15) / 16;
+      auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+        if (CG == 2)
+          ptx::mma_bf16_pair(d, a, b, id, acc);
+        else
+          ptx::mma_bf16(d, a, b, id, acc);
+      };
+      auto commit = [&](uint32_t bar) {
+        if (CG == 2)
+          ptx::mma_commit_pair(bar);
+        else
+          ptx::mma_commit(bar);
+      };
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+      for (int tile = unit; tile < p.total_tiles; tile += nunits) {
         int seg, n0, m0;
-        decode_tile<EPI, BNT>(p, tile, seg, n0, m0);
+        decode_tile<EPI, BNT, CG>(p, tile, seg, n0, m0);
         const bool lora = nlora > 0 && p.seg[seg].lora;
         int kb0 = 0, nkb = nk + (lora ? nlora : 0);
         if (EPI == EPI_PARTIAL) {
-          const int ks = tile / p.m_tiles;
-          kb0 = ks * p.kblocks_per_split;
+          kb0 = (tile / p.m_tiles) * p.kblocks_per_split;
           nkb = min(nk, kb0 + p.kblocks_per_split);
         }
         ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
@@ -299,22 +349,21 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           if (EPI == EPI_PARTIAL || kb < nk) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              ptx::mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, ((kb - kb0) | k) != 0);
+              mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, ((kb - kb0) | k) != 0);
           } else if (EPI == EPI_SILU) {
             const int j = kb - nk;
             for (int k = 0; k < nmma_lora; ++k)
-              ptx::mma_bf16(d_tmem + j * (BN / 2), adesc + 2 * k, bdesc + 2 * k, IDESC_HALF, 1);
+              mma(d_tmem + j * 128, adesc + 2 * k, bdesc + 2 * k, IDESC_HALF, 1);
           } else {
-            for (int k = 0; k < nmma_lora; ++k)
-              ptx::mma_bf16(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, 1);
+            for (int k = 0; k < nmma_lora; ++k) mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, 1);
           }
-          ptx::mma_commit(empty_bar(stage));
+          commit(empty_bar(stage));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
           }
         }
-        ptx::mma_commit(tfull_bar(acc));
+        commit(tfull_bar(acc));
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -323,19 +372,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     }
     __syncwarp();
   } else {
-    // ===================== epilogue (warps 2..5) =====================
+    // ===================== epilogue (warps 2..5, both CTAs) =====================
     const int q = warp & 3;  // TMEM lane quarter this warp may access
     uint8_t* stg = smem + OFF_STG + (warp - 2) * STG_WARP;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = blockIdx.x; tile < p.total_tiles; tile += gridDim.x) {
+    for (int tile = unit; tile < p.total_tiles; tile += nunits) {
       int seg, n0, m0;
-      decode_tile<EPI, BNT>(p, tile, seg, n0, m0);
+      decode_tile<EPI, BNT, CG>(p, tile, seg, n0, m0);
       const GemmSeg sg = p.seg[seg];
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
       ptx::tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNX;
-      const int row0 = m0 + q * 32;
+      const int row0 = m0 + rank * BM + q * 32;
       const int m = row0 + lane;
       float v[32], w[32];
       if (EPI == EPI_PARTIAL) {
@@ -415,7 +464,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
         }
       }
       ptx::tc_fence_before();
-      ptx::mbar_arrive(tempty_bar(acc));
+      if (CG == 2)
+        ptx::mbar_arrive_leader(tempty_bar(acc));
+      else
+        ptx::mbar_arrive(tempty_bar(acc));
       if (++acc == 2) {
         acc = 0;
         acc_phase ^= 1;
@@ -423,10 +475,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  if (CG == 2)
+    ptx::cluster_sync();
+  else
+    __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tmem_base, TMEM_COLS);
+    if (CG == 2)
+      ptx::tmem_dealloc_pair(tmem_base, TMEM_COLS);
+    else
+      ptx::tmem_dealloc(tmem_base, TMEM_COLS);
   }
 }
 
@@ -437,26 +495,52 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 EncodeTiledFn g_encode = nullptr;
 std::once_flag g_once;
 
-template <int EPI, int BNT>
+template <int EPI, int BNT, int CG>
 cudaError_t launch_t(const GemmParams& p, int num_sms, cudaStream_t s) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI, BNT>,
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI, BNT, CG>,
                                          cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  int grid = p.total_tiles < num_sms ? p.total_tiles : num_sms;
+  const int units = num_sms / CG;
+  const int grid = (p.total_tiles < units ? p.total_tiles : units) * CG;
   if (grid <= 0) return cudaSuccess;
-  gemm_tc_kernel<EPI, BNT><<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
-  return cudaGetLastError();
+  if (CG == 1) {
+    gemm_tc_kernel<EPI, BNT, CG><<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
+    return cudaGetLastError();
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(NTHREADS);
+  cfg.dynamicSmemBytes = SMEM_BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeClusterDimension;
+  attr[0].val.clusterDim.x = 2;
+  attr[0].val.clusterDim.y = 1;
+  attr[0].val.clusterDim.z = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BNT, CG>, p);
+}
+
+template <int EPI, int BNT>
+cudaError_t launch_cg(const GemmParams& p, int num_sms, cudaStream_t s) {
+  if (p.cg == 2) return launch_t<EPI, BNT, 2>(p, num_sms, s);
+  return launch_t<EPI, BNT, 1>(p, num_sms, s);
 }
 
 }  // namespace
 
+int gemm_pick_cg(int M) { return M > GEMM_BM ? 2 : 1; }
+
 int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms) {
   if (epi == EPI_SILU) return 128;
-  const int mt = (M + BM - 1) / BM;
+  const int cg = gemm_pick_cg(M);
+  const int mt = (M + BM * cg - 1) / (BM * cg);
+  const int units = num_sms / cg;
   static const int cands[] = {256, 192, 128};
   int best = 256;
   double best_cost = 1e30;
@@ -464,7 +548,7 @@ int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms) {
     if (epi == EPI_ROPE && bn == 192) continue;  // RoPE tiles must hold whole heads
     long tiles = 0;
     for (int s = 0; s < nseg; ++s) tiles += (long)mt * ((seg_n[s] + bn - 1) / bn);
-    const long waves = (tiles + num_sms - 1) / num_sms;
+    const long waves = (tiles + units - 1) / units;
     // 128-wide tiles pay ~15% more per MAC (A-operand smem traffic per MMA doubles)
     const double cost = (double)waves * bn * (bn == 128 ? 1.15 : 1.0);
     if (cost < best_cost - 1e-9) {
@@ -474,6 +558,9 @@ int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms) {
   }
   return best;
 }
+
+int gemm_b_box(int epi, int bn, int cg) { return epi == EPI_SILU ? 128 : bn / cg; }
+int gemm_tb_box(int epi, int bn, int cg) { return epi == EPI_SILU ? 128 / cg : bn / cg; }
 
 bool tma_init() {
   std::call_once(g_once, [] {
@@ -504,31 +591,28 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
 cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t s) {
   switch (epi) {
     case EPI_STORE:
-      if (p.bn == 192) return launch_t<EPI_STORE, 192>(p, num_sms, s);
-      if (p.bn == 128) return launch_t<EPI_STORE, 128>(p, num_sms, s);
-      return launch_t<EPI_STORE, 256>(p, num_sms, s);
+      if (p.bn == 192) return launch_cg<EPI_STORE, 192>(p, num_sms, s);
+      if (p.bn == 128) return launch_cg<EPI_STORE, 128>(p, num_sms, s);
+      return launch_cg<EPI_STORE, 256>(p, num_sms, s);
     case EPI_ROPE:
-      if (p.bn == 128) return launch_t<EPI_ROPE, 128>(p, num_sms, s);
-      return launch_t<EPI_ROPE, 256>(p, num_sms, s);
-    case EPI_SILU: return launch_t<EPI_SILU, 128>(p, num_sms, s);
+      if (p.bn == 128) return launch_cg<EPI_ROPE, 128>(p, num_sms, s);
+      return launch_cg<EPI_ROPE, 256>(p, num_sms, s);
+    case EPI_SILU: return launch_cg<EPI_SILU, 128>(p, num_sms, s);
     case EPI_RESID:
-      if (p.bn == 192) return launch_t<EPI_RESID, 192>(p, num_sms, s);
-      if (p.bn == 128) return launch_t<EPI_RESID, 128>(p, num_sms, s);
-      return launch_t<EPI_RESID, 256>(p, num_sms, s);
-    case EPI_PARTIAL:
-      if (p.bn == 64) return launch_t<EPI_PARTIAL, 64>(p, num_sms, s);
-      if (p.bn == 128) return launch_t<EPI_PARTIAL, 128>(p, num_sms, s);
-      return launch_t<EPI_PARTIAL, 192>(p, num_sms, s);
+      if (p.bn == 192) return launch_cg<EPI_RESID, 192>(p, num_sms, s);
+      if (p.bn == 128) return launch_cg<EPI_RESID, 128>(p, num_sms, s);
+      return launch_cg<EPI_RESID, 256>(p, num_sms, s);
+    case EPI_PARTIAL:  // split-K shrink: single-CTA tiles
+      if (p.bn == 64) return launch_t<EPI_PARTIAL, 64, 1>(p, num_sms, s);
+      if (p.bn == 128) return launch_t<EPI_PARTIAL, 128, 1>(p, num_sms, s);
+      return launch_t<EPI_PARTIAL, 192, 1>(p, num_sms, s);
   }
   return cudaErrorInvalidValue;
 }
 
-}  // namespace tidal
-
 // ---------------------------------------------------------------------------
 // LoRA shrink on tensor cores: split-K EPI_PARTIAL GEMM + fixed-order reduce.
 // ---------------------------------------------------------------------------
-namespace tidal {
 namespace {
 __global__ void shrink_reduce_kernel(const float* __restrict__ ws, int ksplit, int M, int RT, int r,
                                      bf16* T0, bf16* T1, bf16* T2, float scale) {
@@ -549,6 +633,7 @@ bool shrink_plan(ShrinkPlan* sp, const bf16* X, int M, int K, const bf16* const*
   const int RT = nt * r;
   if (nt < 1 || nt > 3 || RT > 192 || r % 8) return false;
   g.bn = RT <= 64 ? 64 : (RT <= 128 ? 128 : 192);
+  g.cg = 1;
   if (!make_tmap(&g.a, X, M, K, (uint64_t)K * 2, 128, 64)) return false;
   for (int s = 0; s < nt; ++s)
     if (!make_tmap(&g.b[s], A[s], r, K, (uint64_t)K * 2, r, 64)) return false;

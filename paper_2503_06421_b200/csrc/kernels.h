@@ -55,7 +55,14 @@ struct alignas(64) GemmParams {
   bf16* vt;            // V^T [n_vt][vt_ld] for the tcgen05 attention (segments with vt=1)
   int vt_ld;
   int ksplit, kblocks_per_split, src_rows;  // EPI_PARTIAL
+  int cg;              // 1: single-CTA 128-row tiles; 2: CTA pair, 256-row tiles (cta_group::2)
 };
+
+// CTA-group size for an M-row GEMM, and the TMA box rows of the W and lora_B
+// maps a CTA loads for (epi, bn, cg).
+int gemm_pick_cg(int M);
+int gemm_b_box(int epi, int bn, int cg);
+int gemm_tb_box(int epi, int bn, int cg);
 
 // LoRA shrink on tensor cores: T_t = bf16(scale * X A_t^T) for nt targets
 // sharing X, as a split-K EPI_PARTIAL GEMM into ws plus a fixed-order reduce.

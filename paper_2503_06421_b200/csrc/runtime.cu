@@ -114,7 +114,8 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
   const int nq = m.n_heads * hd / world, nkv = m.n_kv_heads * hd / world;
   const int F = m.d_ff / world;
   const int r = tt.lora_rank;
-  const int mt = (S + GEMM_BM - 1) / GEMM_BM;
+  const int cg = gemm_pick_cg(S);
+  const int mt = (S + GEMM_BM * cg - 1) / (GEMM_BM * cg);
   std::vector<LayerLaunch> v(L);
   auto W = [&](int id) { return wptr[id]; };
   for (int l = 0; l < L; ++l) {
@@ -129,18 +130,19 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     q.lora_r = 0;
     q.total_tiles = 0;
     q.bn = gemm_pick_bn(EPI_ROPE, S, segn, 3, num_sms);
+    q.cg = cg;
     for (int s = 0; s < 3; ++s) {
       q.seg[s].n = segn[s];
       q.seg[s].out_col = col;
       q.seg[s].rope = s < 2;
       col += segn[s];
-      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, q.bn);
+      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, gemm_b_box(EPI_ROPE, q.bn, cg));
       const int la = tt.lora_a[l][tg[s]];
       q.seg[s].lora = la >= 0;
       if (la >= 0) {
         q.lora_r = r;
         tmap(&q.ta[s], T[tg[s]], S, r, 128);
-        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, q.bn);
+        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, gemm_tb_box(EPI_ROPE, q.bn, cg));
       }
       q.n_tiles[s] = (segn[s] + q.bn - 1) / q.bn;
       q.total_tiles += q.n_tiles[s] * mt;
@@ -160,14 +162,15 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     GemmParams& o = ll.o;
     memset(&o, 0, sizeof o);
     o.bn = gemm_pick_bn(EPI_RESID, S, &d, 1, num_sms);
+    o.cg = cg;
     tmap(&o.a, O, S, nq, 128);
-    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, o.bn);
+    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, gemm_b_box(EPI_RESID, o.bn, cg));
     o.seg[0].n = d;
     o.seg[0].lora = tt.lora_a[l][T_O] >= 0;
     if (o.seg[0].lora) {
       o.lora_r = r;
       tmap(&o.ta[0], T[T_O], S, r, 128);
-      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, o.bn);
+      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, gemm_tb_box(EPI_RESID, o.bn, cg));
     }
     o.nseg = 1;
     o.M = S;
@@ -189,11 +192,12 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
       g.lora_r = r;
       tmap(&g.ta[0], T[T_GATE], S, r, 128);
       tmap(&g.ta[1], T[T_UP], S, r, 128);
-      tmap(&g.tb[0], W(tt.lora_b[l][T_GATE]), F, r, 128);
-      tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, 128);
+      tmap(&g.tb[0], W(tt.lora_b[l][T_GATE]), F, r, gemm_tb_box(EPI_SILU, 128, cg));
+      tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, gemm_tb_box(EPI_SILU, 128, cg));
     }
     g.nseg = 1;
     g.bn = 128;
+    g.cg = cg;
     g.M = S;
     g.K = d;
     g.m_tiles = mt;
@@ -205,14 +209,15 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     GemmParams& dn = ll.down;
     memset(&dn, 0, sizeof dn);
     dn.bn = gemm_pick_bn(EPI_RESID, S, &d, 1, num_sms);
+    dn.cg = cg;
     tmap(&dn.a, Hb, S, F, 128);
-    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, dn.bn);
+    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, gemm_b_box(EPI_RESID, dn.bn, cg));
     dn.seg[0].n = d;
     dn.seg[0].lora = tt.lora_a[l][T_DOWN] >= 0;
     if (dn.seg[0].lora) {
       dn.lora_r = r;
       tmap(&dn.ta[0], T[T_DOWN], S, r, 128);
-      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, dn.bn);
+      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, gemm_tb_box(EPI_RESID, dn.bn, cg));
     }
     dn.nseg = 1;
     dn.M = S;
@@ -330,7 +335,12 @@ void run_forward(Exec& ex, const RunArgs& a) {
   const auto& LP = ex.layer_params(tt, S, a.akey, a.gen);
   cudaStream_t st = ex.compute;
   int waited = -1;
-  auto P0 = [&]() { return ex.profile ? ex.prof_begin() : -1; };
+  // event pair around a launch: every launch (profile_all) or the GEMMs only
+  auto P0 = [&](int cls = -1) {
+    if (!ex.profile) return -1;
+    if (!ex.profile_all && cls < 0) return -1;
+    return ex.prof_begin();
+  };
   auto K = [&](int cls, int ev, double fl, double by, cudaError_t e, const char* what) {
     cuda_check(e, what);
     ++ex.launches;
@@ -398,7 +408,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         shrink(ex.Xn, d, d, l, 0);
         {
           const double n = nq + 2.0 * nkv;
-          const int e0 = P0();
+          const int e0 = P0(KC_GEMM_QKV);
           K(KC_GEMM_QKV, e0, 2.0 * Sd * (n * d + r * lora_n(l, {T_Q, T_K, T_V})),
             2.0 * (n * d + Sd * d + Sd * n), gemm_launch(LP[l].qkv, EPI_ROPE, ex.num_sms, st),
             "gemm_qkv");
@@ -422,7 +432,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         if (ex.world > 1 && ex.rank != 0)
           cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
         {
-          const int e0 = P0();
+          const int e0 = P0(KC_GEMM_O);
           K(KC_GEMM_O, e0, 2.0 * Sd * d * ((double)nq + r * lora_n(l, {T_O}) / d),
             2.0 * ((double)d * nq + Sd * nq) + 8.0 * Sd * d,
             gemm_launch(LP[l].o, EPI_RESID, ex.num_sms, st), "gemm_o");
@@ -438,7 +448,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_GU:
         shrink(ex.Xn, d, d, l, 2);
         {
-          const int e0 = P0();
+          const int e0 = P0(KC_GEMM_GU);
           K(KC_GEMM_GU, e0, 2.0 * Sd * (2.0 * F * d + r * lora_n(l, {T_GATE, T_UP})),
             2.0 * (2.0 * F * d + Sd * d + Sd * F), gemm_launch(LP[l].gu, EPI_SILU, ex.num_sms, st),
             "gemm_gate_up");
@@ -451,7 +461,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         if (ex.world > 1 && ex.rank != 0)
           cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
         {
-          const int e0 = P0();
+          const int e0 = P0(KC_GEMM_DOWN);
           K(KC_GEMM_DOWN, e0, 2.0 * Sd * ((double)d * F + r * lora_n(l, {T_DOWN})),
             2.0 * ((double)d * F + Sd * F) + 8.0 * Sd * d,
             gemm_launch(LP[l].down, EPI_RESID, ex.num_sms, st), "gemm_down");

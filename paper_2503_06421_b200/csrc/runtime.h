@@ -62,7 +62,7 @@ struct Exec {
   int launches = 0;
   // per-kernel-class timing (TIDAL_DEBUG_PROFILE): event pairs on the compute
   // stream around every launch, plus each launch's algorithmic flops/bytes
-  bool profile = false;
+  bool profile = false, profile_all = false;
   std::vector<cudaEvent_t> prof_ev;
   struct ProfRec {
     int cls;

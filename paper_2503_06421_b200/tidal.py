@@ -20,6 +20,7 @@ ERR_NAMES = {0: "OK", 1: "INVALID", 2: "OOM", 3: "CUDA", 4: "NCCL", 5: "STRUCTUR
              6: "RESIDENCY", 7: "COW", 8: "BUFSZ", 9: "NUMERIC"}
 GROUPS_PER_LAYER, GROUPS_MAX_TRANSFERS, GROUPS_PER_TENSOR = 0, 1, 2
 DEBUG_POISON, DEBUG_SKIP_BARRIER, DEBUG_SCRUB_L2, DEBUG_SERIAL, DEBUG_PROFILE = 1, 2, 4, 8, 16
+DEBUG_PROFILE_GEMM = 32
 U64_MAX = (1 << 64) - 1
 
 

@@ -70,12 +70,15 @@ def test_gemm_residual_fp32(T, M, N, K):
     assert np.abs(X.cpu().numpy() - ref).max() <= 1e-4 * np.abs(ref).max()
 
 
+@pytest.mark.parametrize("cg", [1, 2])
 @pytest.mark.parametrize("bn", [128, 192, 256])
 @pytest.mark.parametrize("epi", [0, 3])
-def test_gemm_tile_widths(T, bn, epi):
-    """Every N-tile width the runtime may pick (gemm_pick_bn), with a ragged
-    N tail (N = 5*bn - 64) and LoRA, for the store and residual epilogues."""
-    rng = np.random.default_rng(bn + epi)
+def test_gemm_tile_widths(T, bn, epi, cg):
+    """Every N-tile width the runtime may pick (gemm_pick_bn), single-SM and
+    CTA-pair (cta_group::2) tiles, with a ragged N tail (N = 5*bn - 64), a
+    ragged M tail and LoRA, for the store and residual epilogues."""
+    rng = np.random.default_rng(bn + epi + cg)
+    epi_code = epi | (bn << 8) | (cg << 20)
     M, K, r = 260, 512, 16
     N = 5 * bn - 64
     A, W = _bf(rng, (M, K)), _bf(rng, (N, K), 1 / math.sqrt(K))
@@ -83,12 +86,12 @@ def test_gemm_tile_widths(T, bn, epi):
     ref = A @ W.T + Tm @ B.T
     if epi == 0:
         out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
-        T.k_gemm(epi | (bn << 8), _dev(A), [_dev(W)], [N], out, N, M, K, [_dev(Tm)], [_dev(B)], r)
+        T.k_gemm(epi_code, _dev(A), [_dev(W)], [N], out, N, M, K, [_dev(Tm)], [_dev(B)], r)
         _close_bf16(_host(out), ref)
     else:
         X0 = rng.standard_normal((M, N)).astype(np.float32)
         X = torch.from_numpy(X0.copy()).cuda()
-        T.k_gemm(epi | (bn << 8), _dev(A), [_dev(W)], [N], X, N, M, K, [_dev(Tm)], [_dev(B)], r)
+        T.k_gemm(epi_code, _dev(A), [_dev(W)], [N], X, N, M, K, [_dev(Tm)], [_dev(B)], r)
         assert np.abs(X.cpu().numpy() - (X0 + ref)).max() <= 2e-4 * np.abs(X0 + ref).max()
 
 
@@ -103,10 +106,11 @@ def test_gemm_lora_k_extension(T, r):
     _close_bf16(_host(out), A @ W.T + Tm @ B.T)
 
 
-@pytest.mark.parametrize("Fd,lora", [(688, False), (688, True), (1024, True)])
-def test_gemm_silu_gate_up(T, Fd, lora):
-    rng = np.random.default_rng(Fd)
-    M, K, r = 150, 256, 16
+@pytest.mark.parametrize("Fd,lora,M", [(688, False, 150), (688, True, 150), (1024, True, 150),
+                                        (688, True, 100), (1376, True, 700)])
+def test_gemm_silu_gate_up(T, Fd, lora, M):
+    rng = np.random.default_rng(Fd + M)
+    K, r = 256, 16
     A = _bf(rng, (M, K))
     Wg, Wu = _bf(rng, (Fd, K), 1 / math.sqrt(K)), _bf(rng, (Fd, K), 1 / math.sqrt(K))
     out = torch.zeros(M, Fd, dtype=torch.bfloat16, device="cuda")
