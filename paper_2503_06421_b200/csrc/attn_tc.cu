@@ -27,9 +27,13 @@ namespace {
 constexpr int HD = 128, BQ = 128, BKV = 128;
 constexpr int TILE = 128 * 128 * 2;  // 32 KB: any 128 x 128 bf16 tile (two 64-wide K-blocks)
 constexpr int HALF = TILE / 2;
-constexpr int OFF_Q = 0, OFF_K = OFF_Q + TILE, OFF_V = OFF_K + 2 * TILE, OFF_P = OFF_V + 2 * TILE;
+// K and V have separate rings: K_j is released as soon as S_j is computed, so
+// the next K tiles stream in while softmax runs; V_j lives until PV_j.
+constexpr int KST = 2, VST = 3;
+constexpr int OFF_Q = 0, OFF_K = OFF_Q + TILE, OFF_V = OFF_K + KST * TILE,
+              OFF_P = OFF_V + VST * TILE;
 constexpr int OFF_BAR = OFF_P + TILE;
-constexpr int N_BARS = 10;
+constexpr int N_BARS = 3 + 2 * KST + 2 * VST + 2;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM = OFF_TMEM + 16 + 1024;
 constexpr int NTH = 192;
@@ -48,9 +52,11 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bars = sb + OFF_BAR;
   const uint32_t q_full = bars, p_full = bars + 8, pv_done = bars + 16;
-  auto kv_full = [&](int s) { return bars + 24 + 8u * s; };
-  auto kv_empty = [&](int s) { return bars + 40 + 8u * s; };
-  auto s_full = [&](int s) { return bars + 56 + 8u * s; };
+  auto k_full = [&](int s) { return bars + 24 + 8u * s; };
+  auto k_empty = [&](int s) { return bars + 24 + 8u * (KST + s); };
+  auto v_full = [&](int s) { return bars + 24 + 8u * (2 * KST + s); };
+  auto v_empty = [&](int s) { return bars + 24 + 8u * (2 * KST + VST + s); };
+  auto s_full = [&](int s) { return bars + 24 + 8u * (2 * KST + 2 * VST + s); };
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
 
   const int nq = (p.S + BQ - 1) / BQ;
@@ -66,11 +72,15 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(p_full, 128);
     ptx::mbar_init(pv_done, 1);
-    for (int s = 0; s < 2; ++s) {
-      ptx::mbar_init(kv_full(s), 1);
-      ptx::mbar_init(kv_empty(s), 1);
-      ptx::mbar_init(s_full(s), 1);
+    for (int s = 0; s < KST; ++s) {
+      ptx::mbar_init(k_full(s), 1);
+      ptx::mbar_init(k_empty(s), 1);
     }
+    for (int s = 0; s < VST; ++s) {
+      ptx::mbar_init(v_full(s), 1);
+      ptx::mbar_init(v_empty(s), 1);
+    }
+    for (int s = 0; s < 2; ++s) ptx::mbar_init(s_full(s), 1);
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
@@ -85,16 +95,20 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       ptx::mbar_expect_tx(q_full, TILE);
       ptx::tma_load_2d(&p.qkv, sb + OFF_Q, q_full, qc, q0);
       ptx::tma_load_2d(&p.qkv, sb + OFF_Q + HALF, q_full, qc + 64, q0);
+      // in-order issue K_0 V_0 K_1 V_1 ...: V_j's slot frees (PV_{j-3}) before
+      // K_{j+1}'s (S_{j-1}), so the single producer never waits needlessly
       for (int j = 0; j < nkv; ++j) {
-        const int s = j & 1;
-        ptx::mbar_wait(kv_empty(s), ((j >> 1) & 1) ^ 1);
-        const uint32_t fb = kv_full(s);
-        ptx::mbar_expect_tx(fb, 2 * TILE);
-        const uint32_t ks = sb + OFF_K + s * TILE, vs = sb + OFF_V + s * TILE;
-        ptx::tma_load_2d(&p.qkv, ks, fb, kc, j * BKV);
-        ptx::tma_load_2d(&p.qkv, ks + HALF, fb, kc + 64, j * BKV);
-        ptx::tma_load_2d(&p.vt, vs, fb, j * BKV, vr);
-        ptx::tma_load_2d(&p.vt, vs + HALF, fb, j * BKV + 64, vr);
+        const int s = j % KST, t = j % VST;
+        ptx::mbar_wait(k_empty(s), ((j / KST) & 1) ^ 1);
+        ptx::mbar_expect_tx(k_full(s), TILE);
+        const uint32_t ks = sb + OFF_K + s * TILE;
+        ptx::tma_load_2d(&p.qkv, ks, k_full(s), kc, j * BKV);
+        ptx::tma_load_2d(&p.qkv, ks + HALF, k_full(s), kc + 64, j * BKV);
+        ptx::mbar_wait(v_empty(t), ((j / VST) & 1) ^ 1);
+        ptx::mbar_expect_tx(v_full(t), TILE);
+        const uint32_t vs = sb + OFF_V + t * TILE;
+        ptx::tma_load_2d(&p.vt, vs, v_full(t), j * BKV, vr);
+        ptx::tma_load_2d(&p.vt, vs + HALF, v_full(t), j * BKV + 64, vr);
       }
     }
     __syncwarp();
@@ -103,31 +117,35 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       constexpr uint32_t IDESC = ptx::idesc_bf16(128, 128);
       ptx::mbar_wait(q_full, 0);
       auto issue_s = [&](int j) {
-        const int s = j & 1;
-        ptx::mbar_wait(kv_full(s), (j >> 1) & 1);
+        const int s = j % KST;
+        ptx::mbar_wait(k_full(s), (j / KST) & 1);
         ptx::tc_fence_after();
         const uint32_t ks = sb + OFF_K + s * TILE;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
           const uint32_t off = (kk >> 2) * HALF;
-          ptx::mma_bf16(tmem + COL_S0 + s * 128, ptx::desc_sw128(sb + OFF_Q + off) + 2 * (kk & 3),
+          ptx::mma_bf16(tmem + COL_S0 + (j & 1) * 128,
+                        ptx::desc_sw128(sb + OFF_Q + off) + 2 * (kk & 3),
                         ptx::desc_sw128(ks + off) + 2 * (kk & 3), IDESC, kk > 0);
         }
-        ptx::mma_commit(s_full(s));
+        ptx::mma_commit(s_full(j & 1));
+        ptx::mma_commit(k_empty(s));
       };
       issue_s(0);
       for (int j = 0; j < nkv; ++j) {
         if (j + 1 < nkv) issue_s(j + 1);
+        const int t = j % VST;
         ptx::mbar_wait(p_full, j & 1);
+        ptx::mbar_wait(v_full(t), (j / VST) & 1);
         ptx::tc_fence_after();
-        const uint32_t vs = sb + OFF_V + (j & 1) * TILE;
+        const uint32_t vs = sb + OFF_V + t * TILE;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
           const uint32_t off = (kk >> 2) * HALF;
           ptx::mma_bf16(tmem + COL_O, ptx::desc_sw128(sb + OFF_P + off) + 2 * (kk & 3),
                         ptx::desc_sw128(vs + off) + 2 * (kk & 3), IDESC, (j | kk) != 0);
         }
-        ptx::mma_commit(kv_empty(j & 1));
+        ptx::mma_commit(v_empty(t));
         ptx::mma_commit(pv_done);
       }
     }
@@ -150,16 +168,17 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         ptx::tmem_ld32(tmem + lane_base + COL_S0 + (j & 1) * 128 + c * 32, r);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]) * p.scale_log2;
+        for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]);  // raw scores
       }
       if (j == qt) {  // diagonal tile: causal mask
 #pragma unroll
         for (int i = 0; i < 128; ++i)
           if (j * BKV + i > qi) v[i] = -INFINITY;
       }
-      float mx = m_used;
+      float mraw = -INFINITY;
 #pragma unroll
-      for (int i = 0; i < 128; ++i) mx = fmaxf(mx, v[i]);
+      for (int i = 0; i < 128; ++i) mraw = fmaxf(mraw, v[i]);
+      const float mx = fmaxf(m_used, mraw * p.scale_log2);  // scale > 0: max commutes
       const bool need = mx > m_used + 8.f;
       if (j > 0) ptx::mbar_wait(pv_done, (j - 1) & 1);  // P buffer free, O settled
       if (j > 0 && __any_sync(0xffffffffu, need)) {
@@ -185,7 +204,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         float e[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          e[i] = exp2f(v[c * 8 + i] - m_used);
+          e[i] = exp2f(fmaf(v[c * 8 + i], p.scale_log2, -m_used));
           l += e[i];
         }
         uint4 w;
