@@ -1,0 +1,71 @@
+"""Full-size parity in the launch configuration bench.py times (GPU, slow).
+
+BASELINE.json configs[1] (Llama2-7B shape, fully streamed, no adapter) and
+configs[2] (Llama2-13B shape, rank-16 LoRA on all 7 targets, template-start
+with most weights resident) at S = 2048: tidal_invoke_prefill's last-position
+logits against the plain fp32 oracle forward on the same seeded weights
+(max-abs 2e-2, first token by the margin rule A6).  The oracle streams its
+weights layer by layer from the C generator (keep=False), so host memory stays
+bounded; on a 16-core host a full 13B forward takes ~1-2 min.
+"""
+import numpy as np
+import pytest
+
+import synth
+from oracle import forward as F
+
+torch = pytest.importorskip("torch")
+pytestmark = [pytest.mark.gpu, pytest.mark.slow]
+
+TOL, MARGIN = 2e-2, 4e-2
+
+
+@pytest.fixture(scope="module")
+def T():
+    if not torch.cuda.is_available():
+        pytest.skip("no GPU")
+    from paper_2503_06421_b200 import build
+    build.build()
+    from paper_2503_06421_b200 import tidal
+    tidal.lib()
+    return tidal
+
+
+def _cfg_dict(cfg):
+    return dict(n_layers=cfg.n_layers, d_model=cfg.d_model, n_heads=cfg.n_heads,
+                n_kv_heads=cfg.n_kv_heads, d_ff=cfg.d_ff, vocab=cfg.vocab,
+                rope_theta=cfg.rope_theta, rms_eps=cfg.rms_eps)
+
+
+@pytest.mark.parametrize("name,rank,rho", [("7b", 0, 0.0), ("13b", 16, 0.9)])
+def test_full_size_prefill_matches_oracle(T, name, rank, rho):
+    cfg = synth.config(name)
+    S = 2048
+    tensors, fill = synth.model_inputs(cfg, 0)
+    model = T.Model(_cfg_dict(cfg), tensors, "base:0", fill=fill)
+    trace = T.Trace(model)
+    M = sum(s.nbytes for s in synth.base_tensors(cfg))
+    tpl = T.Template(model, trace, T.template_opts(resident_bytes=int(rho * M), max_tokens=S,
+                                                   device=0))
+    tpl.set_debug(T.DEBUG_POISON)        # streamed weights must really arrive before use
+    ad = None
+    if rank:
+        slots, total = tpl.adapter_layout(rank, 0x7F)
+        buf = T.PinnedBuffer(total)
+        synth.adapter_fill(cfg, rank, 1, slots, buf.view(), 0x7F)
+        ad = T.Adapter(tpl, rank, 1.0, 0x7F, buf, total, "adapter:1")
+    tokens = synth.prompt_fast(cfg, S, 0)
+    tok, logits, st = tpl.invoke(tokens, ad)
+    c0 = tpl.checksum()
+    del tpl, model
+    torch.cuda.empty_cache()
+    ref = F.forward(cfg, F.synth_weights(cfg, 0, fast=True, keep=False), tokens,
+                    F.synth_adapter(cfg, rank, 1, fast=True) if rank else None,
+                    0x7F if rank else 0, 1.0)
+    err = float(np.abs(logits - ref["logits"]).max())
+    assert err <= TOL, err
+    top = np.sort(ref["logits"])[-2:]
+    if top[1] - top[0] > MARGIN:
+        assert tok == ref["token"]
+    assert ref["logits"][tok] >= ref["logits"].max() - MARGIN
+    assert c0 != 0
