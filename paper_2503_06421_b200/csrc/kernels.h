@@ -80,8 +80,9 @@ constexpr int SHRINK_MAX_SPLIT = 16;
 // tcgen05 causal attention (hd = 128): Q/K from QKV [S, (H+2KV)*128], V from
 // V^T [KV*128][vt_ld] (written by the QKV epilogue).
 struct alignas(64) AttnParams {
-  CUtensorMap qkv;  // box {64, 128}
-  CUtensorMap vt;   // box {64 keys, 128 rows}
+  CUtensorMap q;    // over QKV, box {64 cols, 128 rows}
+  CUtensorMap k;    // over QKV, box {64 cols, 64 rows}
+  CUtensorMap vt;   // over V^T, box {64 keys, 128 rows}
   int S, H, KV;
   float scale_log2;
   bf16* out;
