@@ -38,12 +38,13 @@ constexpr int OFF_K = OFF_Q + 2 * QTILE;
 constexpr int OFF_V = OFF_K + RING * KTILE;
 constexpr int OFF_P = OFF_V + RING * VTILE;            // P_A, P_B
 constexpr int OFF_BAR = OFF_P + 2 * PTILE;
-constexpr int N_BARS = 1 + 4 * RING + 6;
+constexpr int N_BARS = 1 + 4 * RING + 8;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM = OFF_TMEM + 16 + 1024;
 constexpr int NTH = 320;
-// TMEM columns: S_A, S_B (64 each), O_A, O_B (128 each)
-constexpr uint32_t COL_S = 0, COL_O = 128;
+// TMEM columns: S_A[2], S_B[2] (64 each: S is double-buffered per tile, so
+// S_x(j+1) is computed while softmax x works on S_x(j)), O_A, O_B (128 each)
+constexpr uint32_t COL_S = 0, COL_O = 256;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -62,9 +63,9 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
   auto k_empty = [&](int s) { return bars + 8u * (1 + RING + s); };
   auto v_full = [&](int s) { return bars + 8u * (1 + 2 * RING + s); };
   auto v_empty = [&](int s) { return bars + 8u * (1 + 3 * RING + s); };
-  auto s_full = [&](int x) { return bars + 8u * (1 + 4 * RING + x); };
-  auto p_full = [&](int x) { return bars + 8u * (3 + 4 * RING + x); };
-  auto pv_done = [&](int x) { return bars + 8u * (5 + 4 * RING + x); };
+  auto s_full = [&](int x, int b) { return bars + 8u * (1 + 4 * RING + 2 * x + b); };
+  auto p_full = [&](int x) { return bars + 8u * (5 + 4 * RING + x); };
+  auto pv_done = [&](int x) { return bars + 8u * (7 + 4 * RING + x); };
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
 
   const int nq = (p.S + BQ - 1) / BQ;
@@ -89,7 +90,8 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       ptx::mbar_init(v_empty(s), 1);
     }
     for (int x = 0; x < 2; ++x) {
-      ptx::mbar_init(s_full(x), 1);
+      ptx::mbar_init(s_full(x, 0), 1);
+      ptx::mbar_init(s_full(x, 1), 1);
       ptx::mbar_init(p_full(x), 128);
       ptx::mbar_init(pv_done(x), 1);
     }
@@ -137,9 +139,10 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         const uint32_t qs = sb + OFF_Q + x * QTILE, ks = sb + OFF_K + s * KTILE;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk)
-          ptx::mma_bf16(tmem + COL_S + x * BKV, ptx::desc_sw128(qs + (kk >> 2) * QHALF) + 2 * (kk & 3),
+          ptx::mma_bf16(tmem + COL_S + (2 * x + (j & 1)) * BKV,
+                        ptx::desc_sw128(qs + (kk >> 2) * QHALF) + 2 * (kk & 3),
                         ptx::desc_sw128(ks + (kk >> 2) * KHALF) + 2 * (kk & 3), IDESC_S, kk > 0);
-        ptx::mma_commit(s_full(x));
+        ptx::mma_commit(s_full(x, j & 1));
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x V_j  (128 x 128, K = 64)
         ptx::mbar_wait(p_full(x), j & 1);
@@ -152,17 +155,21 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
                         ptx::desc_sw128(vs) + 2 * kk, IDESC_O, (j | kk) != 0);
         ptx::mma_commit(pv_done(x));
       };
-      for (int x = 0; x < 2; ++x)
-        if (nt[x]) issue_s(x, 0);
-      ptx::mma_commit(k_empty(0));
+      // S runs two tiles ahead of PV: S_x(j+2) reuses the S buffer of tile j,
+      // which softmax x has released by the time P_x(j) is published.
+      for (int jj = 0; jj < 2 && jj < nmax; ++jj) {
+        for (int x = 0; x < 2; ++x)
+          if (jj < nt[x]) issue_s(x, jj);
+        ptx::mma_commit(k_empty(jj % RING));
+      }
       for (int j = 0; j < nmax; ++j) {
         for (int x = 0; x < 2; ++x) {
           if (j >= nt[x]) continue;
           issue_pv(x, j);
-          if (j + 1 < nt[x]) issue_s(x, j + 1);
+          if (j + 2 < nt[x]) issue_s(x, j + 2);
         }
         ptx::mma_commit(v_empty(j % RING));
-        if (j + 1 < nmax) ptx::mma_commit(k_empty((j + 1) % RING));
+        if (j + 2 < nmax) ptx::mma_commit(k_empty((j + 2) % RING));
       }
     }
     __syncwarp();
@@ -175,12 +182,12 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     const int n = nt[x];
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     uint8_t* Ps = smem + OFF_P + x * PTILE;
-    const uint32_t s_col = tmem + lane_base + COL_S + x * BKV;
     const uint32_t o_col = tmem + lane_base + COL_O + x * HD;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n; ++j) {
-      ptx::mbar_wait(s_full(x), j & 1);
+      ptx::mbar_wait(s_full(x, j & 1), (j >> 1) & 1);
       ptx::tc_fence_after();
+      const uint32_t s_col = tmem + lane_base + COL_S + (2 * x + (j & 1)) * BKV;
       float v[BKV];
 #pragma unroll
       for (int c = 0; c < BKV / 32; ++c) {
