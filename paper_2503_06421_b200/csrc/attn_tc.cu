@@ -36,9 +36,9 @@ constexpr int PTILE = BQ * BKV * 2;     // 16 KB: P [128 q][64 keys], one K-bloc
 constexpr int OFF_Q = 0;                               // Q_A, Q_B
 constexpr int OFF_K = OFF_Q + 2 * QTILE;
 constexpr int OFF_V = OFF_K + RING * KTILE;
-constexpr int OFF_P = OFF_V + RING * VTILE;            // P_A, P_B
-constexpr int OFF_BAR = OFF_P + 2 * PTILE;
-constexpr int N_BARS = 1 + 4 * RING + 8;
+constexpr int OFF_P = OFF_V + RING * VTILE;            // P_A[2], P_B[2] (double-buffered)
+constexpr int OFF_BAR = OFF_P + 4 * PTILE;
+constexpr int N_BARS = 1 + 4 * RING + 10;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM = OFF_TMEM + 16 + 1024;
 constexpr int NTH = 320;
@@ -65,7 +65,8 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
   auto v_empty = [&](int s) { return bars + 8u * (1 + 3 * RING + s); };
   auto s_full = [&](int x, int b) { return bars + 8u * (1 + 4 * RING + 2 * x + b); };
   auto p_full = [&](int x) { return bars + 8u * (5 + 4 * RING + x); };
-  auto pv_done = [&](int x) { return bars + 8u * (7 + 4 * RING + x); };
+  // one PV-done barrier per P buffer: a waiter never sees a phase two ahead
+  auto pv_done = [&](int x, int b) { return bars + 8u * (7 + 4 * RING + 2 * x + b); };
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
 
   const int nq = (p.S + BQ - 1) / BQ;
@@ -93,7 +94,8 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       ptx::mbar_init(s_full(x, 0), 1);
       ptx::mbar_init(s_full(x, 1), 1);
       ptx::mbar_init(p_full(x), 128);
-      ptx::mbar_init(pv_done(x), 1);
+      ptx::mbar_init(pv_done(x, 0), 1);
+      ptx::mbar_init(pv_done(x, 1), 1);
     }
     ptx::fence_mbar_init();
   }
@@ -148,12 +150,13 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         ptx::mbar_wait(p_full(x), j & 1);
         ptx::mbar_wait(v_full(j % RING), (j / RING) & 1);
         ptx::tc_fence_after();
-        const uint32_t ps = sb + OFF_P + x * PTILE, vs = sb + OFF_V + (j % RING) * VTILE;
+        const uint32_t ps = sb + OFF_P + (2 * x + (j & 1)) * PTILE,
+                       vs = sb + OFF_V + (j % RING) * VTILE;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk)
           ptx::mma_bf16(tmem + COL_O + x * HD, ptx::desc_sw128(ps) + 2 * kk,
                         ptx::desc_sw128(vs) + 2 * kk, IDESC_O, (j | kk) != 0);
-        ptx::mma_commit(pv_done(x));
+        ptx::mma_commit(pv_done(x, j & 1));
       };
       // S runs two tiles ahead of PV: S_x(j+2) reuses the S buffer of tile j,
       // which softmax x has released by the time P_x(j) is published.
@@ -181,7 +184,6 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     const int qi = qt[x] * BQ + row;
     const int n = nt[x];
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    uint8_t* Ps = smem + OFF_P + x * PTILE;
     const uint32_t o_col = tmem + lane_base + COL_O + x * HD;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < n; ++j) {
@@ -189,26 +191,33 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       ptx::tc_fence_after();
       const uint32_t s_col = tmem + lane_base + COL_S + (2 * x + (j & 1)) * BKV;
       float v[BKV];
-#pragma unroll
-      for (int c = 0; c < BKV / 32; ++c) {
-        uint32_t r[32];
-        ptx::tmem_ld32(s_col + c * 32, r);
+      {
+        uint32_t r0[32], r1[32];
+        ptx::tmem_ld32(s_col, r0);
+        ptx::tmem_ld32(s_col + 32, r1);
         ptx::tmem_ld_wait();
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[c * 32 + i] = __uint_as_float(r[i]);  // raw scores
+        for (int i = 0; i < 32; ++i) {
+          v[i] = __uint_as_float(r0[i]);  // raw scores
+          v[32 + i] = __uint_as_float(r1[i]);
+        }
       }
       if ((j + 1) * BKV > qt[x] * BQ) {  // tiles reaching the diagonal: causal mask
 #pragma unroll
         for (int i = 0; i < BKV; ++i)
           if (j * BKV + i > qi) v[i] = -INFINITY;
       }
-      float mraw = -INFINITY;
+      float mr[8];  // 8 independent max chains
 #pragma unroll
-      for (int i = 0; i < BKV; ++i) mraw = fmaxf(mraw, v[i]);
+      for (int k = 0; k < 8; ++k) mr[k] = v[k];
+#pragma unroll
+      for (int i = 8; i < BKV; ++i) mr[i & 7] = fmaxf(mr[i & 7], v[i]);
+      const float mraw = fmaxf(fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3])),
+                               fmaxf(fmaxf(mr[4], mr[5]), fmaxf(mr[6], mr[7])));
       const float mx = fmaxf(m_used, mraw * p.scale_log2);  // scale > 0: max commutes
       const bool need = mx > m_used + 8.f;
-      if (j > 0) ptx::mbar_wait(pv_done(x), (j - 1) & 1);  // P_x free, O_x settled
       if (j > 0 && __any_sync(0xffffffffu, need)) {
+        ptx::mbar_wait(pv_done(x, (j - 1) & 1), ((j - 1) >> 1) & 1);  // O_x settled
         ptx::tc_fence_after();
         const float corr = need ? exp2f(m_used - mx) : 1.f;
 #pragma unroll 1
@@ -224,14 +233,18 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         l *= corr;
       }
       if (need) m_used = mx;
+      // P buffer j&1 was last read by PV_x(j-2)
+      if (j > 1) ptx::mbar_wait(pv_done(x, j & 1), ((j - 2) >> 1) & 1);
+      uint8_t* Ps = smem + OFF_P + (2 * x + (j & 1)) * PTILE;
       // P = exp2(s*scale - m) -> bf16, SWIZZLE_128B K-major [128 rows][64 keys]
+      float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent sum chains
 #pragma unroll
       for (int c = 0; c < BKV / 8; ++c) {
         float e[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
           e[i] = exp2f(fmaf(v[c * 8 + i], p.scale_log2, -m_used));
-          l += e[i];
+          ls[i] += e[i];
         }
         uint4 w;
         w.x = pack_bf16x2(e[0], e[1]);
@@ -240,13 +253,14 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         w.w = pack_bf16x2(e[6], e[7]);
         *reinterpret_cast<uint4*>(Ps + row * 128 + ((c ^ (row & 7)) << 4)) = w;
       }
+      l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full(x));
     }
     if (n > 0) {
       // epilogue: O / l -> bf16
-      ptx::mbar_wait(pv_done(x), (n - 1) & 1);
+      ptx::mbar_wait(pv_done(x, (n - 1) & 1), ((n - 1) >> 1) & 1);
       ptx::tc_fence_after();
       const float inv = 1.f / l;
       bf16* out = p.out + (size_t)qi * p.ldo + h * HD;
