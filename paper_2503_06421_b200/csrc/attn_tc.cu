@@ -38,7 +38,7 @@ constexpr int OFF_K = OFF_Q + 2 * QTILE;
 constexpr int OFF_V = OFF_K + RING * KTILE;
 constexpr int OFF_P = OFF_V + RING * VTILE;            // P_A[2], P_B[2] (double-buffered)
 constexpr int OFF_BAR = OFF_P + 4 * PTILE;
-constexpr int N_BARS = 1 + 4 * RING + 10;
+constexpr int N_BARS = 1 + 4 * RING + 12;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM = OFF_TMEM + 16 + 1024;
 constexpr int NTH = 320;
@@ -64,9 +64,11 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
   auto v_full = [&](int s) { return bars + 8u * (1 + 2 * RING + s); };
   auto v_empty = [&](int s) { return bars + 8u * (1 + 3 * RING + s); };
   auto s_full = [&](int x, int b) { return bars + 8u * (1 + 4 * RING + 2 * x + b); };
-  auto p_full = [&](int x) { return bars + 8u * (5 + 4 * RING + x); };
-  // one PV-done barrier per P buffer: a waiter never sees a phase two ahead
-  auto pv_done = [&](int x, int b) { return bars + 8u * (7 + 4 * RING + 2 * x + b); };
+  // P-full and PV-done barriers per P buffer: softmax may run one tile ahead of
+  // the MMA warp, so a single barrier could complete two phases before the
+  // waiter looks (parity aliasing); per-buffer barriers cannot.
+  auto p_full = [&](int x, int b) { return bars + 8u * (5 + 4 * RING + 2 * x + b); };
+  auto pv_done = [&](int x, int b) { return bars + 8u * (9 + 4 * RING + 2 * x + b); };
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
 
   const int nq = (p.S + BQ - 1) / BQ;
@@ -93,7 +95,8 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     for (int x = 0; x < 2; ++x) {
       ptx::mbar_init(s_full(x, 0), 1);
       ptx::mbar_init(s_full(x, 1), 1);
-      ptx::mbar_init(p_full(x), 128);
+      ptx::mbar_init(p_full(x, 0), 128);
+      ptx::mbar_init(p_full(x, 1), 128);
       ptx::mbar_init(pv_done(x, 0), 1);
       ptx::mbar_init(pv_done(x, 1), 1);
     }
@@ -147,7 +150,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         ptx::mma_commit(s_full(x, j & 1));
       };
       auto issue_pv = [&](int x, int j) {  // O_x += P_x V_j  (128 x 128, K = 64)
-        ptx::mbar_wait(p_full(x), j & 1);
+        ptx::mbar_wait(p_full(x, j & 1), (j >> 1) & 1);
         ptx::mbar_wait(v_full(j % RING), (j / RING) & 1);
         ptx::tc_fence_after();
         const uint32_t ps = sb + OFF_P + (2 * x + (j & 1)) * PTILE,
@@ -256,7 +259,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full(x));
+      ptx::mbar_arrive(p_full(x, j & 1));
     }
     if (n > 0) {
       // epilogue: O / l -> bf16

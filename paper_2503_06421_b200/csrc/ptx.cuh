@@ -36,8 +36,13 @@ __device__ __forceinline__ bool mbar_try_wait(uint32_t bar, uint32_t parity) {
       : "memory");
   return ok != 0;
 }
+// Watchdog: try_wait suspends for a bounded time per call, so ~2^28 failed
+// polls is many seconds — a protocol bug then traps (a CUDA error the host
+// reports) instead of hanging the GPU.
 __device__ __forceinline__ void mbar_wait(uint32_t bar, uint32_t parity) {
+  uint32_t n = 0;
   while (!mbar_try_wait(bar, parity)) {
+    if (++n == (1u << 28)) __trap();
   }
 }
 
