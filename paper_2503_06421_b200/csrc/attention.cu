@@ -11,6 +11,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace tidal {
 namespace {
@@ -63,6 +64,8 @@ __global__ void __launch_bounds__(NTH, 2) attn_kernel(const bf16* __restrict__ q
   bf16* qs = reinterpret_cast<bf16*>(sm);
   bf16* ks = qs + BQ * HD;          // [2][BKV * HD]
   bf16* vs = ks + 2 * BKV * HD;     // [2][BKV * HD]
+  asm volatile("griddepcontrol.wait;" ::: "memory");  // PDL: previous kernel complete
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   const int nq = (S + BQ - 1) / BQ;
   const int qt = nq - 1 - blockIdx.x;
   const int h = blockIdx.y;
@@ -240,8 +243,7 @@ cudaError_t launch(const bf16* qkv, bf16* O, int S, int H, int KV, cudaStream_t 
   }
   dim3 grid((S + BQ - 1) / BQ, H);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
-  attn_kernel<HD><<<grid, NTH, smem, s>>>(qkv, O, S, H, KV, scale_log2);
-  return cudaGetLastError();
+  return launch_k(attn_kernel<HD>, grid, dim3(NTH), smem, s, 1, qkv, O, S, H, KV, scale_log2);
 }
 
 }  // namespace

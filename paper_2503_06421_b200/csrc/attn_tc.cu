@@ -19,6 +19,7 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 
 namespace tidal {
@@ -88,6 +89,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_holder;
+  ptx::pdl_begin();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -286,8 +288,7 @@ cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
     attr = true;
   }
   dim3 grid((p.S + BQ - 1) / BQ, p.H);
-  attn_tc_kernel<<<grid, NTH, SMEM, s>>>(p);
-  return cudaGetLastError();
+  return launch_k(attn_tc_kernel, grid, dim3(NTH), SMEM, s, 1, p);
 }
 
 }  // namespace tidal

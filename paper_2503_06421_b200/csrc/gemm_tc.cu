@@ -22,6 +22,7 @@
 #include <mutex>
 
 #include "kernels.h"
+#include "launch.cuh"
 #include "ptx.cuh"
 #include "ptx2.cuh"
 
@@ -236,6 +237,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem_base = *tmem_holder;
+  ptx::pdl_begin();  // prologue above overlapped the previous kernel's tail
 
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
@@ -507,23 +509,7 @@ cudaError_t launch_t(const GemmParams& p, int num_sms, cudaStream_t s) {
   const int units = num_sms / CG;
   const int grid = (p.total_tiles < units ? p.total_tiles : units) * CG;
   if (grid <= 0) return cudaSuccess;
-  if (CG == 1) {
-    gemm_tc_kernel<EPI, BNT, CG><<<grid, NTHREADS, SMEM_BYTES, s>>>(p);
-    return cudaGetLastError();
-  }
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(grid);
-  cfg.blockDim = dim3(NTHREADS);
-  cfg.dynamicSmemBytes = SMEM_BYTES;
-  cfg.stream = s;
-  cudaLaunchAttribute attr[1];
-  attr[0].id = cudaLaunchAttributeClusterDimension;
-  attr[0].val.clusterDim.x = 2;
-  attr[0].val.clusterDim.y = 1;
-  attr[0].val.clusterDim.z = 1;
-  cfg.attrs = attr;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<EPI, BNT, CG>, p);
+  return launch_k(gemm_tc_kernel<EPI, BNT, CG>, dim3(grid), dim3(NTHREADS), SMEM_BYTES, s, CG, p);
 }
 
 template <int EPI, int BNT>
@@ -616,6 +602,7 @@ cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t 
 namespace {
 __global__ void shrink_reduce_kernel(const float* __restrict__ ws, int ksplit, int M, int RT, int r,
                                      bf16* T0, bf16* T1, bf16* T2, float scale) {
+  ptx::pdl_begin();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= M * RT) return;
   float s = 0.f;
@@ -665,9 +652,8 @@ cudaError_t shrink_run(const ShrinkPlan& sp, float scale, int num_sms, cudaStrea
   cudaError_t e = gemm_launch(sp.g, EPI_PARTIAL, num_sms, s);
   if (e != cudaSuccess) return e;
   const int n = sp.M * sp.RT;
-  shrink_reduce_kernel<<<(n + 255) / 256, 256, 0, s>>>(sp.ws, sp.g.ksplit, sp.M, sp.RT, sp.r,
-                                                       sp.T[0], sp.T[1], sp.T[2], scale);
-  return cudaGetLastError();
+  return launch_k(shrink_reduce_kernel, dim3((n + 255) / 256), dim3(256), 0, s, 1, sp.ws,
+                  sp.g.ksplit, sp.M, sp.RT, sp.r, sp.T[0], sp.T[1], sp.T[2], scale);
 }
 
 }  // namespace tidal

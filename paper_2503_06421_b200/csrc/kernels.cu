@@ -9,6 +9,8 @@
 #include <cstdint>
 
 #include "kernels.h"
+#include "launch.cuh"
+#include "ptx.cuh"
 
 namespace tidal {
 
@@ -37,7 +39,10 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 
 // ---------------- embedding gather ----------------
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const bf16* __restrict__ E,
-                             float* __restrict__ X, int d, int row0, int rows) {
+                             float* __restrict__ X, int d, int row0, int rows,
+                             unsigned long long* key_reset) {
+  ptx::pdl_begin();
+  if (key_reset && blockIdx.x == 0 && threadIdx.x == 0) *key_reset = 0ull;  // argmax of this forward
   const int s = blockIdx.x;
   const int t = tok[s] - row0;
   const bool mine = t >= 0 && t < rows;
@@ -64,6 +69,7 @@ __global__ void __launch_bounds__(NORM_THREADS) rmsnorm_kernel(const float* __re
                                                                bf16* __restrict__ Y, int d,
                                                                float eps) {
   __shared__ float red[32];
+  ptx::pdl_begin();
   const float4* x = reinterpret_cast<const float4*>(X + (size_t)blockIdx.x * d);
   const int n4 = d >> 2;
   // the row stays in registers: one HBM read of X (d <= 4 * 256 * NORM_VEC)
@@ -113,6 +119,7 @@ __global__ void __launch_bounds__(HEAD_THREADS) head_kernel(const float* __restr
   extern __shared__ float hs[];  // d floats
   __shared__ float red[32];
   __shared__ unsigned long long kred[HEAD_THREADS / 32];
+  ptx::pdl_begin();
   float ss = 0.f;
   for (int i = threadIdx.x; i < d; i += HEAD_THREADS) {
     const float v = xlast[i];
@@ -185,18 +192,16 @@ __global__ void nan_check_kernel(const float* x, int n, int* flag) {
 }  // namespace
 
 cudaError_t embed_launch(const int32_t* tok, const bf16* E, float* X, int S, int d, int row0,
-                         int rows, cudaStream_t s) {
+                         int rows, cudaStream_t s, unsigned long long* key_reset) {
   int th = d / 8;
   if (th > 1024) th = 1024;
   if (th < 32) th = 32;
-  embed_kernel<<<S, th, 0, s>>>(tok, E, X, d, row0, rows);
-  return cudaGetLastError();
+  return launch_k(embed_kernel, dim3(S), dim3(th), 0, s, 1, tok, E, X, d, row0, rows, key_reset);
 }
 
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d, float eps,
                            cudaStream_t s) {
-  rmsnorm_kernel<<<S, NORM_THREADS, 0, s>>>(X, g, Y, d, eps);
-  return cudaGetLastError();
+  return launch_k(rmsnorm_kernel, dim3(S), dim3(NORM_THREADS), 0, s, 1, X, g, Y, d, eps);
 }
 
 cudaError_t head_launch(const float* X_last, const bf16* g, const bf16* W, int V, int d, float eps,
@@ -211,8 +216,8 @@ cudaError_t head_launch(const float* X_last, const bf16* g, const bf16* W, int V
   int grid = num_sms * 4;
   const int need = (V + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32);
   if (grid > need) grid = need;
-  head_kernel<<<grid, HEAD_THREADS, smem, s>>>(X_last, g, W, V, d, eps, logits, key, vocab_offset);
-  return cudaGetLastError();
+  return launch_k(head_kernel, dim3(grid), dim3(HEAD_THREADS), smem, s, 1, X_last, g, W, V, d, eps,
+                  logits, key, vocab_offset);
 }
 
 cudaError_t poison_launch(void* p, size_t bytes, cudaStream_t s) {

@@ -107,8 +107,9 @@ cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t 
 // SIMT / legacy-MMA kernels (kernels.cu, attention.cu)
 // ------------------------------------------------------------------------
 // X[s, :] = fp32(E[tok[s] - row0, :]) for tokens in [row0, row0+rows), else 0 (vocab shard).
+// key_reset (nullable): zeroed by the kernel — the packed argmax of this forward.
 cudaError_t embed_launch(const int32_t* tok, const bf16* E, float* X, int S, int d, int row0,
-                         int rows, cudaStream_t s);
+                         int rows, cudaStream_t s, unsigned long long* key_reset = nullptr);
 // Y = bf16(g * x * rsqrt(mean(x^2) + eps)), one row per CTA.
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d, float eps,
                            cudaStream_t s);

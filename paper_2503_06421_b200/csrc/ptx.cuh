@@ -146,5 +146,14 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 
 __device__ __forceinline__ uint32_t elect_lane0() { return (threadIdx.x & 31) == 0; }
 
+// Programmatic dependent launch: wait until the previous kernel in the stream
+// has completed (no-op without the launch attribute), then let the next kernel
+// start its prologue on SMs this grid frees.  Every kernel of the forward calls
+// pdl_begin() before its first global-memory access.
+__device__ __forceinline__ void pdl_begin() {
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
 }  // namespace ptx
 }  // namespace tidal

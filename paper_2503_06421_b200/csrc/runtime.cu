@@ -384,7 +384,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_EMBED:
         {
           const int e0 = P0();
-          K(KC_EMBED, e0, 0, Sd * d * 6, embed_launch(ex.tok, Wp(tt.embed), ex.X, S, d, ex.rank * Vl, Vl, st),
+          K(KC_EMBED, e0, 0, Sd * d * 6, embed_launch(ex.tok, Wp(tt.embed), ex.X, S, d, ex.rank * Vl, Vl, st, ex.key),
             "embed");
         }
         break;
@@ -469,8 +469,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         break;
       case OP_FNORM:  // fused into the head kernel (fp32 last-row norm)
         break;
-      case OP_HEAD:
-        cuda_check(cudaMemsetAsync(ex.key, 0, 8, st), "memset key");
+      case OP_HEAD:  // the argmax key was zeroed by the embed kernel of this forward
         {
           const int e0 = P0();
           K(KC_HEAD, e0, 2.0 * Vl * d, 2.0 * Vl * d + 4.0 * Vl,
