@@ -242,18 +242,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
   if (warp == 0) {
     // ===================== TMA producer (both CTAs) =====================
     if (lane == 0) {
-      const uint64_t keep = ptx::policy_evict_last(), stream = ptx::policy_evict_first();
-      auto tma_h = [&](const CUtensorMap* m, uint32_t dst, uint32_t fb, int c0, int c1,
-                       uint64_t pol) {
-        if (CG == 2)
-          ptx::tma_load_2d_pair_hint(m, dst, fb, c0, c1, pol);
-        else
-          ptx::tma_load_2d_hint(m, dst, fb, c0, c1, pol);
-      };
-      // A = activations (re-read by every N tile): keep; everything else
-      // (weights, LoRA B) is read by one M row of tiles at a time: stream
       auto tma = [&](const CUtensorMap* m, uint32_t dst, uint32_t fb, int c0, int c1) {
-        tma_h(m, dst, fb, c0, c1, (m == &p.a || (m >= &p.ta[0] && m <= &p.ta[2])) ? keep : stream);
+        if (CG == 2)
+          ptx::tma_load_2d_pair(m, dst, fb, c0, c1);
+        else
+          ptx::tma_load_2d(m, dst, fb, c0, c1);
       };
       int stage = 0;
       uint32_t phase = 0;
