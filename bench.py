@@ -274,6 +274,19 @@ def main():
         step(T.DEBUG_SCRUB_L2 | T.DEBUG_PROFILE)
     prof_all = tpl.profile(reset=True)
     n_all = 1 if args.quick else 3
+    if not args.quick and not args.no_sweep:
+        # keep-alive with adapter hot-swap (Tidal-DK, §5.2): the streamed
+        # weights of the previous invocation stay; only the adapter streams
+        tpl.keep_alive()
+        sweep["keep_alive_hot_swap"] = max_over_ranks(
+            statistics.median(step(T.DEBUG_SCRUB_L2)["device_ms"] for _ in range(3)))
+        # loading-order ablation at rho = 0 (§7.4)
+        tpl.resize(T.template_opts(resident_bytes=0))
+        for name, order in (("rho0_order_reverse", T.ORDER_REVERSE),
+                            ("rho0_order_registration", T.ORDER_REGISTRATION)):
+            tpl.set_load_order(order)
+            sweep[name] = max_over_ranks(step(T.DEBUG_SCRUB_L2)["device_ms"])
+        tpl.set_load_order(T.ORDER_TRACED)
     dev_ms = [max_over_ranks(s["device_ms"]) for s in stats]
     e2e_ms = [max_over_ranks(s["e2e_ms"]) for s in stats]
     s0 = stats[0]

@@ -137,6 +137,19 @@ tidal_status tidal_template_create(tidal_model* m, const tidal_trace_rec* t,
  * PAPER.md line 576): re-plans the resident prefix from opts (resident_bytes
  * or eq1 fields; other fields ignored) and copies any newly resident bytes. */
 tidal_status tidal_template_resize(tidal_template* tpl, const tidal_template_opts* opts);
+/* Keep-alive of a dynamic function (§5.2 "Keep-alive of dynamic
+ * function", lines 579-587): after an invocation every streamed weight is
+ * already on the device, so the whole layout is marked resident (no copy) and
+ * later invocations stream only their dynamic adapter.  Fails with
+ * TIDAL_ERR_INVALID if the streaming arena does not hold valid weights (no
+ * successful invoke since a fault-injection run). */
+tidal_status tidal_template_keep_alive(tidal_template* tpl);
+/* Loading-order ablation (§7.4): copy the transfer
+ * groups in traced access order (default), reverse order, or registration
+ * (initialisation) order.  Barriers stay correct in every order: each op waits
+ * on the needed group that is copied last. */
+enum { TIDAL_ORDER_TRACED = 0, TIDAL_ORDER_REVERSE = 1, TIDAL_ORDER_REGISTRATION = 2 };
+tidal_status tidal_set_load_order(tidal_template* tpl, int order);
 void tidal_template_destroy(tidal_template* tpl);
 
 /* Canonical adapter layout for (rank, target_mask): tensors in adapter access

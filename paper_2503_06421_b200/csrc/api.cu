@@ -2,6 +2,7 @@
 // pool + device template/arena), adaptive fork and the overlapped invoke.
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <atomic>
 #include <chrono>
 #include <cmath>
@@ -119,6 +120,8 @@ struct tidal_template {
   uint8_t* arena = nullptr;  // adapter arena
   uint64_t arena_cap = 0;
   int debug = 0, debug_arg = -1;
+  int load_order = 0;         // TIDAL_ORDER_*
+  bool suffix_valid = false;  // the streaming arena holds the streamed weights
   void* scrub = nullptr;
   unsigned long long* d_sum = nullptr;
   tidal_comm* comm = nullptr;
@@ -416,6 +419,7 @@ tidal_status tidal_template_create(tidal_model* m, const tidal_trace_rec* t,
                             L - tp->plan.resident_end, cudaMemcpyHostToDevice),
                  "H2D warm");
     warm_kernels(tp);
+    tp->suffix_valid = true;  // the warm-up copied the whole layout
   } catch (...) {
     tidal_template_destroy(tp);
     throw;
@@ -446,6 +450,26 @@ tidal_status tidal_template_resize(tidal_template* tp, const tidal_template_opts
   tp->choice = c;
   tp->plan = std::move(p);
   ++tp->gen;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_template_keep_alive(tidal_template* tp) {
+  TIDAL_TRY
+  require(tp != nullptr && !tp->dry, "keep-alive needs a device template");
+  require(tp->suffix_valid, "streaming arena does not hold valid weights");
+  TemplateChoice c = tp->choice;
+  c.eq1 = false;
+  c.resident_bytes = UINT64_MAX;
+  tp->plan = make_plan(tp->tt, tp->tr, c);  // every base weight resident; no copy needed
+  tp->choice = c;
+  ++tp->gen;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_set_load_order(tidal_template* tp, int order) {
+  TIDAL_TRY
+  require(tp != nullptr && order >= 0 && order <= 2, "bad load order");
+  tp->load_order = order;
   TIDAL_CATCH
 }
 
@@ -604,6 +628,7 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
   const auto t0 = (tp->debug & (TIDAL_DEBUG_POISON | TIDAL_DEBUG_SCRUB_L2))
                       ? std::chrono::steady_clock::now()
                       : t_entry;
+  tp->suffix_valid = false;  // set again once every streamed group has landed
   ex.launches = 0;
   ex.profile = (tp->debug & (TIDAL_DEBUG_PROFILE | TIDAL_DEBUG_PROFILE_GEMM)) != 0;
   ex.profile_all = (tp->debug & TIDAL_DEBUG_PROFILE) != 0;
@@ -614,11 +639,27 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
   // ---- copy stream: groups in traced access order, one event each ----
   cuda_check(cudaEventRecord(tp->e_h2d0, ex.copy), "event");
   const int skip = (tp->debug & TIDAL_DEBUG_SKIP_BARRIER) ? tp->debug_arg : -1;
-  for (size_t g = 0; g < P.groups.size(); ++g) {
+  // copy order (traced by default; ablations reverse / registration order)
+  std::vector<int> order(P.groups.size());
+  for (size_t g = 0; g < order.size(); ++g) order[g] = (int)g;
+  if (tp->load_order == TIDAL_ORDER_REVERSE) {
+    std::reverse(order.begin(), order.end());
+  } else if (tp->load_order == TIDAL_ORDER_REGISTRATION) {
+    auto first_id = [&](int g) {
+      int m = INT32_MAX;
+      for (int id : P.groups[g].members) m = std::min(m, id);
+      return m;
+    };
+    std::stable_sort(order.begin(), order.end(),
+                     [&](int x, int y) { return first_id(x) < first_id(y); });
+  }
+  std::vector<int> copy_pos(P.groups.size());
+  for (size_t i = 0; i < order.size(); ++i) copy_pos[order[i]] = (int)i;
+  for (int g : order) {
     const Group& G = P.groups[g];
     const uint8_t* src = G.adapter ? a->host + G.offset : tp->pool + G.offset;
     uint8_t* dst = G.adapter ? tp->arena + G.offset : tp->dev + G.offset;
-    if ((int)g == skip) {
+    if (g == skip) {
       sleep_kernel<<<1, 1, 0, ex.copy>>>(20000);  // fault injection: late group
       cuda_check(cudaGetLastError(), "sleep");
     }
@@ -636,6 +677,7 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
   ra.ops = &P.ops;
   ra.barriers = &P.barriers;
   ra.events = &tp->ev;
+  ra.copy_pos = &copy_pos;
   ra.skip_group = skip;
   ra.S = n_tokens;
   ra.lora_scale = a ? a->scale : 1.f;
@@ -650,6 +692,7 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
                "D2H logits");
   cuda_check(cudaEventRecord(tp->e_end, ex.compute), "event");
   cuda_check(cudaEventSynchronize(tp->e_end), "invoke");
+  tp->suffix_valid = skip < 0;
   if (ex.profile) ex.prof_collect();
   const unsigned long long key = *ex.h_key;
   const uint32_t hi = (uint32_t)(key >> 32);

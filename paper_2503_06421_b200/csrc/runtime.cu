@@ -370,12 +370,20 @@ void run_forward(Exec& ex, const RunArgs& a) {
     const Op& op = ops[k];
     if (a.rec) a.rec->op((int)k, op.reads, tt.n_base);
     if (a.barriers && !(*a.barriers)[k].empty()) {
-      int g = -1;
-      for (int x : (*a.barriers)[k])
-        if (x != a.skip_group) g = std::max(g, x);
-      if (g > waited) {
+      // the copy stream is FIFO: waiting on the needed group copied last covers
+      // all of them (waited = copy position already covered)
+      int g = -1, gp = -1;
+      for (int x : (*a.barriers)[k]) {
+        if (x == a.skip_group) continue;
+        const int pos = a.copy_pos ? (*a.copy_pos)[x] : x;
+        if (pos > gp) {
+          gp = pos;
+          g = x;
+        }
+      }
+      if (gp > waited) {
         cuda_check(cudaStreamWaitEvent(st, (*a.events)[g], 0), "cudaStreamWaitEvent");
-        waited = g;
+        waited = gp;
       }
     }
     const int l = op.layer;

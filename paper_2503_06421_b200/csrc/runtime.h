@@ -110,6 +110,7 @@ struct RunArgs {
   const std::vector<Op>* ops = nullptr;
   const std::vector<std::vector<int>>* barriers = nullptr;  // nullable
   const std::vector<cudaEvent_t>* events = nullptr;         // per group
+  const std::vector<int>* copy_pos = nullptr;               // position of each group in the copy stream
   int skip_group = -1;                                       // fault injection
   int S = 0;
   float lora_scale = 1.f;

@@ -21,6 +21,7 @@ ERR_NAMES = {0: "OK", 1: "INVALID", 2: "OOM", 3: "CUDA", 4: "NCCL", 5: "STRUCTUR
 GROUPS_PER_LAYER, GROUPS_MAX_TRANSFERS, GROUPS_PER_TENSOR = 0, 1, 2
 DEBUG_POISON, DEBUG_SKIP_BARRIER, DEBUG_SCRUB_L2, DEBUG_SERIAL, DEBUG_PROFILE = 1, 2, 4, 8, 16
 DEBUG_PROFILE_GEMM = 32
+ORDER_TRACED, ORDER_REVERSE, ORDER_REGISTRATION = 0, 1, 2
 U64_MAX = (1 << 64) - 1
 
 
@@ -88,6 +89,8 @@ SIGNATURES = [
     ("tidal_trace_dump", C.c_int, [VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("tidal_template_create", C.c_int, [VP, VP, C.POINTER(TemplateOpts), C.POINTER(VP)]),
     ("tidal_template_resize", C.c_int, [VP, C.POINTER(TemplateOpts)]),
+    ("tidal_template_keep_alive", C.c_int, [VP]),
+    ("tidal_set_load_order", C.c_int, [VP, C.c_int]),
     ("tidal_template_destroy", None, [VP]),
     ("tidal_adapter_layout", C.c_int, [VP, C.c_int, C.c_uint32, C.POINTER(Slot), C.c_int,
                                        C.POINTER(C.c_int), C.POINTER(C.c_uint64)]),
@@ -238,6 +241,12 @@ class Template:
 
     def resize(self, opts: TemplateOpts) -> None:
         _check(lib().tidal_template_resize(self.h, C.byref(opts)))
+
+    def keep_alive(self) -> None:
+        _check(lib().tidal_template_keep_alive(self.h))
+
+    def set_load_order(self, order: int) -> None:
+        _check(lib().tidal_set_load_order(self.h, order))
 
     def plan_dump(self, adapter: Optional["Adapter"] = None) -> str:
         return _dump(lib().tidal_plan_dump, self.h, adapter.h if adapter else None)

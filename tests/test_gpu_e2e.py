@@ -196,3 +196,33 @@ def test_serial_mode_same_result(T, tiny):
     tiny.tpl.set_debug(0)
     assert t0 == t1 and np.array_equal(l0, l1)
     assert st["compute_first_ms"] >= st["h2d_last_ms"] - 1e-3
+
+
+def test_keep_alive_hot_swap(T):
+    """Tidal-DK (§5.2 keep-alive): after one invocation the streamed
+    weights stay; a new adapter is then the only thing streamed."""
+    cfg = synth.config("tiny")
+    rig = Rig(T, cfg, seed=5, budget=0.0)
+    rig.tpl.set_debug(T.DEBUG_POISON)
+    tok = synth.prompt(cfg, 20, 5)
+    a1 = rig.adapter(8, 1)
+    check(rig.tpl.invoke(tok, a1), F.forward(cfg, rig.w, tok, F.synth_adapter(cfg, 8, 1), 0x7F, 1.0))
+    rig.tpl.keep_alive()
+    a2 = rig.adapter(16, 2)
+    res = rig.tpl.invoke(tok, a2)
+    check(res, F.forward(cfg, rig.w, tok, F.synth_adapter(cfg, 16, 2), 0x7F, 1.0))
+    assert res[2]["bytes_streamed"] == 0 and res[2]["bytes_adapter"] > 0
+    assert all(" adapter " in l for l in rig.tpl.plan_dump(a2).splitlines() if l.startswith("GROUP"))
+
+
+@pytest.mark.parametrize("order", [0, 1, 2])
+def test_load_order_ablation_correct(T, order):
+    """Traced / reverse / registration copy orders (§7.4) all give the
+    same result: barriers wait on the needed group copied last."""
+    cfg = synth.config("tiny")
+    rig = Rig(T, cfg, seed=6, budget=0.2, policy=2)
+    rig.tpl.set_debug(T.DEBUG_POISON)
+    rig.tpl.set_load_order(order)
+    tok = synth.prompt(cfg, 24, 6)
+    a = rig.adapter(8, 3)
+    check(rig.tpl.invoke(tok, a), F.forward(cfg, rig.w, tok, F.synth_adapter(cfg, 8, 3), 0x7F, 1.0))
