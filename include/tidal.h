@@ -209,6 +209,15 @@ void tidal_host_free(void* p);
 tidal_status tidal_comm_unique_id(void* out128);
 tidal_status tidal_comm_create(int world, int rank, const void* unique_id128, int device,
                                tidal_comm** out);
+/* In-process ranks (one host thread per rank, SURVEY.md §8(e) collectives C1-C4
+ * over device pointers): every rank of one process calls this with the same
+ * `group` string and world; ranks may share a device (TP=N on one GPU, used by
+ * the tests) or sit on peer-accessible devices.  Collectives rendezvous on the
+ * host (each rank's invoke must run concurrently on its own thread; a peer
+ * missing for 120 s gives TIDAL_ERR_NCCL) and sum in rank order, so all ranks
+ * hold bit-identical results.  world must be <= 8. */
+tidal_status tidal_comm_create_local(int world, int rank, const char* group, int device,
+                                     tidal_comm** out);
 void tidal_comm_destroy(tidal_comm* c);
 
 /* ---- invariants and fault injection (test support) ---- */

@@ -23,8 +23,8 @@ using namespace tidal;
 
 namespace tidal {
 bool nccl_unique_id(void* out128);
-void* nccl_comm_create(int world, int rank, const void* id128, int device);
-void nccl_comm_destroy(void* c);
+Comm* nccl_comm_create(int world, int rank, const void* id128, int device);
+Comm* local_comm_create(int world, int rank, const std::string& key, int device);
 }  // namespace tidal
 
 namespace {
@@ -86,7 +86,7 @@ struct tidal_trace_rec {
 };
 
 struct tidal_comm {
-  void* nccl = nullptr;
+  Comm* impl = nullptr;  // NCCL (one process per GPU) or in-process ranks
   int world = 1, rank = 0, device = 0;
 };
 
@@ -349,7 +349,7 @@ static void warm_kernels(tidal_template* tp) {
   a.S = S;
   a.akey = nullptr;
   a.gen = tp->gen;
-  a.nccl = tp->comm ? tp->comm->nccl : nullptr;
+  a.comm = tp->comm ? tp->comm->impl : nullptr;
   run_forward(ex, a);
   const bf16* A[1] = {ex.Xn};
   bf16* T[1] = {ex.T[0]};
@@ -683,7 +683,7 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
   ra.lora_scale = a ? a->scale : 1.f;
   ra.akey = a ? (const void*)tp->arena : nullptr;
   ra.gen = tp->gen;
-  ra.nccl = tp->comm ? tp->comm->nccl : nullptr;
+  ra.comm = tp->comm ? tp->comm->impl : nullptr;
   run_forward(ex, ra);
   cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_h2d1, 0), "wait copies");
   cuda_check(cudaMemcpyAsync(ex.h_key, ex.key, 8, cudaMemcpyDeviceToHost, ex.compute), "D2H key");
@@ -752,7 +752,27 @@ tidal_status tidal_comm_create(int world, int rank, const void* id, int device, 
   c->device = device;
   if (world > 1) {
     try {
-      c->nccl = nccl_comm_create(world, rank, id, device);
+      c->impl = nccl_comm_create(world, rank, id, device);
+    } catch (...) {
+      delete c;
+      throw;
+    }
+  }
+  *out = c;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_comm_create_local(int world, int rank, const char* group, int device,
+                                     tidal_comm** out) {
+  TIDAL_TRY
+  require(out && group && world >= 1 && rank >= 0 && rank < world, "bad argument");
+  auto* c = new tidal_comm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  if (world > 1) {
+    try {
+      c->impl = local_comm_create(world, rank, group, device);
     } catch (...) {
       delete c;
       throw;
@@ -764,7 +784,7 @@ tidal_status tidal_comm_create(int world, int rank, const void* id, int device, 
 
 void tidal_comm_destroy(tidal_comm* c) {
   if (!c) return;
-  nccl_comm_destroy(c->nccl);
+  delete c->impl;
   delete c;
 }
 

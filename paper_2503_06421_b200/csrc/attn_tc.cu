@@ -1,15 +1,19 @@
 // attn_tc.cu — causal GQA prefill attention on 5th-gen tensor cores (hd = 128).
 //   O_h = softmax(Q_h K_g^T / sqrt(hd) + causal) V_g,   g = h / (H / KV)
 // CTA = 128 queries of one head; warp-specialised like the GEMM:
-//   warp 0      TMA: Q once, then K / V^T tiles of 128 keys (2-stage ring)
+//   warp 0      TMA: Q once, then K / V^T tiles of 128 keys (separate rings:
+//               K_j is released as soon as S_j is computed)
 //   warp 1      tcgen05.mma: S_j = Q K_j^T into TMEM (double-buffered, so
 //               S_{j+1} runs while softmax works on S_j), then O += P_j V_j
-//   warps 2..5  softmax, one query row per thread (TMEM lane = row): row max,
-//               P = exp2(S*scale - m) rounded to bf16 into a SWIZZLE_128B smem
-//               tile (the A operand of the PV MMA), running row sum in fp32.
-//               O lives in TMEM for the whole CTA; it is rescaled only when a
-//               row max grows by more than 2^8 (exact: O and l share the same
-//               stale max, P <= 256 cannot overflow), then O / l -> bf16.
+//   warps 2..9  softmax in two column halves: warps 2..5 own keys 0..63 and
+//               warps 6..9 keys 64..127 of the same 128 query rows (TMEM lane
+//               = row; both halves share a lane quarter), exchanging row
+//               maxima through shared memory; P = exp2(S*scale - m) rounded
+//               to bf16 into a SWIZZLE_128B smem tile (each half writes one
+//               K-block of the PV MMA's A operand); fp32 running row sums.
+//               O lives in TMEM for the whole CTA; it is rescaled (each half
+//               its 64 columns) only when a row max grows by more than 2^8
+//               (exact: O and l share the same stale max, P <= 256).
 // V is consumed as V^T [hd][S] (written transposed by the QKV GEMM epilogue),
 // so both MMAs read K-major operands.
 #include <cuda.h>
@@ -28,21 +32,24 @@ namespace {
 constexpr int HD = 128, BQ = 128, BKV = 128;
 constexpr int TILE = 128 * 128 * 2;  // 32 KB: any 128 x 128 bf16 tile (two 64-wide K-blocks)
 constexpr int HALF = TILE / 2;
-// K and V have separate rings: K_j is released as soon as S_j is computed, so
-// the next K tiles stream in while softmax runs; V_j lives until PV_j.
-constexpr int KST = 2, VST = 3;
+constexpr int KST = 2, VST = 2;
 constexpr int OFF_Q = 0, OFF_K = OFF_Q + TILE, OFF_V = OFF_K + KST * TILE,
               OFF_P = OFF_V + VST * TILE;
-constexpr int OFF_BAR = OFF_P + TILE;
+constexpr int OFF_RED = OFF_P + TILE;                // [2 slots][2 halves][128] row maxima
+constexpr int OFF_BAR = OFF_RED + 2 * 2 * BQ * 4;
 constexpr int N_BARS = 3 + 2 * KST + 2 * VST + 2;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM = OFF_TMEM + 16 + 1024;
-constexpr int NTH = 192;
+constexpr int NSOFT = 256;           // softmax threads
+constexpr int NTH = 64 + NSOFT;
 constexpr uint32_t COL_S0 = 0, COL_O = 256;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
+}
+__device__ __forceinline__ void softmax_bar() {  // the 8 softmax warps only
+  asm volatile("bar.sync 1, %0;" ::"n"(NSOFT) : "memory");
 }
 
 __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
@@ -71,7 +78,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     ptx::prefetch_tmap(&p.q);
     ptx::prefetch_tmap(&p.vt);
     ptx::mbar_init(q_full, 1);
-    ptx::mbar_init(p_full, 128);
+    ptx::mbar_init(p_full, NSOFT);
     ptx::mbar_init(pv_done, 1);
     for (int s = 0; s < KST; ++s) {
       ptx::mbar_init(k_full(s), 1);
@@ -97,7 +104,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       ptx::mbar_expect_tx(q_full, TILE);
       ptx::tma_load_2d(&p.q, sb + OFF_Q, q_full, qc, q0);
       ptx::tma_load_2d(&p.q, sb + OFF_Q + HALF, q_full, qc + 64, q0);
-      // in-order issue K_0 V_0 K_1 V_1 ...: V_j's slot frees (PV_{j-3}) before
+      // in-order issue K_0 V_0 K_1 V_1 ...: V_j's slot frees (PV_{j-2}) before
       // K_{j+1}'s (S_{j-1}), so the single producer never waits needlessly
       for (int j = 0; j < nkv; ++j) {
         const int s = j % KST, t = j % VST;
@@ -153,65 +160,73 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     }
     __syncwarp();
   } else {
-    // ===================== softmax warps =====================
-    const int q = warp & 3;
+    // ===================== softmax: two column halves =====================
+    const int half = (warp - 2) >> 2;  // 0: keys 0..63, 1: keys 64..127 of each tile
+    const int q = warp & 3;            // TMEM lane quarter (shared by both halves)
     const int row = q * 32 + lane;
     const int qi = q0 + row;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    uint8_t* Ps = smem + OFF_P;
+    float* red = reinterpret_cast<float*>(smem + OFF_RED);  // [slot][half][row]
+    uint8_t* Ps = smem + OFF_P + half * HALF;               // this half's K-block of P
+    const uint32_t o_col = tmem + lane_base + COL_O + half * 64;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
       ptx::mbar_wait(s_full(j & 1), (j >> 1) & 1);
       ptx::tc_fence_after();
-      float v[128];
-#pragma unroll
-      for (int c = 0; c < 4; c += 2) {
+      float v[64];
+      {
         uint32_t r0[32], r1[32];
-        ptx::tmem_ld32(tmem + lane_base + COL_S0 + (j & 1) * 128 + c * 32, r0);
-        ptx::tmem_ld32(tmem + lane_base + COL_S0 + (j & 1) * 128 + c * 32 + 32, r1);
+        const uint32_t sc = tmem + lane_base + COL_S0 + (j & 1) * 128 + half * 64;
+        ptx::tmem_ld32(sc, r0);
+        ptx::tmem_ld32(sc + 32, r1);
         ptx::tmem_ld_wait();
 #pragma unroll
         for (int i = 0; i < 32; ++i) {
-          v[c * 32 + i] = __uint_as_float(r0[i]);  // raw scores
-          v[c * 32 + 32 + i] = __uint_as_float(r1[i]);
+          v[i] = __uint_as_float(r0[i]);  // raw scores
+          v[32 + i] = __uint_as_float(r1[i]);
         }
       }
-      if (j == qt) {  // diagonal tile: causal mask
+      const int key0 = j * BKV + half * 64;
+      if (key0 + 63 > q0) {  // reaches the diagonal: causal mask
 #pragma unroll
-        for (int i = 0; i < 128; ++i)
-          if (j * BKV + i > qi) v[i] = -INFINITY;
+        for (int i = 0; i < 64; ++i)
+          if (key0 + i > qi) v[i] = -INFINITY;
       }
       float mr[8];  // 8 independent max chains
 #pragma unroll
       for (int k = 0; k < 8; ++k) mr[k] = v[k];
 #pragma unroll
-      for (int i = 8; i < 128; ++i) mr[i & 7] = fmaxf(mr[i & 7], v[i]);
-      const float mraw = fmaxf(fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3])),
-                               fmaxf(fmaxf(mr[4], mr[5]), fmaxf(mr[6], mr[7])));
+      for (int i = 8; i < 64; ++i) mr[i & 7] = fmaxf(mr[i & 7], v[i]);
+      float mraw = fmaxf(fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3])),
+                         fmaxf(fmaxf(mr[4], mr[5]), fmaxf(mr[6], mr[7])));
+      // exchange the half-row maxima (double-buffered slot: no WAR hazard)
+      float* slot = red + (j & 1) * 2 * BQ;
+      slot[half * BQ + row] = mraw;
+      softmax_bar();
+      mraw = fmaxf(mraw, slot[(half ^ 1) * BQ + row]);
       const float mx = fmaxf(m_used, mraw * p.scale_log2);  // scale > 0: max commutes
-      const bool need = mx > m_used + 8.f;
-      if (j > 0) ptx::mbar_wait(pv_done, (j - 1) & 1);  // P buffer free, O settled
+      const bool need = mx > m_used + 8.f;                  // identical in both halves
+      if (j > 0) ptx::mbar_wait(pv_done, (j - 1) & 1);    // P free, O settled
       if (j > 0 && __any_sync(0xffffffffu, need)) {
         ptx::tc_fence_after();
         const float corr = need ? exp2f(m_used - mx) : 1.f;
 #pragma unroll 1
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < 2; ++c) {
           uint32_t r[32];
-          const uint32_t ta = tmem + lane_base + COL_O + c * 32;
-          ptx::tmem_ld32(ta, r);
+          ptx::tmem_ld32(o_col + c * 32, r);
           ptx::tmem_ld_wait();
 #pragma unroll
           for (int i = 0; i < 32; ++i) r[i] = __float_as_uint(__uint_as_float(r[i]) * corr);
-          ptx::tmem_st32(ta, r);
+          ptx::tmem_st32(o_col + c * 32, r);
         }
         ptx::tmem_st_wait();
         l *= corr;
       }
       if (need) m_used = mx;
-      // P = exp2(v - m) -> bf16, SWIZZLE_128B K-major tile (two 64-key blocks)
+      // P = exp2(s*scale - m) -> bf16 into this half's SWIZZLE_128B K-block
       float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent sum chains
 #pragma unroll
-      for (int c = 0; c < 16; ++c) {
+      for (int c = 0; c < 8; ++c) {
         float e[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
@@ -223,23 +238,26 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         w.y = pack_bf16x2(e[2], e[3]);
         w.z = pack_bf16x2(e[4], e[5]);
         w.w = pack_bf16x2(e[6], e[7]);
-        const int blk = c >> 3, ch = c & 7;
-        *reinterpret_cast<uint4*>(Ps + blk * HALF + row * 128 + ((ch ^ (row & 7)) << 4)) = w;
+        *reinterpret_cast<uint4*>(Ps + row * 128 + ((c ^ (row & 7)) << 4)) = w;
       }
       l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
       ptx::fence_proxy_async_smem();
       ptx::tc_fence_before();
       ptx::mbar_arrive(p_full);
     }
-    // epilogue: O / l -> bf16
+    // epilogue: combine the half-row sums, O / l -> bf16 (each half its 64 columns)
+    float* lsum = red;  // reuse slot 0 after a barrier (all maxima consumed)
+    softmax_bar();
+    lsum[half * BQ + row] = l;
+    softmax_bar();
+    const float inv = 1.f / (l + lsum[(half ^ 1) * BQ + row]);
     ptx::mbar_wait(pv_done, (nkv - 1) & 1);
     ptx::tc_fence_after();
-    const float inv = 1.f / l;
-    bf16* out = p.out + (size_t)qi * p.ldo + h * HD;
+    bf16* out = p.out + (size_t)qi * p.ldo + h * HD + half * 64;
 #pragma unroll 1
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       uint32_t r[32];
-      ptx::tmem_ld32(tmem + lane_base + COL_O + c * 32, r);
+      ptx::tmem_ld32(o_col + c * 32, r);
       ptx::tmem_ld_wait();
       if (qi < p.S) {
 #pragma unroll
@@ -268,7 +286,7 @@ bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, b
                     int H, int KV) {
   const int ld = (H + 2 * KV) * HD;
   if (!make_tmap(&p->q, qkv, S, ld, (uint64_t)ld * 2, 128, 64)) return false;
-  p->k = p->q;  // K tiles are 128 keys here: same box as Q
+  p->k = p->q;  // K tiles are 128 keys: same box as Q
   if (!make_tmap(&p->vt, vt, (uint64_t)KV * HD, S, (uint64_t)vt_ld * 2, 128, 64)) return false;
   p->S = S;
   p->H = H;

@@ -1,0 +1,314 @@
+// comm.cu — tensor-parallel exchange steps: allreduce of the
+// row-parallel partial sums (C1/C2) and of the vocab-parallel embedding (C3),
+// max-reduce of the packed argmax key and allgather of logit slices (C4).
+//
+// Two implementations of the same three collectives behind `Comm`:
+//   NcclComm   one process per GPU (the deployment path; bench.py under
+//              torchrun).  NCCL is resolved at run time with dlopen (the
+//              torch-bundled libnccl.so.2 is already mapped in a torch
+//              process), so the library loads on boxes without it.
+//   LocalComm  the ranks of one process (one thread per rank), over device
+//              pointers: each rank publishes its buffer, every rank reduces
+//              all ranks' buffers in rank order into private scratch, and a
+//              second rendezvous keeps a buffer alive until every peer read
+//              it.  Ranks may share a GPU, so TP=N runs (and is tested) on a
+//              single device; across GPUs it needs peer access, enabled at
+//              create.  Rendezvous are host-side (the collective's enqueue
+//              blocks until all ranks enqueued theirs); ordering on the
+//              device is by cross-stream events.  Sums are left folds in rank
+//              order, so every rank holds bit-identical results (like NCCL).
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+
+#include <chrono>
+#include <condition_variable>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+
+#include "runtime.h"
+
+namespace tidal {
+
+namespace {
+typedef struct ncclComm* ncclComm_t;
+typedef struct {
+  char internal[128];
+} ncclUniqueId;
+enum { ncclSuccess = 0 };
+enum { ncclUint64 = 5, ncclFloat32 = 7 };
+enum { ncclSum = 0, ncclMax = 2 };
+
+struct NcclApi {
+  int (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  int (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*AllGather)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+  bool ok = false;
+};
+NcclApi g_nccl;
+std::once_flag g_nccl_once;
+
+const NcclApi& nccl() {
+  std::call_once(g_nccl_once, [] {
+    const char* names[] = {"libnccl.so.2", "libnccl.so"};
+    void* h = nullptr;
+    for (const char* n : names)
+      if ((h = dlopen(n, RTLD_NOW | RTLD_GLOBAL))) break;
+    if (!h) return;
+    g_nccl.GetUniqueId = (int (*)(ncclUniqueId*))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (int (*)(ncclComm_t*, int, ncclUniqueId, int))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllReduce = (int (*)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t))dlsym(
+        h, "ncclAllReduce");
+    g_nccl.AllGather =
+        (int (*)(const void*, void*, size_t, int, ncclComm_t, cudaStream_t))dlsym(h, "ncclAllGather");
+    g_nccl.CommDestroy = (int (*)(ncclComm_t))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (const char* (*)(int))dlsym(h, "ncclGetErrorString");
+    g_nccl.ok = g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce && g_nccl.AllGather &&
+                g_nccl.CommDestroy;
+  });
+  return g_nccl;
+}
+
+void nccl_check(int r, const char* what) {
+  if (r != ncclSuccess) {
+    const char* s = g_nccl.GetErrorString ? g_nccl.GetErrorString(r) : "?";
+    fail(4, std::string(what) + ": " + s);
+  }
+}
+
+struct NcclComm final : Comm {
+  ncclComm_t c = nullptr;
+  ~NcclComm() override {
+    if (c && g_nccl.ok) g_nccl.CommDestroy(c);
+  }
+  void allreduce_f32(float* buf, size_t n, cudaStream_t s) override {
+    nccl_check(g_nccl.AllReduce(buf, buf, n, ncclFloat32, ncclSum, c, s), "ncclAllReduce");
+  }
+  void max_u64(unsigned long long* key, cudaStream_t s) override {
+    nccl_check(g_nccl.AllReduce(key, key, 1, ncclUint64, ncclMax, c, s), "ncclAllReduce(max)");
+  }
+  void allgather_f32(float* buf, size_t n, cudaStream_t s) override {
+    nccl_check(g_nccl.AllGather(buf + (size_t)rank * n, buf, n, ncclFloat32, c, s), "ncclAllGather");
+  }
+};
+
+// ---------------- in-process ranks ----------------
+constexpr int kMaxLocal = 8;
+struct SrcPtrs {
+  const float* p[kMaxLocal];
+  int n;
+};
+
+__global__ void sum_ranks_kernel(SrcPtrs src, float* __restrict__ out, size_t n4) {
+  // out = ((src0 + src1) + src2) + ...   (rank order: identical on every rank)
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float4 acc = reinterpret_cast<const float4*>(src.p[0])[i];
+    for (int k = 1; k < src.n; ++k) {
+      const float4 v = reinterpret_cast<const float4*>(src.p[k])[i];
+      acc.x += v.x;
+      acc.y += v.y;
+      acc.z += v.z;
+      acc.w += v.w;
+    }
+    reinterpret_cast<float4*>(out)[i] = acc;
+  }
+}
+
+__global__ void max_ranks_kernel(SrcPtrs src, unsigned long long* out) {
+  unsigned long long m = 0;
+  for (int k = 0; k < src.n; ++k) {
+    const unsigned long long v = *reinterpret_cast<const unsigned long long*>(src.p[k]);
+    m = v > m ? v : m;
+  }
+  *out = m;
+}
+
+struct LocalGroup {
+  int world;
+  std::mutex m;
+  std::condition_variable cv;
+  int arrived = 0;
+  uint64_t phase = 0;
+  void* ptr[kMaxLocal] = {};
+  cudaEvent_t ev_a[kMaxLocal] = {}, ev_b[kMaxLocal] = {};
+  int joined = 0;
+
+  void rendezvous() {
+    std::unique_lock<std::mutex> lk(m);
+    const uint64_t ph = phase;
+    if (++arrived == world) {
+      arrived = 0;
+      ++phase;
+      cv.notify_all();
+    } else if (!cv.wait_for(lk, std::chrono::seconds(120), [&] { return phase != ph; })) {
+      fail(4, "local communicator: a peer rank never reached the collective (120 s)");
+    }
+  }
+};
+
+std::mutex g_groups_mu;
+std::map<std::string, std::weak_ptr<LocalGroup>> g_groups;
+
+struct LocalComm final : Comm {
+  std::shared_ptr<LocalGroup> g;
+  float* scratch = nullptr;
+  size_t scratch_n = 0;
+  unsigned long long* kscratch = nullptr;
+
+  ~LocalComm() override {
+    if (scratch) cudaFree(scratch);
+    if (kscratch) cudaFree(kscratch);
+    if (g) {
+      cudaEventDestroy(g->ev_a[rank]);
+      cudaEventDestroy(g->ev_b[rank]);
+    }
+  }
+  // Phase 1: publish `p`, order this stream after every peer's producer.
+  void publish(void* p, cudaStream_t s) {
+    g->ptr[rank] = p;
+    cuda_check(cudaEventRecord(g->ev_a[rank], s), "cudaEventRecord");
+    g->rendezvous();
+    for (int k = 0; k < world; ++k)
+      if (k != rank) cuda_check(cudaStreamWaitEvent(s, g->ev_a[k], 0), "cudaStreamWaitEvent");
+  }
+  // Phase 2: after this rank's reads of peer buffers, wait until every peer's
+  // reads of ours are done before anything later on `s` may overwrite it.
+  void retire(cudaStream_t s) {
+    cuda_check(cudaEventRecord(g->ev_b[rank], s), "cudaEventRecord");
+    g->rendezvous();
+    for (int k = 0; k < world; ++k)
+      if (k != rank) cuda_check(cudaStreamWaitEvent(s, g->ev_b[k], 0), "cudaStreamWaitEvent");
+  }
+  SrcPtrs srcs() const {
+    SrcPtrs sp;
+    sp.n = world;
+    for (int k = 0; k < world; ++k) sp.p[k] = static_cast<const float*>(g->ptr[k]);
+    return sp;
+  }
+  void allreduce_f32(float* buf, size_t n, cudaStream_t s) override {
+    if (n % 4) fail(1, "local allreduce: length must be a multiple of 4");
+    if (n > scratch_n) {
+      if (scratch) cudaFree(scratch);
+      scratch = nullptr;
+      cuda_check(cudaMalloc(&scratch, n * 4), "cudaMalloc(comm scratch)");
+      scratch_n = n;
+    }
+    publish(buf, s);
+    const SrcPtrs sp = srcs();
+    sum_ranks_kernel<<<4 * 148, 256, 0, s>>>(sp, scratch, n / 4);  // plain launch: no PDL overlap
+    cuda_check(cudaGetLastError(), "sum_ranks");
+    retire(s);
+    cuda_check(cudaMemcpyAsync(buf, scratch, n * 4, cudaMemcpyDeviceToDevice, s), "D2D");
+  }
+  void max_u64(unsigned long long* key, cudaStream_t s) override {
+    publish(key, s);
+    max_ranks_kernel<<<1, 1, 0, s>>>(srcs(), kscratch);
+    cuda_check(cudaGetLastError(), "max_ranks");
+    retire(s);
+    cuda_check(cudaMemcpyAsync(key, kscratch, 8, cudaMemcpyDeviceToDevice, s), "D2D");
+  }
+  void allgather_f32(float* buf, size_t n, cudaStream_t s) override {
+    publish(buf, s);
+    for (int k = 0; k < world; ++k)
+      if (k != rank)
+        cuda_check(cudaMemcpyAsync(buf + (size_t)k * n, static_cast<const float*>(g->ptr[k]) + (size_t)k * n,
+                                   n * 4, cudaMemcpyDeviceToDevice, s),
+                   "allgather D2D");
+    retire(s);
+  }
+};
+}  // namespace
+
+bool nccl_unique_id(void* out128) {
+  const NcclApi& n = nccl();
+  if (!n.ok) fail(4, "libnccl.so.2 not found (tensor parallelism needs NCCL)");
+  ncclUniqueId id;
+  nccl_check(n.GetUniqueId(&id), "ncclGetUniqueId");
+  memcpy(out128, &id, sizeof id);
+  return true;
+}
+
+Comm* nccl_comm_create(int world, int rank, const void* id128, int device) {
+  const NcclApi& n = nccl();
+  if (!n.ok) fail(4, "libnccl.so.2 not found (tensor parallelism needs NCCL)");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  ncclUniqueId id;
+  memcpy(&id, id128, sizeof id);
+  auto* c = new NcclComm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  const int r = n.CommInitRank(&c->c, world, id, rank);
+  if (r != ncclSuccess) {
+    delete c;
+    nccl_check(r, "ncclCommInitRank");
+  }
+  return c;
+}
+
+Comm* local_comm_create(int world, int rank, const std::string& key, int device) {
+  if (world > kMaxLocal) fail(1, "local communicator: at most 8 ranks");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  std::shared_ptr<LocalGroup> g;
+  {
+    std::lock_guard<std::mutex> lk(g_groups_mu);
+    g = g_groups[key].lock();
+    if (!g) {
+      g = std::make_shared<LocalGroup>();
+      g->world = world;
+      g_groups[key] = g;
+    }
+  }
+  if (g->world != world) fail(1, "local communicator: world size differs from the group's");
+  {
+    std::lock_guard<std::mutex> lk(g->m);
+    if (g->ev_a[rank]) fail(1, "local communicator: rank joined twice");
+    cuda_check(cudaEventCreateWithFlags(&g->ev_a[rank], cudaEventDisableTiming), "cudaEventCreate");
+    cuda_check(cudaEventCreateWithFlags(&g->ev_b[rank], cudaEventDisableTiming), "cudaEventCreate");
+    ++g->joined;
+  }
+  auto* c = new LocalComm();
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  c->g = g;
+  cuda_check(cudaMalloc(&c->kscratch, 8), "cudaMalloc");
+  // peers on other devices are read directly: enable access to all of them
+  int ndev = 0;
+  cudaGetDeviceCount(&ndev);
+  for (int d = 0; d < ndev; ++d) {
+    int can = 0;
+    if (d != device && cudaDeviceCanAccessPeer(&can, device, d) == cudaSuccess && can) {
+      const cudaError_t e = cudaDeviceEnablePeerAccess(d, 0);
+      if (e != cudaSuccess && e != cudaErrorPeerAccessAlreadyEnabled) cuda_check(e, "peer access");
+      cudaGetLastError();
+    }
+  }
+  return c;
+}
+
+void tp_allreduce_f32(Exec& ex, Comm* comm, float* buf, size_t n) {
+  if (ex.world <= 1) return;
+  if (!comm) fail(1, "tensor-parallel template without a communicator");
+  comm->allreduce_f32(buf, n, ex.compute);
+}
+
+void tp_argmax_reduce(Exec& ex, Comm* comm, unsigned long long* key) {
+  if (ex.world <= 1) return;
+  if (!comm) fail(1, "tensor-parallel template without a communicator");
+  comm->max_u64(key, ex.compute);
+}
+
+void tp_allgather_logits(Exec& ex, Comm* comm) {
+  if (ex.world <= 1) return;
+  if (!comm) fail(1, "tensor-parallel template without a communicator");
+  comm->allgather_f32(ex.logits, (size_t)ex.m.vocab / ex.world, ex.compute);
+}
+
+}  // namespace tidal

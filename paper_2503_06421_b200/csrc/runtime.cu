@@ -319,10 +319,10 @@ static int op_kind(const std::string& n) {
   return it->second;
 }
 
-// TP collectives (nccl.cu); no-ops when world == 1.
-void tp_allreduce_f32(Exec& ex, void* comm, float* buf, size_t n);
-void tp_argmax_reduce(Exec& ex, void* comm, unsigned long long* key);
-void tp_allgather_logits(Exec& ex, void* comm);
+// TP collectives (comm.cu); no-ops when world == 1.
+void tp_allreduce_f32(Exec& ex, Comm* comm, float* buf, size_t n);
+void tp_argmax_reduce(Exec& ex, Comm* comm, unsigned long long* key);
+void tp_allgather_logits(Exec& ex, Comm* comm);
 
 void run_forward(Exec& ex, const RunArgs& a) {
   const TensorTable& tt = *a.tt;
@@ -401,7 +401,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_MLP_AR:
         {
           const int e0 = P0();
-          tp_allreduce_f32(ex, a.nccl, ex.X, (size_t)S * d);
+          tp_allreduce_f32(ex, a.comm, ex.X, (size_t)S * d);
           if (e0 >= 0) ex.prof_end(KC_ALLREDUCE, e0, 0, Sd * d * 4);
         }
         break;
@@ -487,10 +487,10 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_LOGITS_AG:
-        tp_allgather_logits(ex, a.nccl);
+        tp_allgather_logits(ex, a.comm);
         break;
       case OP_ARGMAX:  // fused: atomicMax of packed keys in the head kernel
-        tp_argmax_reduce(ex, a.nccl, ex.key);
+        tp_argmax_reduce(ex, a.comm, ex.key);
         break;
     }
   }

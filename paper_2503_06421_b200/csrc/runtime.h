@@ -105,6 +105,17 @@ struct Recorder {  // lax tracing: first-read order of weights as ops execute
   }
 };
 
+// TP collectives (comm.cu), enqueued on `s`; every rank calls them in the same
+// order with the same sizes.  allgather_f32: buf holds world slices of n
+// floats, this rank's slice filled in place.
+struct Comm {
+  int world = 1, rank = 0, device = 0;
+  virtual ~Comm() {}
+  virtual void allreduce_f32(float* buf, size_t n, cudaStream_t s) = 0;
+  virtual void max_u64(unsigned long long* key, cudaStream_t s) = 0;
+  virtual void allgather_f32(float* buf, size_t n, cudaStream_t s) = 0;
+};
+
 struct RunArgs {
   const TensorTable* tt = nullptr;
   const std::vector<Op>* ops = nullptr;
@@ -117,7 +128,7 @@ struct RunArgs {
   const void* akey = nullptr;
   uint64_t gen = 0;
   Recorder* rec = nullptr;
-  void* nccl = nullptr;  // ncclComm_t for TP (nullable)
+  Comm* comm = nullptr;  // TP communicator (nullable when world == 1)
 };
 
 // Enqueue the forward for one prompt on exec.compute (tokens already in exec.tok).

@@ -102,6 +102,7 @@ SIGNATURES = [
     ("tidal_host_free", None, [VP]),
     ("tidal_comm_unique_id", C.c_int, [VP]),
     ("tidal_comm_create", C.c_int, [C.c_int, C.c_int, VP, C.c_int, C.POINTER(VP)]),
+    ("tidal_comm_create_local", C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_int, C.POINTER(VP)]),
     ("tidal_comm_destroy", None, [VP]),
     ("tidal_set_debug", C.c_int, [VP, C.c_int, C.c_int]),
     ("tidal_template_checksum", C.c_int, [VP, C.POINTER(C.c_uint64)]),
@@ -333,10 +334,18 @@ class Adapter:
 
 
 class Comm:
-    def __init__(self, world: int, rank: int, unique_id: bytes, device: int):
+    """TP communicator: NCCL (one process per GPU, `unique_id` from rank 0) or,
+    with `local=<group name>`, the in-process ranks of one process (one thread
+    per rank; ranks may share a GPU)."""
+
+    def __init__(self, world: int, rank: int, unique_id: bytes = b"", device: int = 0,
+                 local: Optional[str] = None):
         h = VP()
-        idb = C.create_string_buffer(unique_id, 128)
-        _check(lib().tidal_comm_create(world, rank, idb, device, C.byref(h)))
+        if local is not None:
+            _check(lib().tidal_comm_create_local(world, rank, local.encode(), device, C.byref(h)))
+        else:
+            idb = C.create_string_buffer(unique_id, 128)
+            _check(lib().tidal_comm_create(world, rank, idb, device, C.byref(h)))
         self.h = h
 
     @staticmethod
