@@ -201,6 +201,20 @@ tidal_status tidal_invoke_prefill(tidal_template* tpl, const tidal_adapter* a,
                                   float* host_logits_out, int32_t* host_token_out,
                                   tidal_stats* stats);
 
+/* Batched prefill (§7.2 "TTFT with varied input lengths and batch
+ * sizes", Fig. ttft-bs: batch of prompts of one input length): n_seqs prompts of
+ * seq_len tokens each, host_tokens row-major [n_seqs][seq_len]; every prompt
+ * attends only to itself and its positions restart at 0.  The weights are
+ * streamed once for the whole batch.  1 <= n_seqs <= 64 and n_seqs * seq_len
+ * <= max_tokens.  Outputs: host_tokens_out[n_seqs] (first token of each
+ * prompt) and, if non-NULL, host_logits_out[n_seqs][vocab].  Same
+ * synchronisation, TP and error rules as tidal_invoke_prefill, which is the
+ * n_seqs = 1 case. */
+tidal_status tidal_invoke_prefill_batch(tidal_template* tpl, const tidal_adapter* a,
+                                        const int32_t* host_tokens, int n_seqs, int seq_len,
+                                        float* host_logits_out, int32_t* host_tokens_out,
+                                        tidal_stats* stats);
+
 /* ---- pinned host memory for adapters / pools (cudaHostAlloc) ---- */
 tidal_status tidal_host_alloc(uint64_t bytes, void** out);
 void tidal_host_free(void* p);

@@ -583,11 +583,22 @@ tidal_status tidal_plan_dump(const tidal_template* tp, const tidal_adapter* a, c
 tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
                                   const int32_t* host_tokens, int n_tokens, float* host_logits_out,
                                   int32_t* host_token_out, tidal_stats* stats) {
+  return tidal_invoke_prefill_batch(tp, ca, host_tokens, 1, n_tokens, host_logits_out,
+                                    host_token_out, stats);
+}
+
+tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter* ca,
+                                        const int32_t* host_tokens, int n_seqs, int seq_len,
+                                        float* host_logits_out, int32_t* host_tokens_out,
+                                        tidal_stats* stats) {
   TIDAL_TRY
   const auto t_entry = std::chrono::steady_clock::now();
-  require(tp && host_tokens && host_token_out, "null argument");
+  require(tp && host_tokens && host_tokens_out, "null argument");
   require(!tp->dry, "dry template cannot be invoked");
-  require(n_tokens >= 1 && n_tokens <= tp->max_tokens, "n_tokens out of range");
+  require(n_seqs >= 1 && n_seqs <= kMaxBatch, "n_seqs out of range (1..64)");
+  require(seq_len >= 1 && (int64_t)n_seqs * seq_len <= tp->max_tokens,
+          "n_seqs * seq_len exceeds the template's max_tokens");
+  const int n_tokens = n_seqs * seq_len;
   const int V = tp->shape.vocab;
   for (int i = 0; i < n_tokens; ++i)
     require(host_tokens[i] >= 0 && host_tokens[i] < V, "token out of range");
@@ -680,27 +691,33 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
   ra.copy_pos = &copy_pos;
   ra.skip_group = skip;
   ra.S = n_tokens;
+  ra.nseq = n_seqs;
   ra.lora_scale = a ? a->scale : 1.f;
   ra.akey = a ? (const void*)tp->arena : nullptr;
   ra.gen = tp->gen;
   ra.comm = tp->comm ? tp->comm->impl : nullptr;
   run_forward(ex, ra);
   cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_h2d1, 0), "wait copies");
-  cuda_check(cudaMemcpyAsync(ex.h_key, ex.key, 8, cudaMemcpyDeviceToHost, ex.compute), "D2H key");
+  cuda_check(cudaMemcpyAsync(ex.h_key, ex.key, 8ull * n_seqs, cudaMemcpyDeviceToHost, ex.compute),
+             "D2H key");
   if (host_logits_out)
-    cuda_check(cudaMemcpyAsync(ex.h_logits, ex.logits, 4ull * V, cudaMemcpyDeviceToHost, ex.compute),
+    cuda_check(cudaMemcpyAsync(ex.h_logits, ex.logits, 4ull * V * n_seqs, cudaMemcpyDeviceToHost,
+                               ex.compute),
                "D2H logits");
   cuda_check(cudaEventRecord(tp->e_end, ex.compute), "event");
   cuda_check(cudaEventSynchronize(tp->e_end), "invoke");
   tp->suffix_valid = skip < 0;
   if (ex.profile) ex.prof_collect();
-  const unsigned long long key = *ex.h_key;
-  const uint32_t hi = (uint32_t)(key >> 32);
-  const uint32_t bits = (hi & 0x80000000u) ? (hi & 0x7FFFFFFFu) : ~hi;
-  float best;
-  memcpy(&best, &bits, 4);
-  *host_token_out = (int32_t)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu));
-  if (host_logits_out) memcpy(host_logits_out, ex.h_logits, 4ull * V);
+  for (int b = 0; b < n_seqs; ++b)  // packed key: low word = ~token
+    host_tokens_out[b] = (int32_t)(0xFFFFFFFFu - (uint32_t)(ex.h_key[b] & 0xFFFFFFFFu));
+  if (host_logits_out) {
+    // device layout [world][n_seqs][V / world] -> [n_seqs][V]
+    const int W = tp->world, Vl = V / W;
+    for (int k = 0; k < W; ++k)
+      for (int b = 0; b < n_seqs; ++b)
+        memcpy(host_logits_out + (size_t)b * V + (size_t)k * Vl,
+               ex.h_logits + ((size_t)k * n_seqs + b) * Vl, 4ull * Vl);
+  }
   const auto t1 = std::chrono::steady_clock::now();
   if (stats) {
     memset(stats, 0, sizeof *stats);
@@ -721,7 +738,14 @@ tidal_status tidal_invoke_prefill(tidal_template* tp, const tidal_adapter* ca,
     stats->n_copies = (int)P.groups.size();
     stats->n_kernels = ex.launches;
   }
-  if (key == 0 || std::isnan(best)) fail(TIDAL_ERR_NUMERIC, "NaN in logits (argmax undefined)");
+  for (int i = 0; i < n_seqs; ++i) {
+    const unsigned long long key = ex.h_key[i];
+    const uint32_t hi = (uint32_t)(key >> 32);
+    const uint32_t bits = (hi & 0x80000000u) ? (hi & 0x7FFFFFFFu) : ~hi;
+    float best;
+    memcpy(&best, &bits, 4);
+    if (key == 0 || std::isnan(best)) fail(TIDAL_ERR_NUMERIC, "NaN in logits (argmax undefined)");
+  }
   TIDAL_CATCH
 }
 
@@ -897,7 +921,7 @@ tidal_status tidal_k_head(const float* xlast, const void* g, const void* W, int 
                           float* logits, unsigned long long* key) {
   cudaError_t e = cudaMemset(key, 0, 8);
   if (e == cudaSuccess)
-    e = head_launch(xlast, (const bf16*)g, (const bf16*)W, V, d, eps, logits, key, 0, sms(), 0);
+    e = head_launch(xlast, 0, 1, (const bf16*)g, (const bf16*)W, V, d, eps, logits, V, key, 0, sms(), 0);
   return sync_status(e, "head");
 }
 

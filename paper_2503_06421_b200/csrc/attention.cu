@@ -71,6 +71,8 @@ __global__ void __launch_bounds__(NTH, 2) attn_kernel(const bf16* __restrict__ q
   const int h = blockIdx.y;
   const int g = h / (H / KV);
   const int ld = (H + 2 * KV) * HD;
+  qkv += (size_t)blockIdx.z * S * ld;  // sequence blockIdx.z of a batch (rows z*S .. z*S+S-1)
+  O += (size_t)blockIdx.z * S * (H * HD);
   const int q0 = qt * BQ;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const bf16* Qg = qkv + (size_t)h * HD;
@@ -232,7 +234,7 @@ __global__ void __launch_bounds__(NTH, 2) attn_kernel(const bf16* __restrict__ q
 }
 
 template <int HD>
-cudaError_t launch(const bf16* qkv, bf16* O, int S, int H, int KV, cudaStream_t s) {
+cudaError_t launch(const bf16* qkv, bf16* O, int S, int H, int KV, cudaStream_t s, int nseq) {
   const int smem = (BQ + 4 * BKV) * HD * 2;
   static bool attr = false;
   if (!attr) {
@@ -241,7 +243,7 @@ cudaError_t launch(const bf16* qkv, bf16* O, int S, int H, int KV, cudaStream_t 
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((S + BQ - 1) / BQ, H);
+  dim3 grid((S + BQ - 1) / BQ, H, nseq);
   const float scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
   return launch_k(attn_kernel<HD>, grid, dim3(NTH), smem, s, 1, qkv, O, S, H, KV, scale_log2);
 }
@@ -249,9 +251,10 @@ cudaError_t launch(const bf16* qkv, bf16* O, int S, int H, int KV, cudaStream_t 
 }  // namespace
 
 cudaError_t attention_launch(const bf16* qkv, bf16* O, int S, int H, int KV, int hd,
-                             cudaStream_t s) {
-  if (hd == 128) return launch<128>(qkv, O, S, H, KV, s);
-  if (hd == 64) return launch<64>(qkv, O, S, H, KV, s);
+                             cudaStream_t s, int nseq) {
+  if (nseq < 1 || nseq > 65535) return cudaErrorInvalidValue;
+  if (hd == 128) return launch<128>(qkv, O, S, H, KV, s, nseq);
+  if (hd == 64) return launch<64>(qkv, O, S, H, KV, s, nseq);
   return cudaErrorInvalidValue;
 }
 

@@ -71,7 +71,9 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
   const int qt = nq - 1 - (int)blockIdx.x;  // heavy (late) query tiles first
   const int h = blockIdx.y;
   const int g = h / (p.H / p.KV);
-  const int q0 = qt * BQ;
+  const int q0 = qt * BQ;                   // positions within the sequence
+  const int base = blockIdx.z * p.S;        // first row of this sequence (batched prompts)
+  const int vbase = blockIdx.z * ((p.S + 63) & ~63);  // its first V^T column (64-aligned)
   const int nkv = qt + 1;                   // causal: key tiles 0..qt (BQ == BKV)
 
   if (warp == 0 && lane == 0) {
@@ -102,8 +104,8 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     if (lane == 0) {
       const int qc = h * HD, kc = (p.H + g) * HD, vr = g * HD;
       ptx::mbar_expect_tx(q_full, TILE);
-      ptx::tma_load_2d(&p.q, sb + OFF_Q, q_full, qc, q0);
-      ptx::tma_load_2d(&p.q, sb + OFF_Q + HALF, q_full, qc + 64, q0);
+      ptx::tma_load_2d(&p.q, sb + OFF_Q, q_full, qc, base + q0);
+      ptx::tma_load_2d(&p.q, sb + OFF_Q + HALF, q_full, qc + 64, base + q0);
       // in-order issue K_0 V_0 K_1 V_1 ...: V_j's slot frees (PV_{j-2}) before
       // K_{j+1}'s (S_{j-1}), so the single producer never waits needlessly
       for (int j = 0; j < nkv; ++j) {
@@ -111,13 +113,13 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         ptx::mbar_wait(k_empty(s), ((j / KST) & 1) ^ 1);
         ptx::mbar_expect_tx(k_full(s), TILE);
         const uint32_t ks = sb + OFF_K + s * TILE;
-        ptx::tma_load_2d(&p.q, ks, k_full(s), kc, j * BKV);
-        ptx::tma_load_2d(&p.q, ks + HALF, k_full(s), kc + 64, j * BKV);
+        ptx::tma_load_2d(&p.q, ks, k_full(s), kc, base + j * BKV);
+        ptx::tma_load_2d(&p.q, ks + HALF, k_full(s), kc + 64, base + j * BKV);
         ptx::mbar_wait(v_empty(t), ((j / VST) & 1) ^ 1);
         ptx::mbar_expect_tx(v_full(t), TILE);
         const uint32_t vs = sb + OFF_V + t * TILE;
-        ptx::tma_load_2d(&p.vt, vs, v_full(t), j * BKV, vr);
-        ptx::tma_load_2d(&p.vt, vs + HALF, v_full(t), j * BKV + 64, vr);
+        ptx::tma_load_2d(&p.vt, vs, v_full(t), vbase + j * BKV, vr);
+        ptx::tma_load_2d(&p.vt, vs + HALF, v_full(t), vbase + j * BKV + 64, vr);
       }
     }
     __syncwarp();
@@ -253,7 +255,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     const float inv = 1.f / (l + lsum[(half ^ 1) * BQ + row]);
     ptx::mbar_wait(pv_done, (nkv - 1) & 1);
     ptx::tc_fence_after();
-    bf16* out = p.out + (size_t)qi * p.ldo + h * HD + half * 64;
+    bf16* out = p.out + (size_t)(base + qi) * p.ldo + h * HD + half * 64;
 #pragma unroll 1
     for (int c = 0; c < 2; ++c) {
       uint32_t r[32];
@@ -283,12 +285,19 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
 }  // namespace
 
 bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, bf16* out, int S,
-                    int H, int KV) {
+                    int H, int KV, int nseq) {
   const int ld = (H + 2 * KV) * HD;
-  if (!make_tmap(&p->q, qkv, S, ld, (uint64_t)ld * 2, 128, 64)) return false;
+  const uint64_t rows = (uint64_t)S * nseq;
+  if (nseq < 1 || nseq > 65535) return false;
+  if (!make_tmap(&p->q, qkv, rows, ld, (uint64_t)ld * 2, 128, 64)) return false;
   p->k = p->q;  // K tiles are 128 keys: same box as Q
-  if (!make_tmap(&p->vt, vt, (uint64_t)KV * HD, S, (uint64_t)vt_ld * 2, 128, 64)) return false;
+  // V^T columns: sequence b at b * round_up(S, 64) (the QKV epilogue's layout); one
+  // sequence: S columns, keys past S read as zero (out of bounds)
+  const uint64_t vcols = nseq > 1 ? (uint64_t)nseq * ((S + 63) & ~63) : (uint64_t)S;
+  if (vcols > (uint64_t)vt_ld) return false;
+  if (!make_tmap(&p->vt, vt, (uint64_t)KV * HD, vcols, (uint64_t)vt_ld * 2, 128, 64)) return false;
   p->S = S;
+  p->nseq = nseq;
   p->H = H;
   p->KV = KV;
   p->scale_log2 = 1.4426950408889634f / sqrtf((float)HD);
@@ -305,7 +314,7 @@ cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  dim3 grid((p.S + BQ - 1) / BQ, p.H);
+  dim3 grid((p.S + BQ - 1) / BQ, p.H, p.nseq);
   return launch_k(attn_tc_kernel, grid, dim3(NTH), SMEM, s, 1, p);
 }
 

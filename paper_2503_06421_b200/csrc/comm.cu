@@ -89,8 +89,8 @@ struct NcclComm final : Comm {
   void allreduce_f32(float* buf, size_t n, cudaStream_t s) override {
     nccl_check(g_nccl.AllReduce(buf, buf, n, ncclFloat32, ncclSum, c, s), "ncclAllReduce");
   }
-  void max_u64(unsigned long long* key, cudaStream_t s) override {
-    nccl_check(g_nccl.AllReduce(key, key, 1, ncclUint64, ncclMax, c, s), "ncclAllReduce(max)");
+  void max_u64(unsigned long long* key, size_t n, cudaStream_t s) override {
+    nccl_check(g_nccl.AllReduce(key, key, n, ncclUint64, ncclMax, c, s), "ncclAllReduce(max)");
   }
   void allgather_f32(float* buf, size_t n, cudaStream_t s) override {
     nccl_check(g_nccl.AllGather(buf + (size_t)rank * n, buf, n, ncclFloat32, c, s), "ncclAllGather");
@@ -120,13 +120,15 @@ __global__ void sum_ranks_kernel(SrcPtrs src, float* __restrict__ out, size_t n4
   }
 }
 
-__global__ void max_ranks_kernel(SrcPtrs src, unsigned long long* out) {
-  unsigned long long m = 0;
-  for (int k = 0; k < src.n; ++k) {
-    const unsigned long long v = *reinterpret_cast<const unsigned long long*>(src.p[k]);
-    m = v > m ? v : m;
+__global__ void max_ranks_kernel(SrcPtrs src, unsigned long long* out, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    unsigned long long m = 0;
+    for (int k = 0; k < src.n; ++k) {
+      const unsigned long long v = reinterpret_cast<const unsigned long long*>(src.p[k])[i];
+      m = v > m ? v : m;
+    }
+    out[i] = m;
   }
-  *out = m;
 }
 
 struct LocalGroup {
@@ -206,12 +208,13 @@ struct LocalComm final : Comm {
     retire(s);
     cuda_check(cudaMemcpyAsync(buf, scratch, n * 4, cudaMemcpyDeviceToDevice, s), "D2D");
   }
-  void max_u64(unsigned long long* key, cudaStream_t s) override {
+  void max_u64(unsigned long long* key, size_t n, cudaStream_t s) override {
+    if (n > kMaxBatch) fail(1, "local max-reduce: too many keys");
     publish(key, s);
-    max_ranks_kernel<<<1, 1, 0, s>>>(srcs(), kscratch);
+    max_ranks_kernel<<<1, 64, 0, s>>>(srcs(), kscratch, (int)n);
     cuda_check(cudaGetLastError(), "max_ranks");
     retire(s);
-    cuda_check(cudaMemcpyAsync(key, kscratch, 8, cudaMemcpyDeviceToDevice, s), "D2D");
+    cuda_check(cudaMemcpyAsync(key, kscratch, 8 * n, cudaMemcpyDeviceToDevice, s), "D2D");
   }
   void allgather_f32(float* buf, size_t n, cudaStream_t s) override {
     publish(buf, s);
@@ -278,7 +281,7 @@ Comm* local_comm_create(int world, int rank, const std::string& key, int device)
   c->rank = rank;
   c->device = device;
   c->g = g;
-  cuda_check(cudaMalloc(&c->kscratch, 8), "cudaMalloc");
+  cuda_check(cudaMalloc(&c->kscratch, 8 * kMaxBatch), "cudaMalloc");
   // peers on other devices are read directly: enable access to all of them
   int ndev = 0;
   cudaGetDeviceCount(&ndev);
@@ -299,16 +302,17 @@ void tp_allreduce_f32(Exec& ex, Comm* comm, float* buf, size_t n) {
   comm->allreduce_f32(buf, n, ex.compute);
 }
 
-void tp_argmax_reduce(Exec& ex, Comm* comm, unsigned long long* key) {
+void tp_argmax_reduce(Exec& ex, Comm* comm, unsigned long long* key, int nseq) {
   if (ex.world <= 1) return;
   if (!comm) fail(1, "tensor-parallel template without a communicator");
-  comm->max_u64(key, ex.compute);
+  comm->max_u64(key, (size_t)nseq, ex.compute);
 }
 
-void tp_allgather_logits(Exec& ex, Comm* comm) {
+// logits are [world][nseq][V / world]: rank r's slices are contiguous
+void tp_allgather_logits(Exec& ex, Comm* comm, int nseq) {
   if (ex.world <= 1) return;
   if (!comm) fail(1, "tensor-parallel template without a communicator");
-  comm->allgather_f32(ex.logits, (size_t)ex.m.vocab / ex.world, ex.compute);
+  comm->allgather_f32(ex.logits, (size_t)nseq * (ex.m.vocab / ex.world), ex.compute);
 }
 
 }  // namespace tidal

@@ -433,7 +433,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
             ld_chunk(tacc + c1, v);
             ld_chunk(tacc + c2, w);
             if (m < p.M) {
-              const float2* cs = p.rope + (size_t)m * half + j * 32;
+              const int pos = p.seq_len ? m % p.seq_len : m;  // batched prompts restart at 0
+              const float2* cs = p.rope + (size_t)pos * half + j * 32;
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
                 const float2 t = cs[i];
@@ -456,12 +457,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           store_chunk_bf16(v, stg, lane, reinterpret_cast<bf16*>(p.out), p.ldo, row0, p.M,
                            sg.out_col + n0 + j * 32, ncols - j * 32);
           if (EPI == EPI_ROPE && sg.vt && m < p.M) {
-            // V^T for the tcgen05 attention: lanes are consecutive tokens -> coalesced
-            bf16* dst = p.vt + (size_t)(n0 + j * 32) * p.vt_ld + m;
+            // V^T for the tcgen05 attention: lanes are consecutive tokens -> coalesced.
+            // Batched prompts: sequence b's keys start at column b * round_up(seq_len, 64),
+            // so every TMA box of V^T starts 16-B aligned; the last row of a sequence
+            // also zeroes its padding columns (masked keys must hold finite values).
+            int vcol = m, pad = 0;
+            if (p.seq_len) {
+              const int sb = m / p.seq_len, pos = m - sb * p.seq_len;
+              const int lp = (p.seq_len + 63) & ~63;
+              vcol = sb * lp + pos;
+              if (pos == p.seq_len - 1) pad = lp - p.seq_len;
+            }
+            bf16* dst = p.vt + (size_t)(n0 + j * 32) * p.vt_ld + vcol;
             const int nv = min(32, ncols - j * 32);
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (i < nv) dst[(size_t)i * p.vt_ld] = __float2bfloat16_rn(v[i]);
+#pragma unroll 1
+            for (int i = 0; i < nv; ++i)
+              for (int c = 1; c <= pad; ++c) dst[(size_t)i * p.vt_ld + c] = __float2bfloat16_rn(0.f);
           }
         }
       }

@@ -40,9 +40,9 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // ---------------- embedding gather ----------------
 __global__ void embed_kernel(const int32_t* __restrict__ tok, const bf16* __restrict__ E,
                              float* __restrict__ X, int d, int row0, int rows,
-                             unsigned long long* key_reset) {
+                             unsigned long long* key_reset, int n_keys) {
   ptx::pdl_begin();
-  if (key_reset && blockIdx.x == 0 && threadIdx.x == 0) *key_reset = 0ull;  // argmax of this forward
+  if (key_reset && blockIdx.x == 0 && threadIdx.x < n_keys) key_reset[threadIdx.x] = 0ull;  // argmax keys
   const int s = blockIdx.x;
   const int t = tok[s] - row0;
   const bool mine = t >= 0 && t < rows;
@@ -111,54 +111,73 @@ __device__ __forceinline__ unsigned long long argmax_key(float v, int idx) {
 }
 
 __global__ void __launch_bounds__(HEAD_THREADS) head_kernel(const float* __restrict__ xlast,
+                                                            size_t x_stride, int nrows,
                                                             const bf16* __restrict__ g,
                                                             const bf16* __restrict__ W, int V,
                                                             int d, float eps,
-                                                            float* __restrict__ logits,
+                                                            float* __restrict__ logits, int ldl,
                                                             unsigned long long* key, int voff) {
-  extern __shared__ float hs[];  // d floats
+  extern __shared__ float hs[];  // nrows x d floats: the normalised last rows
   __shared__ float red[32];
-  __shared__ unsigned long long kred[HEAD_THREADS / 32];
+  __shared__ unsigned long long kred[HEAD_MAX_ROWS][HEAD_THREADS / 32];
   ptx::pdl_begin();
-  float ss = 0.f;
-  for (int i = threadIdx.x; i < d; i += HEAD_THREADS) {
-    const float v = xlast[i];
-    ss += v * v;
+  for (int b = 0; b < nrows; ++b) {
+    const float* x = xlast + (size_t)b * x_stride;
+    float ss = 0.f;
+    for (int i = threadIdx.x; i < d; i += HEAD_THREADS) {
+      const float v = x[i];
+      ss += v * v;
+    }
+    ss = block_sum<HEAD_THREADS>(ss, red);
+    const float inv = rsqrtf(ss / (float)d + eps);
+    for (int i = threadIdx.x; i < d; i += HEAD_THREADS)
+      hs[b * d + i] = x[i] * inv * __bfloat162float(g[i]);
   }
-  ss = block_sum<HEAD_THREADS>(ss, red);
-  const float inv = rsqrtf(ss / (float)d + eps);
-  for (int i = threadIdx.x; i < d; i += HEAD_THREADS) hs[i] = xlast[i] * inv * __bfloat162float(g[i]);
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * (HEAD_THREADS / 32) + warp;
   const int nw = gridDim.x * (HEAD_THREADS / 32);
-  unsigned long long best = 0;
+  unsigned long long best[HEAD_MAX_ROWS];
+#pragma unroll
+  for (int b = 0; b < HEAD_MAX_ROWS; ++b) best[b] = 0;
   for (int v = gw; v < V; v += nw) {
     const bf16* w = W + (size_t)v * d;
-    float acc = 0.f;
-    for (int c = lane * 8; c < d; c += 256) {
+    float acc[HEAD_MAX_ROWS];
+#pragma unroll
+    for (int b = 0; b < HEAD_MAX_ROWS; ++b) acc[b] = 0.f;
+    for (int c = lane * 8; c < d; c += 256) {  // each W row is read once for all rows
       uint4 q = __ldg(reinterpret_cast<const uint4*>(w + c));
       const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-      const float4 x0 = *reinterpret_cast<const float4*>(hs + c);
-      const float4 x1 = *reinterpret_cast<const float4*>(hs + c + 4);
-      float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
-      float2 e = __bfloat1622float2(h[2]), f = __bfloat1622float2(h[3]);
-      acc += a.x * x0.x + a.y * x0.y + b.x * x0.z + b.y * x0.w + e.x * x1.x + e.y * x1.y +
-             f.x * x1.z + f.y * x1.w;
+      const float2 a = __bfloat1622float2(h[0]), bb = __bfloat1622float2(h[1]);
+      const float2 e = __bfloat1622float2(h[2]), f = __bfloat1622float2(h[3]);
+#pragma unroll
+      for (int b = 0; b < HEAD_MAX_ROWS; ++b) {
+        if (b >= nrows) break;
+        const float4 x0 = *reinterpret_cast<const float4*>(hs + b * d + c);
+        const float4 x1 = *reinterpret_cast<const float4*>(hs + b * d + c + 4);
+        acc[b] += a.x * x0.x + a.y * x0.y + bb.x * x0.z + bb.y * x0.w + e.x * x1.x + e.y * x1.y +
+                  f.x * x1.z + f.y * x1.w;
+      }
     }
-    acc = warp_sum(acc);
-    if (lane == 0) {
-      logits[v] = acc;
-      const unsigned long long k = argmax_key(acc, v + voff);
-      best = k > best ? k : best;
+#pragma unroll
+    for (int b = 0; b < HEAD_MAX_ROWS; ++b) {
+      if (b >= nrows) break;
+      const float r = warp_sum(acc[b]);
+      if (lane == 0) {
+        logits[(size_t)b * ldl + v] = r;
+        const unsigned long long k = argmax_key(r, v + voff);
+        best[b] = k > best[b] ? k : best[b];
+      }
     }
   }
-  if (lane == 0) kred[warp] = best;
+  if (lane == 0)
+#pragma unroll
+    for (int b = 0; b < HEAD_MAX_ROWS; ++b) kred[b][warp] = best[b];
   __syncthreads();
-  if (threadIdx.x == 0) {
-    unsigned long long b = 0;
-    for (int i = 0; i < HEAD_THREADS / 32; ++i) b = kred[i] > b ? kred[i] : b;
-    if (b) atomicMax(key, b);
+  if (threadIdx.x < nrows) {
+    unsigned long long m = 0;
+    for (int i = 0; i < HEAD_THREADS / 32; ++i) m = kred[threadIdx.x][i] > m ? kred[threadIdx.x][i] : m;
+    if (m) atomicMax(key + threadIdx.x, m);
   }
 }
 
@@ -192,11 +211,13 @@ __global__ void nan_check_kernel(const float* x, int n, int* flag) {
 }  // namespace
 
 cudaError_t embed_launch(const int32_t* tok, const bf16* E, float* X, int S, int d, int row0,
-                         int rows, cudaStream_t s, unsigned long long* key_reset) {
+                         int rows, cudaStream_t s, unsigned long long* key_reset, int n_keys) {
   int th = d / 8;
   if (th > 1024) th = 1024;
   if (th < 32) th = 32;
-  return launch_k(embed_kernel, dim3(S), dim3(th), 0, s, 1, tok, E, X, d, row0, rows, key_reset);
+  if (key_reset && n_keys > th) return cudaErrorInvalidValue;
+  return launch_k(embed_kernel, dim3(S), dim3(th), 0, s, 1, tok, E, X, d, row0, rows, key_reset,
+                  n_keys);
 }
 
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d, float eps,
@@ -204,20 +225,32 @@ cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d,
   return launch_k(rmsnorm_kernel, dim3(S), dim3(NORM_THREADS), 0, s, 1, X, g, Y, d, eps);
 }
 
-cudaError_t head_launch(const float* X_last, const bf16* g, const bf16* W, int V, int d, float eps,
-                        float* logits, unsigned long long* key, int vocab_offset, int num_sms,
-                        cudaStream_t s) {
-  const size_t smem = (size_t)d * sizeof(float);
-  if (smem > 48 * 1024) {
+cudaError_t head_launch(const float* X_last, size_t x_stride, int nseq, const bf16* g, const bf16* W,
+                        int V, int d, float eps, float* logits, int ldl, unsigned long long* key,
+                        int vocab_offset, int num_sms, cudaStream_t s) {
+  static bool attr = false;
+  if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(head_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)smem);
+                                         200 * 1024);
     if (e != cudaSuccess) return e;
+    attr = true;
   }
+  // rows per launch: the normalised rows must fit the 200 KB of shared memory
+  int per = (int)((200 * 1024) / ((size_t)d * sizeof(float)));
+  per = per < HEAD_MAX_ROWS ? per : HEAD_MAX_ROWS;
+  if (per < 1) return cudaErrorInvalidValue;
   int grid = num_sms * 4;
   const int need = (V + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32);
   if (grid > need) grid = need;
-  return launch_k(head_kernel, dim3(grid), dim3(HEAD_THREADS), smem, s, 1, X_last, g, W, V, d, eps,
-                  logits, key, vocab_offset);
+  for (int b0 = 0; b0 < nseq; b0 += per) {
+    const int nr = nseq - b0 < per ? nseq - b0 : per;
+    const cudaError_t e = launch_k(head_kernel, dim3(grid), dim3(HEAD_THREADS),
+                                   (size_t)nr * d * sizeof(float), s, 1, X_last + b0 * x_stride,
+                                   x_stride, nr, g, W, V, d, eps, logits + (size_t)b0 * ldl, ldl,
+                                   key + b0, vocab_offset);
+    if (e != cudaSuccess) return e;
+  }
+  return cudaSuccess;
 }
 
 cudaError_t poison_launch(void* p, size_t bytes, cudaStream_t s) {

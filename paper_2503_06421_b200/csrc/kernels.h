@@ -51,6 +51,7 @@ struct alignas(64) GemmParams {
   int ldo;
   const float2* rope;  // [S, head_dim/2] (cos, sin)
   int head_dim;
+  int seq_len;         // EPI_ROPE: position = row % seq_len (batched prompts); 0: position = row
   int bn;              // N tile: 256 | 192 | 128 (EPI_SILU: 128 output cols = 256 acc cols)
   bf16* vt;            // V^T [n_vt][vt_ld] for the tcgen05 attention (segments with vt=1)
   int vt_ld;
@@ -83,13 +84,14 @@ struct alignas(64) AttnParams {
   CUtensorMap q;    // over QKV, box {64 cols, 128 rows}
   CUtensorMap k;    // over QKV, box {64 cols, 64 rows}
   CUtensorMap vt;   // over V^T, box {64 keys, 128 rows}
-  int S, H, KV;
+  int S, H, KV;     // S: tokens per sequence
+  int nseq;         // sequences of S tokens each, stacked along the rows (grid.z)
   float scale_log2;
   bf16* out;
   int ldo;
 };
 bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, bf16* out, int S,
-                    int H, int KV);
+                    int H, int KV, int nseq = 1);
 cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s);
 
 // N-tile width minimising (waves x tile width) on num_sms SMs; the W/lora_B
@@ -107,9 +109,10 @@ cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t 
 // SIMT / legacy-MMA kernels (kernels.cu, attention.cu)
 // ------------------------------------------------------------------------
 // X[s, :] = fp32(E[tok[s] - row0, :]) for tokens in [row0, row0+rows), else 0 (vocab shard).
-// key_reset (nullable): zeroed by the kernel — the packed argmax of this forward.
+// key_reset (nullable): n_keys keys zeroed by the kernel — the packed argmax keys of this forward.
 cudaError_t embed_launch(const int32_t* tok, const bf16* E, float* X, int S, int d, int row0,
-                         int rows, cudaStream_t s, unsigned long long* key_reset = nullptr);
+                         int rows, cudaStream_t s, unsigned long long* key_reset = nullptr,
+                         int n_keys = 1);
 // Y = bf16(g * x * rsqrt(mean(x^2) + eps)), one row per CTA.
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d, float eps,
                            cudaStream_t s);
@@ -117,14 +120,17 @@ cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d,
 // One read of X for all targets; intra-CTA split-K, deterministic reduction.
 cudaError_t lora_shrink_launch(const bf16* X, int ldx, int M, int K, const bf16* const* A,
                                bf16* const* T, int nt, int r, float scale, cudaStream_t s);
-// Causal GQA prefill attention over QKV [S, (H + 2 KV) hd] -> O [S, H hd].
+// Causal GQA prefill attention over QKV [nseq * S, (H + 2 KV) hd] -> O [nseq * S, H hd],
+// each sequence of S rows attending only to itself.
 cudaError_t attention_launch(const bf16* qkv, bf16* O, int S, int H, int KV, int hd,
-                             cudaStream_t s);
-// Final RMSNorm of row X_last, logits[v] = W[v] . h (fp32), packed argmax key
-// (orderable(logit) << 32 | ~v) max-reduced into *key (must be preset to 0).
-cudaError_t head_launch(const float* X_last, const bf16* g, const bf16* W, int V, int d, float eps,
-                        float* logits, unsigned long long* key, int vocab_offset, int num_sms,
-                        cudaStream_t s);
+                             cudaStream_t s, int nseq = 1);
+// For each of nseq rows X_last + b * x_stride: final RMSNorm, logits[b * ldl + v]
+// = W[v] . h (fp32), and the packed argmax key (orderable(logit) << 32 | ~v)
+// max-reduced into key[b] (preset to 0).  W is read once for all rows.
+constexpr int HEAD_MAX_ROWS = 8;
+cudaError_t head_launch(const float* X_last, size_t x_stride, int nseq, const bf16* g, const bf16* W,
+                        int V, int d, float eps, float* logits, int ldl, unsigned long long* key,
+                        int vocab_offset, int num_sms, cudaStream_t s);
 // Debug / invariants.
 cudaError_t poison_launch(void* p, size_t bytes, cudaStream_t s);           // bf16 NaN 0x7FC0
 cudaError_t checksum_launch(const void* p, size_t bytes, unsigned long long* out, cudaStream_t s);

@@ -57,12 +57,14 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   dalloc(O, S * nq * 2);
   dalloc(Hb, S * (size_t)(m.d_ff / world) * 2);
   for (int t = 0; t < kNumTargets; ++t) dalloc(T[t], S * 64 * 2);
-  dalloc(logits, (size_t)m.vocab * 4);
-  dalloc(key, 64);
+  dalloc(logits, (size_t)kMaxBatch * m.vocab * 4);
+  dalloc(key, 8 * kMaxBatch);
   dalloc(tok, S * 4);
   dalloc(shrink_ws, (size_t)SHRINK_MAX_SPLIT * S * 192 * 4);
-  vt_ld = (int)((S + 63) / 64 * 64);
+  // V^T: batched prompts pad each sequence to 64 columns (<= 63 per prompt)
+  vt_ld = (int)((S + 63) / 64 * 64 + 64 * (size_t)kMaxBatch);
   dalloc(Vt, nkv * (size_t)vt_ld * 2);
+  cuda_check(cudaMemset(Vt, 0, nkv * (size_t)vt_ld * 2), "memset V^T");  // padding stays finite
   // RoPE table: angle = pos * theta^(-2i/hd), cos/sin in double, stored fp32
   std::vector<float2> cs(S * (hd / 2));
   for (size_t p = 0; p < S; ++p)
@@ -75,9 +77,10 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   cuda_check(cudaMemcpy(rope, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice),
              "rope upload");
   cuda_check(cudaHostAlloc((void**)&h_tok, S * 4 + 16, cudaHostAllocDefault), "pinned tokens");
-  cuda_check(cudaHostAlloc((void**)&h_logits, (size_t)m.vocab * 4 + 16, cudaHostAllocDefault),
+  cuda_check(cudaHostAlloc((void**)&h_logits, (size_t)kMaxBatch * m.vocab * 4 + 16,
+                           cudaHostAllocDefault),
              "pinned logits");
-  cuda_check(cudaHostAlloc((void**)&h_key, 64, cudaHostAllocDefault), "pinned key");
+  cuda_check(cudaHostAlloc((void**)&h_key, 8 * kMaxBatch, cudaHostAllocDefault), "pinned key");
 }
 
 void Exec::destroy() {
@@ -105,9 +108,9 @@ static void tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
                 " cols=" + std::to_string(cols) + ")");
 }
 
-const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S, const void* akey,
-                                                   uint64_t gen) {
-  auto k = std::make_tuple(S, tt.lora_rank, tt.lora_mask, akey, gen);
+const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S, int nseq,
+                                                   const void* akey, uint64_t gen) {
+  auto k = std::make_tuple(S, nseq, tt.lora_rank, tt.lora_mask, akey, gen);
   auto it = cache.find(k);
   if (it != cache.end()) return it->second;
   const int L = m.n_layers, d = m.d_model, hd = m.head_dim();
@@ -158,6 +161,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     q.ldo = nq + 2 * nkv;
     q.rope = rope;
     q.head_dim = hd;
+    q.seq_len = nseq > 1 ? S / nseq : 0;
     // ---- O (+ residual) ----
     GemmParams& o = ll.o;
     memset(&o, 0, sizeof o);
@@ -289,14 +293,15 @@ void Exec::prof_collect() {
   prof_pending.clear();
 }
 
-cudaError_t Exec::attention_tc(int S, cudaStream_t s) {
-  auto it = attn_cache.find(S);
+cudaError_t Exec::attention_tc(int S, int nseq, cudaStream_t s) {
+  auto it = attn_cache.find({S, nseq});
   if (it == attn_cache.end()) {
     AttnParams p;
     memset(&p, 0, sizeof p);
-    if (!attn_tc_params(&p, QKV, Vt, vt_ld, O, S, m.n_heads / world, m.n_kv_heads / world))
+    if (!attn_tc_params(&p, QKV, Vt, vt_ld, O, S / nseq, m.n_heads / world, m.n_kv_heads / world,
+                        nseq))
       fail(3, "attention tensor maps");
-    it = attn_cache.emplace(S, p).first;
+    it = attn_cache.emplace(std::make_pair(S, nseq), p).first;
   }
   return attn_tc_launch(it->second, s);
 }
@@ -321,8 +326,8 @@ static int op_kind(const std::string& n) {
 
 // TP collectives (comm.cu); no-ops when world == 1.
 void tp_allreduce_f32(Exec& ex, Comm* comm, float* buf, size_t n);
-void tp_argmax_reduce(Exec& ex, Comm* comm, unsigned long long* key);
-void tp_allgather_logits(Exec& ex, Comm* comm);
+void tp_argmax_reduce(Exec& ex, Comm* comm, unsigned long long* key, int nseq);
+void tp_allgather_logits(Exec& ex, Comm* comm, int nseq);
 
 void run_forward(Exec& ex, const RunArgs& a) {
   const TensorTable& tt = *a.tt;
@@ -332,7 +337,9 @@ void run_forward(Exec& ex, const RunArgs& a) {
   const int F = m.d_ff / ex.world;
   const int Vl = m.vocab / ex.world;
   const int r = tt.lora_rank;
-  const auto& LP = ex.layer_params(tt, S, a.akey, a.gen);
+  const int B = a.nseq, Ls = S / B;  // B prompts of Ls tokens
+  if (B < 1 || B > kMaxBatch || Ls * B != S) fail(1, "bad batch shape");
+  const auto& LP = ex.layer_params(tt, S, B, a.akey, a.gen);
   cudaStream_t st = ex.compute;
   int waited = -1;
   // event pair around a launch: every launch (profile_all) or the GEMMs only
@@ -392,7 +399,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_EMBED:
         {
           const int e0 = P0();
-          K(KC_EMBED, e0, 0, Sd * d * 6, embed_launch(ex.tok, Wp(tt.embed), ex.X, S, d, ex.rank * Vl, Vl, st, ex.key),
+          K(KC_EMBED, e0, 0, Sd * d * 6, embed_launch(ex.tok, Wp(tt.embed), ex.X, S, d, ex.rank * Vl, Vl, st, ex.key, B),
             "embed");
         }
         break;
@@ -427,11 +434,11 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_ATTN:
         {
           const int e0 = P0();
-          K(KC_ATTN, e0, 2.0 * hd * ((double)m.n_heads / ex.world) * Sd * (Sd + 1),
+          K(KC_ATTN, e0, 2.0 * hd * ((double)m.n_heads / ex.world) * Sd * (Ls + 1.0),
             2.0 * Sd * (2.0 * nq + 2.0 * nkv),
-            hd == 128 ? ex.attention_tc(S, st)
-                      : attention_launch(ex.QKV, ex.O, S, m.n_heads / ex.world,
-                                         m.n_kv_heads / ex.world, hd, st),
+            hd == 128 ? ex.attention_tc(S, B, st)
+                      : attention_launch(ex.QKV, ex.O, Ls, m.n_heads / ex.world,
+                                         m.n_kv_heads / ex.world, hd, st, B),
             "attention");
         }
         break;
@@ -480,17 +487,19 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_HEAD:  // the argmax key was zeroed by the embed kernel of this forward
         {
           const int e0 = P0();
-          K(KC_HEAD, e0, 2.0 * Vl * d, 2.0 * Vl * d + 4.0 * Vl,
-            head_launch(ex.X + (size_t)(S - 1) * d, Wp(tt.fnorm), Wp(tt.head), Vl, d, ex.eps,
-                        ex.logits + (size_t)ex.rank * Vl, ex.key, ex.rank * Vl, ex.num_sms, st),
+          // logits layout [world][B][Vl]: this rank's slices contiguous for the allgather
+          K(KC_HEAD, e0, 2.0 * B * Vl * d, 2.0 * Vl * d + 4.0 * B * Vl,
+            head_launch(ex.X + (size_t)(Ls - 1) * d, (size_t)Ls * d, B, Wp(tt.fnorm), Wp(tt.head),
+                        Vl, d, ex.eps, ex.logits + (size_t)ex.rank * B * Vl, Vl, ex.key,
+                        ex.rank * Vl, ex.num_sms, st),
             "head");
         }
         break;
       case OP_LOGITS_AG:
-        tp_allgather_logits(ex, a.comm);
+        tp_allgather_logits(ex, a.comm, B);
         break;
       case OP_ARGMAX:  // fused: atomicMax of packed keys in the head kernel
-        tp_argmax_reduce(ex, a.comm, ex.key);
+        tp_argmax_reduce(ex, a.comm, ex.key, B);
         break;
     }
   }

@@ -32,6 +32,8 @@ struct LayerLaunch {
 
 // Device execution context: streams, activation arena, rope table, the fork
 // pointer table (tensor id -> device address) and a launch-parameter cache.
+constexpr int kMaxBatch = 64;  // prompts per invocation (logits / argmax buffers)
+
 struct Exec {
   int device = -1, num_sms = 148;
   ModelShape m;
@@ -50,7 +52,7 @@ struct Exec {
   float* shrink_ws = nullptr;  // split-K partials of the LoRA shrink
   bf16* Vt = nullptr;  // V^T [KV*hd][vt_ld] (tcgen05 attention, hd = 128)
   int vt_ld = 0;
-  std::map<int, AttnParams> attn_cache;  // per prompt length
+  std::map<std::pair<int, int>, AttnParams> attn_cache;  // per (rows, prompts)
   // pinned host staging
   int32_t* h_tok = nullptr;
   float* h_logits = nullptr;
@@ -58,7 +60,7 @@ struct Exec {
   // fork pointer table
   std::vector<void*> wptr;
   // cache: (S, lora_rank, mask, adapter arena base) -> per-layer params
-  std::map<std::tuple<int, int, uint32_t, const void*, uint64_t>, std::vector<LayerLaunch>> cache;
+  std::map<std::tuple<int, int, int, uint32_t, const void*, uint64_t>, std::vector<LayerLaunch>> cache;
   int launches = 0;
   // per-kernel-class timing (TIDAL_DEBUG_PROFILE): event pairs on the compute
   // stream around every launch, plus each launch's algorithmic flops/bytes
@@ -82,9 +84,9 @@ struct Exec {
   void init(int device, const ModelShape& m, float eps, float theta, int world, int rank,
             int max_tokens);
   void destroy();
-  const std::vector<LayerLaunch>& layer_params(const TensorTable& tt, int S, const void* akey,
-                                               uint64_t gen);
-  cudaError_t attention_tc(int S, cudaStream_t s);
+  const std::vector<LayerLaunch>& layer_params(const TensorTable& tt, int S, int nseq,
+                                               const void* akey, uint64_t gen);
+  cudaError_t attention_tc(int S, int nseq, cudaStream_t s);
 };
 
 enum KernelClass {
@@ -112,7 +114,7 @@ struct Comm {
   int world = 1, rank = 0, device = 0;
   virtual ~Comm() {}
   virtual void allreduce_f32(float* buf, size_t n, cudaStream_t s) = 0;
-  virtual void max_u64(unsigned long long* key, cudaStream_t s) = 0;
+  virtual void max_u64(unsigned long long* key, size_t n, cudaStream_t s) = 0;
   virtual void allgather_f32(float* buf, size_t n, cudaStream_t s) = 0;
 };
 
@@ -123,7 +125,8 @@ struct RunArgs {
   const std::vector<cudaEvent_t>* events = nullptr;         // per group
   const std::vector<int>* copy_pos = nullptr;               // position of each group in the copy stream
   int skip_group = -1;                                       // fault injection
-  int S = 0;
+  int S = 0;     // total rows: nseq prompts of S / nseq tokens each
+  int nseq = 1;
   float lora_scale = 1.f;
   const void* akey = nullptr;
   uint64_t gen = 0;

@@ -98,6 +98,8 @@ SIGNATURES = [
     ("tidal_adapter_destroy", None, [VP]),
     ("tidal_plan_dump", C.c_int, [VP, VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("tidal_invoke_prefill", C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.POINTER(Stats)]),
+    ("tidal_invoke_prefill_batch", C.c_int,
+     [VP, VP, VP, C.c_int, C.c_int, VP, VP, C.POINTER(Stats)]),
     ("tidal_host_alloc", C.c_int, [C.c_uint64, C.POINTER(VP)]),
     ("tidal_host_free", None, [VP]),
     ("tidal_comm_unique_id", C.c_int, [VP]),
@@ -272,6 +274,22 @@ class Template:
                                           len(tok), logits.ctypes.data if want_logits else None,
                                           C.addressof(t), C.byref(st)))
         return t.value, logits, st.as_dict()
+
+    def invoke_batch(self, tokens: np.ndarray, adapter: Optional["Adapter"] = None,
+                     want_logits: bool = True) -> Tuple[np.ndarray, Optional[np.ndarray], dict]:
+        """tokens [n_seqs, seq_len] -> (first tokens [n_seqs], logits [n_seqs, vocab], stats)."""
+        tok = np.ascontiguousarray(tokens, dtype=np.int32)
+        if tok.ndim != 2:
+            raise ValueError("tokens must be [n_seqs, seq_len]")
+        B, S = tok.shape
+        logits = np.empty((B, self.vocab), np.float32) if want_logits else None
+        out = np.empty(B, np.int32)
+        st = Stats()
+        _check(lib().tidal_invoke_prefill_batch(self.h, adapter.h if adapter else None,
+                                                tok.ctypes.data, B, S,
+                                                logits.ctypes.data if want_logits else None,
+                                                out.ctypes.data, C.byref(st)))
+        return out, logits, st.as_dict()
 
     def set_debug(self, flags: int, arg: int = -1) -> None:
         _check(lib().tidal_set_debug(self.h, flags, arg))

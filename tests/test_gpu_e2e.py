@@ -226,3 +226,30 @@ def test_load_order_ablation_correct(T, order):
     tok = synth.prompt(cfg, 24, 6)
     a = rig.adapter(8, 3)
     check(rig.tpl.invoke(tok, a), F.forward(cfg, rig.w, tok, F.synth_adapter(cfg, 8, 3), 0x7F, 1.0))
+
+
+@pytest.mark.parametrize("cfg,B,Ls,rho,rank", [
+    (synth.config("tiny"), 3, 100, 0.5, 8),                                   # hd 64 (mma.sync)
+    (synth.ModelConfig("gqa128", 2, 512, 4, 2, 1376, 2048, rope_theta=500000.0), 4, 130, 0.4, 16),
+    (synth.ModelConfig("gqa128", 2, 512, 4, 2, 1376, 2048, rope_theta=500000.0), 2, 256, 0.0, 0),
+])
+def test_batch_prompts_match_oracle(T, cfg, B, Ls, rho, rank):
+    """Batched prefill (§7.2, Fig. ttft-bs): B prompts of one length in
+    one invocation, weights streamed once; each prompt's first token and logits
+    equal the oracle run on that prompt alone."""
+    rig = Rig(T, cfg, seed=8, budget=rho, max_tokens=B * Ls)
+    rig.tpl.set_debug(T.DEBUG_POISON)
+    toks = np.stack([synth.prompt(cfg, Ls, 40 + b) for b in range(B)])
+    a = rig.adapter(rank, 5) if rank else None
+    aw = F.synth_adapter(cfg, rank, 5) if rank else None
+    c0 = rig.tpl.checksum()
+    out, logits, st = rig.tpl.invoke_batch(toks, a)
+    assert out.shape == (B,) and logits.shape == (B, cfg.vocab)
+    for b in range(B):
+        ref = F.forward(cfg, rig.w, toks[b], aw, 0x7F if rank else 0, 1.0)
+        check((int(out[b]), logits[b], None), ref)
+    assert rig.tpl.checksum() == c0
+    # one-prompt batch == the plain invoke, bit for bit
+    t1, l1, _ = rig.tpl.invoke(toks[1], a)
+    o1, lb, _ = rig.tpl.invoke_batch(toks[1:2], a)
+    assert int(o1[0]) == t1 and np.array_equal(lb[0], l1)

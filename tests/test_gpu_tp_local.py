@@ -129,3 +129,20 @@ def test_tp_keep_alive_and_resize(T):
     run_ranks(world, lambda k: ranks[k].tpl.resize(T.template_opts(resident_bytes=T.U64_MAX, device=0,
                                                                    comm=ranks[k].comm)))
     check_all(run_ranks(world, lambda k: ranks[k].tpl.invoke(tok)), F.forward(cfg, w, tok))
+
+
+def test_tp_batch(T):
+    """Batched prompts under TP: logits come back [B][V] from the [world][B][V/world]
+    device layout, per-prompt argmax max-reduced across ranks."""
+    cfg = synth.ModelConfig("gqa128", 2, 512, 4, 2, 1376, 2048, rope_theta=500000.0)
+    world, seed, B, Ls = 2, 12, 3, 150
+    group = f"tp-batch-{next(_uid)}"
+    ranks = run_ranks(world, lambda k: Rank(T, cfg, world, k, group, 0.3, seed, 0))
+    ads = [rk.adapter(8, 4, 0x7F, 1.0) for rk in ranks]
+    toks = np.stack([synth.prompt(cfg, Ls, 60 + b) for b in range(B)])
+    res = run_ranks(world, lambda k: ranks[k].tpl.invoke_batch(toks, ads[k]))
+    w = F.synth_weights(cfg, seed)
+    aw = F.synth_adapter(cfg, 8, 4)
+    for b in range(B):
+        ref = F.forward(cfg, w, toks[b], aw, 0x7F, 1.0)
+        check_all([(int(o[b]), l[b], s) for o, l, s in res], ref)
