@@ -6,6 +6,7 @@
 #include <atomic>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <map>
@@ -930,6 +931,8 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
                           const void* const* B, int r, const void* rope, int head_dim) {
   TIDAL_TRY
   const int cg_req = (epi >> 20) & 0x3;  // bits 20-21: CTA group (0 = auto)
+  const int mc_req = (epi >> 22) & 0x3;  // bits 22-23: CTA pairs per cluster (0 = auto)
+  const int ks_req = (epi >> 24) & 0xF;  // bits 24-27: EPI_RESID split-K parts (0 = auto)
   const int bn_req = (epi >> 8) & 0x1FF;  // bits 8-16: N tile (0 = auto)
   epi &= 0xFF;
   require(epi >= 0 && epi <= 3 && nseg >= 1 && nseg <= 3, "bad gemm arguments");
@@ -941,12 +944,31 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
   if (epi == EPI_ROPE && p.bn == 192) p.bn = 256;
   p.cg = cg_req ? cg_req : gemm_pick_cg(M);
   require(p.cg == 1 || p.cg == 2, "cg must be 1 or 2");
-  const int bbox = gemm_b_box(epi, p.bn, p.cg), tbbox = gemm_tb_box(epi, p.bn, p.cg);
+  p.mc = mc_req ? mc_req : (p.cg == 2 ? gemm_pick_mc(M, sms()) : 1);
+  require(p.mc == 1 || (p.mc == 2 && p.cg == 2), "mc must be 1, or 2 with cg 2");
+  if (epi == EPI_RESID) {
+    int bn_auto = 256, ks = 1;
+    gemm_plan_resid(M, seg_n[0], K, sms(), &bn_auto, &ks);
+    if (ks_req) ks = ks_req;
+    const int nk = (K + GEMM_BK - 1) / GEMM_BK;
+    require(ks >= 1 && ks <= nk, "bad split-K");
+    p.kblocks_per_split = (nk + ks - 1) / ks;
+    p.ksplit = (nk + p.kblocks_per_split - 1) / p.kblocks_per_split;  // parts non-empty
+    if (!bn_req) p.bn = bn_auto;
+    static int* flags = nullptr;  // per process; this entry is synchronous
+    if (!flags) {
+      cudaError_t e = cudaMalloc(&flags, GEMM_MAX_FLAGS * sizeof(int));
+      if (e == cudaSuccess) e = cudaMemset(flags, 0, GEMM_MAX_FLAGS * sizeof(int));
+      if (e != cudaSuccess) return sync_status(e, "gemm flags");
+    }
+    p.flags = flags;
+  }
+  const int bbox = gemm_b_box(epi, p.bn, p.cg, p.mc), tbbox = gemm_tb_box(epi, p.bn, p.cg, p.mc);
   auto mk = [&](CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols, uint32_t box) {
     require(make_tmap(m, base, rows, cols, cols * 2, box, 64), "tensor map encode failed");
   };
   mk(&p.a, A, M, K, 128);
-  const int mt = (M + GEMM_BM * p.cg - 1) / (GEMM_BM * p.cg);
+  const int mt = gemm_m_tiles(M, p.cg, p.mc);
   p.M = M;
   p.K = K;
   p.m_tiles = mt;
@@ -956,8 +978,8 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
   p.head_dim = head_dim;
   p.lora_r = (T && B) ? r : 0;
   if (epi == EPI_SILU) {
-    mk(&p.b[0], W[0], seg_n[0], K, 128);
-    mk(&p.b[1], W[1], seg_n[0], K, 128);
+    mk(&p.b[0], W[0], seg_n[0], K, bbox);
+    mk(&p.b[1], W[1], seg_n[0], K, bbox);
     if (p.lora_r) {
       mk(&p.ta[0], T[0], M, r, 128);
       mk(&p.ta[1], T[1], M, r, 128);
@@ -987,7 +1009,12 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
       p.total_tiles += p.n_tiles[s] * mt;
     }
   }
-  cudaError_t e = gemm_launch(p, epi, sms(), 0);
+  // TIDAL_K_REPEAT=n launches the same GEMM n times back to back (timing
+  // harness tools/gemm_bench.py; epilogues that accumulate keep accumulating)
+  const char* rep = getenv("TIDAL_K_REPEAT");
+  const int reps = rep ? atoi(rep) : 1;
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < (reps > 0 ? reps : 1) && e == cudaSuccess; ++i) e = gemm_launch(p, epi, sms(), 0);
   tidal_status s = sync_status(e, "gemm");
   if (s != TIDAL_OK) return s;
   TIDAL_CATCH

@@ -2,20 +2,24 @@
 //   O_h = softmax(Q_h K_g^T / sqrt(hd) + causal) V_g,   g = h / (H / KV)
 // CTA = 128 queries of one head; warp-specialised like the GEMM:
 //   warp 0      TMA: Q once, then K / V^T tiles of 128 keys (separate rings:
-//               K_j is released as soon as S_j is computed)
+//               K_j is released as soon as S_j is computed, V_j after PV_j)
 //   warp 1      tcgen05.mma: S_j = Q K_j^T into TMEM (double-buffered, so
 //               S_{j+1} runs while softmax works on S_j), then O += P_j V_j
+//               with P_j read straight from TMEM (the "TS" MMA form)
 //   warps 2..9  softmax in two column halves: warps 2..5 own keys 0..63 and
 //               warps 6..9 keys 64..127 of the same 128 query rows (TMEM lane
 //               = row; both halves share a lane quarter), exchanging row
-//               maxima through shared memory; P = exp2(S*scale - m) rounded
-//               to bf16 into a SWIZZLE_128B smem tile (each half writes one
-//               K-block of the PV MMA's A operand); fp32 running row sums.
-//               O lives in TMEM for the whole CTA; it is rescaled (each half
-//               its 64 columns) only when a row max grows by more than 2^8
-//               (exact: O and l share the same stale max, P <= 256).
+//               maxima through shared memory; P = 2^(S*scale - m) rounded to
+//               bf16 and stored to TMEM (tcgen05.st, double-buffered: softmax
+//               of tile j+1 writes P_{j+1} while the tensor core runs PV_j);
+//               fp32 running row sums.  O lives in TMEM for the whole CTA; it
+//               is rescaled (each half its 64 columns) only when a row max
+//               grows by more than 2^8 (exact: O and l share the same stale
+//               max, P <= 256).
 // V is consumed as V^T [hd][S] (written transposed by the QKV GEMM epilogue),
-// so both MMAs read K-major operands.
+// so the PV MMA's B operand is K-major in shared memory.
+// TMEM columns: S_0 [0,128), S_1 [128,256), O [256,384), P_0 [384,448),
+// P_1 [448,512) (P: 128 keys as 64 packed bf16x2 columns).
 #include <cuda.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
@@ -32,17 +36,16 @@ namespace {
 constexpr int HD = 128, BQ = 128, BKV = 128;
 constexpr int TILE = 128 * 128 * 2;  // 32 KB: any 128 x 128 bf16 tile (two 64-wide K-blocks)
 constexpr int HALF = TILE / 2;
-constexpr int KST = 2, VST = 2;
-constexpr int OFF_Q = 0, OFF_K = OFF_Q + TILE, OFF_V = OFF_K + KST * TILE,
-              OFF_P = OFF_V + VST * TILE;
-constexpr int OFF_RED = OFF_P + TILE;                // [2 slots][2 halves][128] row maxima
+constexpr int KST = 2, VST = 3;
+constexpr int OFF_Q = 0, OFF_K = OFF_Q + TILE, OFF_V = OFF_K + KST * TILE;
+constexpr int OFF_RED = OFF_V + VST * TILE;          // [2 slots][2 halves][128] row maxima
 constexpr int OFF_BAR = OFF_RED + 2 * 2 * BQ * 4;
-constexpr int N_BARS = 3 + 2 * KST + 2 * VST + 2;
+constexpr int N_BARS = 1 + 2 * KST + 2 * VST + 2 + 2 + 2;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM = OFF_TMEM + 16 + 1024;
 constexpr int NSOFT = 256;           // softmax threads
 constexpr int NTH = 64 + NSOFT;
-constexpr uint32_t COL_S0 = 0, COL_O = 256;
+constexpr uint32_t COL_S0 = 0, COL_O = 256, COL_P = 384;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
@@ -51,20 +54,24 @@ __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
 __device__ __forceinline__ void softmax_bar() {  // the 8 softmax warps only
   asm volatile("bar.sync 1, %0;" ::"n"(NSOFT) : "memory");
 }
-
 __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) &
-                                             ~uintptr_t(1023));
+  // 1024-B aligned (SWIZZLE_128B); offsetting smem_raw keeps the shared state
+  // space visible to the compiler (STS/LDS, not generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sb = ptx::smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const uint32_t bars = sb + OFF_BAR;
-  const uint32_t q_full = bars, p_full = bars + 8, pv_done = bars + 16;
-  auto k_full = [&](int s) { return bars + 24 + 8u * s; };
-  auto k_empty = [&](int s) { return bars + 24 + 8u * (KST + s); };
-  auto v_full = [&](int s) { return bars + 24 + 8u * (2 * KST + s); };
-  auto v_empty = [&](int s) { return bars + 24 + 8u * (2 * KST + VST + s); };
-  auto s_full = [&](int s) { return bars + 24 + 8u * (2 * KST + 2 * VST + s); };
+  const uint32_t q_full = bars;
+  auto k_full = [&](int s) { return bars + 8u * (1 + s); };
+  auto k_empty = [&](int s) { return bars + 8u * (1 + KST + s); };
+  auto v_full = [&](int s) { return bars + 8u * (1 + 2 * KST + s); };
+  auto v_empty = [&](int s) { return bars + 8u * (1 + 2 * KST + VST + s); };
+  auto s_full = [&](int b) { return bars + 8u * (1 + 2 * KST + 2 * VST + b); };
+  // per-P-buffer barriers: softmax runs up to one tile ahead of the PV MMAs, so
+  // a single barrier could complete two phases before its waiter looks
+  auto p_full = [&](int b) { return bars + 8u * (3 + 2 * KST + 2 * VST + b); };
+  auto pv_done = [&](int b) { return bars + 8u * (5 + 2 * KST + 2 * VST + b); };
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
 
   const int nq = (p.S + BQ - 1) / BQ;
@@ -80,8 +87,6 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     ptx::prefetch_tmap(&p.q);
     ptx::prefetch_tmap(&p.vt);
     ptx::mbar_init(q_full, 1);
-    ptx::mbar_init(p_full, NSOFT);
-    ptx::mbar_init(pv_done, 1);
     for (int s = 0; s < KST; ++s) {
       ptx::mbar_init(k_full(s), 1);
       ptx::mbar_init(k_empty(s), 1);
@@ -90,7 +95,11 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       ptx::mbar_init(v_full(s), 1);
       ptx::mbar_init(v_empty(s), 1);
     }
-    for (int s = 0; s < 2; ++s) ptx::mbar_init(s_full(s), 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(s_full(b), 1);
+      ptx::mbar_init(p_full(b), NSOFT);
+      ptx::mbar_init(pv_done(b), 1);
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
@@ -106,8 +115,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       ptx::mbar_expect_tx(q_full, TILE);
       ptx::tma_load_2d(&p.q, sb + OFF_Q, q_full, qc, base + q0);
       ptx::tma_load_2d(&p.q, sb + OFF_Q + HALF, q_full, qc + 64, base + q0);
-      // in-order issue K_0 V_0 K_1 V_1 ...: V_j's slot frees (PV_{j-2}) before
-      // K_{j+1}'s (S_{j-1}), so the single producer never waits needlessly
+      // in-order issue K_0 V_0 K_1 V_1 ...
       for (int j = 0; j < nkv; ++j) {
         const int s = j % KST, t = j % VST;
         ptx::mbar_wait(k_empty(s), ((j / KST) & 1) ^ 1);
@@ -144,20 +152,22 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       };
       issue_s(0);
       for (int j = 0; j < nkv; ++j) {
+        // S_{j+1} overwrites S buffer (j+1)&1, last read by softmax j-1 (it
+        // arrived on p_full(j-1), which this thread observed last iteration)
         if (j + 1 < nkv) issue_s(j + 1);
-        const int t = j % VST;
-        ptx::mbar_wait(p_full, j & 1);
+        const int t = j % VST, b = j & 1;
+        ptx::mbar_wait(p_full(b), (j >> 1) & 1);
         ptx::mbar_wait(v_full(t), (j / VST) & 1);
         ptx::tc_fence_after();
         const uint32_t vs = sb + OFF_V + t * TILE;
 #pragma unroll
         for (int kk = 0; kk < BKV / 16; ++kk) {
           const uint32_t off = (kk >> 2) * HALF;
-          ptx::mma_bf16(tmem + COL_O, ptx::desc_sw128(sb + OFF_P + off) + 2 * (kk & 3),
-                        ptx::desc_sw128(vs + off) + 2 * (kk & 3), IDESC, (j | kk) != 0);
+          ptx::mma_bf16_ts(tmem + COL_O, tmem + COL_P + b * 64 + kk * 8,
+                           ptx::desc_sw128(vs + off) + 2 * (kk & 3), IDESC, (j | kk) != 0);
         }
         ptx::mma_commit(v_empty(t));
-        ptx::mma_commit(pv_done);
+        ptx::mma_commit(pv_done(b));
       }
     }
     __syncwarp();
@@ -169,16 +179,16 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     const int qi = q0 + row;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     float* red = reinterpret_cast<float*>(smem + OFF_RED);  // [slot][half][row]
-    uint8_t* Ps = smem + OFF_P + half * HALF;               // this half's K-block of P
     const uint32_t o_col = tmem + lane_base + COL_O + half * 64;
     float m_used = -INFINITY, l = 0.f;
     for (int j = 0; j < nkv; ++j) {
-      ptx::mbar_wait(s_full(j & 1), (j >> 1) & 1);
+      const int b = j & 1;
+      ptx::mbar_wait(s_full(b), (j >> 1) & 1);
       ptx::tc_fence_after();
       float v[64];
       {
         uint32_t r0[32], r1[32];
-        const uint32_t sc = tmem + lane_base + COL_S0 + (j & 1) * 128 + half * 64;
+        const uint32_t sc = tmem + lane_base + COL_S0 + b * 128 + half * 64;
         ptx::tmem_ld32(sc, r0);
         ptx::tmem_ld32(sc + 32, r1);
         ptx::tmem_ld_wait();
@@ -202,16 +212,17 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       float mraw = fmaxf(fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3])),
                          fmaxf(fmaxf(mr[4], mr[5]), fmaxf(mr[6], mr[7])));
       // exchange the half-row maxima (double-buffered slot: no WAR hazard)
-      float* slot = red + (j & 1) * 2 * BQ;
+      float* slot = red + b * 2 * BQ;
       slot[half * BQ + row] = mraw;
       softmax_bar();
       mraw = fmaxf(mraw, slot[(half ^ 1) * BQ + row]);
       const float mx = fmaxf(m_used, mraw * p.scale_log2);  // scale > 0: max commutes
       const bool need = mx > m_used + 8.f;                  // identical in both halves
-      if (j > 0) ptx::mbar_wait(pv_done, (j - 1) & 1);    // P free, O settled
       if (j > 0 && __any_sync(0xffffffffu, need)) {
+        // O settled: PV_{j-1} (and so every earlier PV) has completed
+        ptx::mbar_wait(pv_done((j - 1) & 1), ((j - 1) >> 1) & 1);
         ptx::tc_fence_after();
-        const float corr = need ? exp2f(m_used - mx) : 1.f;
+        const float corr = need ? ptx::ex2(m_used - mx) : 1.f;
 #pragma unroll 1
         for (int c = 0; c < 2; ++c) {
           uint32_t r[32];
@@ -225,27 +236,30 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         l *= corr;
       }
       if (need) m_used = mx;
-      // P = exp2(s*scale - m) -> bf16 into this half's SWIZZLE_128B K-block
+      // P buffer b was last read by PV_{j-2}
+      if (j >= 2) ptx::mbar_wait(pv_done(b), ((j - 2) >> 1) & 1);
+      // P = 2^(s*scale - m) -> packed bf16 pairs, 32 TMEM columns per half
       float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent sum chains
+      uint32_t pk[32];
 #pragma unroll
       for (int c = 0; c < 8; ++c) {
         float e[8];
 #pragma unroll
         for (int i = 0; i < 8; ++i) {
-          e[i] = exp2f(fmaf(v[c * 8 + i], p.scale_log2, -m_used));
+          e[i] = ptx::ex2(fmaf(v[c * 8 + i], p.scale_log2, -m_used));
           ls[i] += e[i];
         }
-        uint4 w;
-        w.x = pack_bf16x2(e[0], e[1]);
-        w.y = pack_bf16x2(e[2], e[3]);
-        w.z = pack_bf16x2(e[4], e[5]);
-        w.w = pack_bf16x2(e[6], e[7]);
-        *reinterpret_cast<uint4*>(Ps + row * 128 + ((c ^ (row & 7)) << 4)) = w;
+        pk[4 * c + 0] = pack_bf16x2(e[0], e[1]);
+        pk[4 * c + 1] = pack_bf16x2(e[2], e[3]);
+        pk[4 * c + 2] = pack_bf16x2(e[4], e[5]);
+        pk[4 * c + 3] = pack_bf16x2(e[6], e[7]);
       }
+      ptx::tc_fence_after();
+      ptx::tmem_st32(tmem + lane_base + COL_P + b * 64 + half * 32, pk);
       l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
-      ptx::fence_proxy_async_smem();
+      ptx::tmem_st_wait();
       ptx::tc_fence_before();
-      ptx::mbar_arrive(p_full);
+      ptx::mbar_arrive(p_full(b));
     }
     // epilogue: combine the half-row sums, O / l -> bf16 (each half its 64 columns)
     float* lsum = red;  // reuse slot 0 after a barrier (all maxima consumed)
@@ -253,7 +267,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     lsum[half * BQ + row] = l;
     softmax_bar();
     const float inv = 1.f / (l + lsum[(half ^ 1) * BQ + row]);
-    ptx::mbar_wait(pv_done, (nkv - 1) & 1);
+    ptx::mbar_wait(pv_done((nkv - 1) & 1), ((nkv - 1) >> 1) & 1);
     ptx::tc_fence_after();
     bf16* out = p.out + (size_t)(base + qi) * p.ldo + h * HD + half * 64;
 #pragma unroll 1

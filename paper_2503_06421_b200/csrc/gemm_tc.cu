@@ -19,6 +19,7 @@
 
 #include <cstdio>
 #include <cstring>
+#include <cstdlib>
 #include <mutex>
 
 #include "kernels.h"
@@ -30,20 +31,37 @@ namespace tidal {
 
 namespace {
 
-constexpr int BM = GEMM_BM, BN = GEMM_BN, BK = GEMM_BK, STAGES = GEMM_STAGES;
+constexpr int BM = GEMM_BM, BN = GEMM_BN, BK = GEMM_BK;
 constexpr int A_BYTES = BM * BK * 2;          // 16 KB
-constexpr int B_BYTES = BN * BK * 2;          // 32 KB (stage slot; a CTA uses <= this)
 constexpr int ROW_BYTES = BK * 2;             // one 64-element K row = 128 B
 constexpr int STG_ROW = 144;                  // staging row stride (bytes)
 constexpr int STG_WARP = 32 * STG_ROW;
-constexpr int OFF_A = 0;
-constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
-constexpr int OFF_STG = OFF_B + STAGES * B_BYTES;
-constexpr int OFF_BAR = OFF_STG + 4 * STG_WARP;
-constexpr int N_BARS = 2 * STAGES + 4;
-constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
-constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;   // + alignment slack
+constexpr int SMEM_LIMIT = 227 * 1024;        // max dynamic shared memory per CTA
 constexpr int TMEM_COLS = 512;
+
+// Shared-memory layout of one instantiation: a stage holds this CTA's A box
+// (128 rows) and its B rows (BNX / CG), so the ring is as deep as 227 KB
+// allows (4..8 stages): a CTA-pair 256 x 192 tile streams 28 KB per K-block
+// and gets 7 stages (~1.6 us of L2/DRAM latency cover at full MMA rate).
+template <int EPI, int BNT, int CG>
+struct Cfg {
+  static constexpr int BNX = EPI == EPI_SILU ? 256 : BNT;  // MMA N = accumulator columns
+  static constexpr int BROWS = BNX / CG;                   // B rows staged by this CTA
+  static constexpr int BBYTES = BROWS * ROW_BYTES;
+  static constexpr int STAGE = A_BYTES + BBYTES;
+  static constexpr int FIXED = 4 * STG_WARP + 16 * 8 + 8 * 4 + 16 + 1024;
+  static constexpr int ST_RAW = (SMEM_LIMIT - FIXED) / STAGE;
+  static constexpr int STAGES = ST_RAW > 8 ? 8 : ST_RAW;
+  static constexpr int OFF_A = 0;
+  static constexpr int OFF_B = OFF_A + STAGES * A_BYTES;
+  static constexpr int OFF_STG = OFF_B + STAGES * BBYTES;
+  static constexpr int OFF_BAR = OFF_STG + 4 * STG_WARP;
+  static constexpr int N_BARS = 2 * STAGES + 4;
+  static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
+  static constexpr int SMEM_BYTES = OFF_TMEM + 16 + 1024;  // + alignment slack
+  static_assert(STAGES >= 4 && SMEM_BYTES <= SMEM_LIMIT, "GEMM shared-memory layout");
+  static_assert(BBYTES % 1024 == 0, "SWIZZLE_128B stage alignment");
+};
 constexpr int NTHREADS = 192;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -86,7 +104,16 @@ __device__ __forceinline__ void store_chunk_bf16(const float (&v)[32], uint8_t* 
   __syncwarp();
 }
 
-// out[m, col + j] += v[j]  (fp32 residual), coalesced through staging.
+__device__ __forceinline__ void red_add_f32x4(float* dst, float4 a) {
+  asm volatile("red.global.add.v4.f32 [%0], {%1, %2, %3, %4};" ::"l"(dst), "f"(a.x), "f"(a.y),
+               "f"(a.z), "f"(a.w)
+               : "memory");
+}
+
+// out[m, col + j] += v[j]  (fp32 residual), coalesced through staging, as
+// L2 reductions (red.global.add.v4.f32): no load round trip in the epilogue.
+// One writer per element at a time (split-K parts are ordered by flags), so
+// the sum order is fixed and the result deterministic.
 __device__ __forceinline__ void add_chunk_f32(const float (&v)[32], uint8_t* stg, int lane,
                                               float* out, int ldo, int row0, int M, int col,
                                               int nvalid) {
@@ -95,35 +122,19 @@ __device__ __forceinline__ void add_chunk_f32(const float (&v)[32], uint8_t* stg
   for (int k = 0; k < 8; ++k) st[k] = make_float4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
   __syncwarp();
   const int ch = lane & 7, c = ch * 4;
-  if (c + 4 <= nvalid) {
-    // issue all 8 residual loads before any store (one memory latency per chunk)
-    float4 x[8];
 #pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int m = row0 + it * 4 + (lane >> 3);
-      if (m < M) x[it] = __ldcg(reinterpret_cast<const float4*>(out + (size_t)m * ldo + col + c));
-    }
-#pragma unroll
-    for (int it = 0; it < 8; ++it) {
-      const int r = it * 4 + (lane >> 3);
-      const int m = row0 + r;
-      if (m < M) {
-        const float4 a = *reinterpret_cast<const float4*>(stg + r * STG_ROW + ch * 16);
-        x[it].x += a.x;
-        x[it].y += a.y;
-        x[it].z += a.z;
-        x[it].w += a.w;
-        *reinterpret_cast<float4*>(out + (size_t)m * ldo + col + c) = x[it];
-      }
-    }
-  } else if (c < nvalid) {
-    for (int it = 0; it < 8; ++it) {
-      const int r = it * 4 + (lane >> 3);
-      const int m = row0 + r;
-      if (m >= M) continue;
-      const float* s = reinterpret_cast<const float*>(stg + r * STG_ROW + ch * 16);
+  for (int it = 0; it < 8; ++it) {
+    const int r = it * 4 + (lane >> 3);
+    const int m = row0 + r;
+    if (m < M && c < nvalid) {
+      const float4 a = *reinterpret_cast<const float4*>(stg + r * STG_ROW + ch * 16);
       float* dst = out + (size_t)m * ldo + col + c;
-      for (int e = 0; e < nvalid - c; ++e) dst[e] += s[e];
+      if (c + 4 <= nvalid) {
+        red_add_f32x4(dst, a);
+      } else {
+        const float* sa = reinterpret_cast<const float*>(&a);
+        for (int e = 0; e < nvalid - c; ++e) atomicAdd(dst + e, sa[e]);
+      }
     }
   }
   __syncwarp();
@@ -167,7 +178,7 @@ __device__ __forceinline__ void ld_chunk(uint32_t taddr, float (&v)[32]) {
 // tile -> (segment, first output column within the segment, first row of the
 // cluster tile).  Cluster tiles are n-major so concurrently running tiles share
 // the same weight panel (read from HBM once, then from L2).
-template <int EPI, int BNT, int CG>
+template <int EPI, int BNT, int CG, int MC>
 __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& seg, int& n0,
                                             int& m0) {
   if (EPI == EPI_PARTIAL) {  // tile = ks * m_tiles + m
@@ -177,7 +188,7 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
     return;
   }
   int gn = tile / p.m_tiles;
-  m0 = (tile - gn * p.m_tiles) * (BM * CG);
+  m0 = (tile - gn * p.m_tiles) * (BM * CG * MC);  // cluster tile: MC pairs stacked in M
   seg = 0;
   while (seg < p.nseg - 1 && gn >= p.n_tiles[seg]) {
     gn -= p.n_tiles[seg];
@@ -186,20 +197,79 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
   n0 = gn * (EPI == EPI_SILU ? 128 : BNT);
 }
 
-template <int EPI, int BNT, int CG>
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+// One unit of persistent work: a tile, or (EPI_RESID split-K) one K range of
+// a tile.  Work w = split * total_tiles + tile, so every split-s part of a
+// tile is scheduled after its split-(s-1) part on any CTA (no circular wait).
+struct Work {
+  int seg, n0, m0;  // m0: first row of this CTA pair
+  int kb0, kb1;     // main-loop K blocks [kb0, kb1)
+  int lora;         // LoRA K-extension blocks follow (last split only)
+  int split, tile;
+};
+
+template <int EPI, int BNT, int CG, int MC>
+__device__ __forceinline__ Work decode_work(const GemmParams& p, int w, int pr, int nk,
+                                            int nlora) {
+  Work r;
+  if (EPI == EPI_PARTIAL) {  // w = ks * m_tiles + m
+    r.seg = 0;
+    r.n0 = 0;
+    r.m0 = (w % p.m_tiles) * BM;
+    r.kb0 = (w / p.m_tiles) * p.kblocks_per_split;
+    r.kb1 = min(nk, r.kb0 + p.kblocks_per_split);
+    r.lora = 0;
+    r.split = 0;
+    r.tile = w;
+    return r;
+  }
+  const int ks = EPI == EPI_RESID && p.ksplit > 1 ? p.ksplit : 1;
+  r.split = ks > 1 ? w / p.total_tiles : 0;
+  r.tile = w - r.split * p.total_tiles;
+  decode_tile<EPI, BNT, CG, MC>(p, r.tile, r.seg, r.n0, r.m0);
+  r.m0 += pr * BM * CG;
+  const int kps = ks > 1 ? p.kblocks_per_split : nk;
+  r.kb0 = r.split * kps;
+  r.kb1 = min(nk, r.kb0 + kps);
+  r.lora = (nlora > 0 && p.seg[r.seg].lora && r.split == ks - 1) ? nlora : 0;
+  return r;
+}
+
+__device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps of this CTA
+  asm volatile("bar.sync 2, 128;" ::: "memory");
+}
+
+template <int EPI, int BNT, int CG, int MC>
 __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_constant__ GemmParams p) {
-  constexpr int BNX = EPI == EPI_SILU ? 256 : BNT;  // MMA N = accumulator columns
-  constexpr int BROWS = BNX / CG;                   // B rows staged by this CTA
-  constexpr int BBYTES = BROWS * ROW_BYTES;
+  static_assert(MC == 1 || CG == 2, "multicast clusters are built from CTA pairs");
+  using C = Cfg<EPI, BNT, CG>;
+  constexpr int BNX = C::BNX, BROWS = C::BROWS, BBYTES = C::BBYTES, STAGES = C::STAGES;
+  constexpr int OFF_A = C::OFF_A, OFF_B = C::OFF_B, OFF_STG = C::OFF_STG, OFF_BAR = C::OFF_BAR,
+                OFF_TMEM = C::OFF_TMEM;
   constexpr int SILU_LORA_ROWS = 128 / CG;          // per-CTA rows of a gate/up LoRA-B box
   extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>(
-      (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1024-B aligned (SWIZZLE_128B); offsetting smem_raw keeps the shared state
+  // space visible to the compiler (STS/LDS, not generic ST/LD)
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
   const uint32_t sbase = ptx::smem_u32(smem);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int rank = CG == 2 ? (int)ptx::cluster_rank() : 0;
-  const int unit = CG == 2 ? (int)blockIdx.x >> 1 : (int)blockIdx.x;
-  const int nunits = CG == 2 ? (int)gridDim.x >> 1 : (int)gridDim.x;
+  // cluster = MC CTA pairs (ranks 2p, 2p+1) stacked along M: they share every
+  // B (weight) box, each CTA loading 1/MC of it and multicasting to the
+  // same-rank CTA of every pair, so L2->SM operand traffic per MAC drops
+  const int crank = CG == 2 ? (int)ptx::cluster_rank() : 0;
+  const int rank = crank & 1;   // CTA within its pair
+  const int pr = crank >> 1;    // pair within the cluster
+  const int unit = (int)blockIdx.x / (CG * MC);
+  const int nunits = (int)gridDim.x / (CG * MC);
+  const uint16_t mc_mask = (uint16_t)((1u << rank) | (1u << (2 + rank)));
   const uint32_t bar0 = sbase + OFF_BAR;
   auto full_bar = [&](int s) { return bar0 + 8u * s; };
   auto empty_bar = [&](int s) { return bar0 + 8u * (STAGES + s); };
@@ -209,6 +279,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
 
   const int nk = (p.K + BK - 1) / BK;
   const int nlora = p.lora_r > 0 ? (EPI == EPI_SILU ? 2 : 1) : 0;
+  const int nwork = EPI == EPI_RESID && p.ksplit > 1 ? p.total_tiles * p.ksplit : p.total_tiles;
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&p.a);
@@ -216,7 +287,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       if (i < p.nseg || (EPI == EPI_SILU && i < 2)) ptx::prefetch_tmap(&p.b[i]);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full_bar(s), CG);  // leader expect_tx + peer arrive
-      ptx::mbar_init(empty_bar(s), 1);
+      ptx::mbar_init(empty_bar(s), MC);  // one MMA commit per pair of the cluster
     }
     for (int a = 0; a < 2; ++a) {
       ptx::mbar_init(tfull_bar(a), 1);
@@ -248,27 +319,32 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
         else
           ptx::tma_load_2d(m, dst, fb, c0, c1);
       };
+      // B-side box of `rows` rows at (c0, r0) into dst: with MC pairs, this CTA
+      // loads its 1/MC slice and multicasts it to the same-rank CTA of each pair
+      auto tmab = [&](const CUtensorMap* m, uint32_t dst, uint32_t fb, int c0, int r0, int rows) {
+        if (MC == 1) {
+          tma(m, dst, fb, c0, r0);
+        } else {
+          const int part = rows / MC;
+          ptx::tma_load_2d_pair_mc(m, dst + pr * part * ROW_BYTES, fb, c0, r0 + pr * part, mc_mask);
+        }
+      };
       int stage = 0;
       uint32_t phase = 0;
-      for (int tile = unit; tile < p.total_tiles; tile += nunits) {
-        int seg, n0, m0;
-        decode_tile<EPI, BNT, CG>(p, tile, seg, n0, m0);
-        const int ma = m0 + rank * BM;  // this CTA's A rows
-        const bool lora = nlora > 0 && p.seg[seg].lora;
-        int kb0 = 0, nkb = nk + (lora ? nlora : 0);
-        if (EPI == EPI_PARTIAL) {
-          kb0 = (tile / p.m_tiles) * p.kblocks_per_split;
-          nkb = min(nk, kb0 + p.kblocks_per_split);
-        }
-        for (int kb = kb0; kb < nkb; ++kb) {
+      for (int w = unit; w < nwork; w += nunits) {
+        const Work wk = decode_work<EPI, BNT, CG, MC>(p, w, pr, nk, nlora);
+        const int seg = wk.seg, n0 = wk.n0;
+        const int ma = wk.m0 + rank * BM;  // this CTA's A rows
+        const int nkb = wk.kb1 + wk.lora;
+        for (int kb = wk.kb0; kb < nkb; ++kb) {
           ptx::mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + OFF_A + stage * A_BYTES;
-          const uint32_t sb = sbase + OFF_B + stage * B_BYTES;
+          const uint32_t sb = sbase + OFF_B + stage * BBYTES;
           const uint32_t fb = full_bar(stage);
           int bytes;  // this CTA's bytes for the stage
           if (EPI == EPI_PARTIAL) {
             bytes = A_BYTES + p.nseg * p.src_rows * ROW_BYTES;
-          } else if (kb < nk) {
+          } else if (kb < wk.kb1) {
             bytes = A_BYTES + BBYTES;
           } else {
             bytes = A_BYTES + (EPI == EPI_SILU ? SILU_LORA_ROWS : BROWS) * ROW_BYTES;
@@ -281,25 +357,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
             tma(&p.a, sa, fb, kb * BK, ma);
             for (int s = 0; s < p.nseg; ++s)
               tma(&p.b[s], sb + s * p.src_rows * ROW_BYTES, fb, kb * BK, 0);
-          } else if (kb < nk) {
+          } else if (kb < wk.kb1) {
             tma(&p.a, sa, fb, kb * BK, ma);
             if (EPI == EPI_SILU) {
               if (CG == 2) {
-                tma(&p.b[rank], sb, fb, kb * BK, n0);  // rank 0: gate rows, rank 1: up rows
+                tmab(&p.b[rank], sb, fb, kb * BK, n0, 128);  // rank 0: gate rows, rank 1: up rows
               } else {
                 tma(&p.b[0], sb, fb, kb * BK, n0);
                 tma(&p.b[1], sb + 128 * ROW_BYTES, fb, kb * BK, n0);
               }
             } else {
-              tma(&p.b[seg], sb, fb, kb * BK, n0 + rank * BROWS);
+              tmab(&p.b[seg], sb, fb, kb * BK, n0 + rank * BROWS, BROWS);
             }
           } else {
-            const int j = kb - nk;  // LoRA stage: EPI_SILU j=0 gate, j=1 up
+            const int j = kb - wk.kb1;  // LoRA stage: EPI_SILU j=0 gate, j=1 up
             tma(&p.ta[EPI == EPI_SILU ? j : seg], sa, fb, 0, ma);
             if (EPI == EPI_SILU)
-              tma(&p.tb[j], sb, fb, 0, n0 + rank * SILU_LORA_ROWS);
+              tmab(&p.tb[j], sb, fb, 0, n0 + rank * SILU_LORA_ROWS, SILU_LORA_ROWS);
             else
-              tma(&p.tb[seg], sb, fb, 0, n0 + rank * BROWS);
+              tmab(&p.tb[seg], sb, fb, 0, n0 + rank * BROWS, BROWS);
           }
           if (++stage == STAGES) {
             stage = 0;
@@ -321,25 +397,25 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
         else
           ptx::mma_bf16(d, a, b, id, acc);
       };
-      auto commit = [&](uint32_t bar) {
+      auto commit = [&](uint32_t bar) {  // this pair's two CTAs
         if (CG == 2)
-          ptx::mma_commit_pair(bar);
+          ptx::mma_commit_mask(bar, (uint16_t)(3u << (2 * pr)));
         else
           ptx::mma_commit(bar);
+      };
+      auto commit_stage = [&](uint32_t bar) {  // a stage slot is shared by all pairs
+        if (MC == 2)
+          ptx::mma_commit_mask(bar, (uint16_t)0xF);
+        else
+          commit(bar);
       };
       int stage = 0;
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int tile = unit; tile < p.total_tiles; tile += nunits) {
-        int seg, n0, m0;
-        decode_tile<EPI, BNT, CG>(p, tile, seg, n0, m0);
-        const bool lora = nlora > 0 && p.seg[seg].lora;
-        int kb0 = 0, nkb = nk + (lora ? nlora : 0);
-        if (EPI == EPI_PARTIAL) {
-          kb0 = (tile / p.m_tiles) * p.kblocks_per_split;
-          nkb = min(nk, kb0 + p.kblocks_per_split);
-        }
+      for (int w = unit; w < nwork; w += nunits) {
+        const Work wk = decode_work<EPI, BNT, CG, MC>(p, w, pr, nk, nlora);
+        const int kb0 = wk.kb0, nkb = wk.kb1 + wk.lora;
         ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BNX;
@@ -347,19 +423,19 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           ptx::mbar_wait(full_bar(stage), phase);
           ptx::tc_fence_after();
           const uint64_t adesc = ptx::desc_sw128(sbase + OFF_A + stage * A_BYTES);
-          const uint64_t bdesc = ptx::desc_sw128(sbase + OFF_B + stage * B_BYTES);
-          if (EPI == EPI_PARTIAL || kb < nk) {
+          const uint64_t bdesc = ptx::desc_sw128(sbase + OFF_B + stage * BBYTES);
+          if (EPI == EPI_PARTIAL || kb < wk.kb1) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, ((kb - kb0) | k) != 0);
           } else if (EPI == EPI_SILU) {
-            const int j = kb - nk;
+            const int j = kb - wk.kb1;
             for (int k = 0; k < nmma_lora; ++k)
               mma(d_tmem + j * 128, adesc + 2 * k, bdesc + 2 * k, IDESC_HALF, 1);
           } else {
             for (int k = 0; k < nmma_lora; ++k) mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, 1);
           }
-          commit(empty_bar(stage));
+          commit_stage(empty_bar(stage));
           if (++stage == STAGES) {
             stage = 0;
             phase ^= 1;
@@ -379,10 +455,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     uint8_t* stg = smem + OFF_STG + (warp - 2) * STG_WARP;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int tile = unit; tile < p.total_tiles; tile += nunits) {
-      int seg, n0, m0;
-      decode_tile<EPI, BNT, CG>(p, tile, seg, n0, m0);
-      const GemmSeg sg = p.seg[seg];
+    for (int wi = unit; wi < nwork; wi += nunits) {
+      const Work wk = decode_work<EPI, BNT, CG, MC>(p, wi, pr, nk, nlora);
+      const int tile = wk.tile, n0 = wk.n0, m0 = wk.m0;
+      const GemmSeg sg = p.seg[wk.seg];
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
       ptx::tc_fence_after();
       const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNX;
@@ -408,19 +484,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const float g = v[i];
-            v[i] = g / (1.0f + __expf(-g)) * w[i];
+            v[i] = g * ptx::rcp(1.0f + ptx::ex2(-1.4426950408889634f * g)) * w[i];
           }
           store_chunk_bf16(v, stg, lane, reinterpret_cast<bf16*>(p.out), p.ldo, row0, p.M,
                            sg.out_col + n0 + j * 32, ncols - j * 32);
         }
       } else if (EPI == EPI_RESID) {
         const int ncols = min(BNT, sg.n - n0);
+        const int ks = p.ksplit > 1 ? p.ksplit : 1;
+        int* flag = ks > 1 ? p.flags + (tile * MC + pr) * CG + rank : nullptr;
+        if (ks > 1 && wk.split > 0) {
+          // split s adds after split s-1 of this tile half has landed
+          if (threadIdx.x == 64) {
+            uint32_t n = 0;
+            while (ld_acquire(flag) != wk.split)
+              if (++n == (1u << 30)) __trap();
+          }
+          epi_bar();
+        }
 #pragma unroll 1
         for (int j = 0; j < BNT / 32; ++j) {
           if (j * 32 >= ncols) break;
           ld_chunk(tacc + j * 32, v);
           add_chunk_f32(v, stg, lane, reinterpret_cast<float*>(p.out), p.ldo, row0, p.M,
                         sg.out_col + n0 + j * 32, ncols - j * 32);
+        }
+        if (ks > 1) {
+          __threadfence();  // this thread's reductions are performed before the flag
+          epi_bar();
+          if (threadIdx.x == 64) st_release(flag, wk.split + 1 < ks ? wk.split + 1 : 0);
         }
       } else if (EPI == EPI_ROPE && sg.rope) {
         const int hd = p.head_dim, half = hd >> 1;
@@ -511,23 +603,26 @@ typedef CUresult (*EncodeTiledFn)(CUtensorMap*, CUtensorMapDataType, cuuint32_t,
 EncodeTiledFn g_encode = nullptr;
 std::once_flag g_once;
 
-template <int EPI, int BNT, int CG>
+template <int EPI, int BNT, int CG, int MC = 1>
 cudaError_t launch_t(const GemmParams& p, int num_sms, cudaStream_t s) {
   static bool attr_done = false;
   if (!attr_done) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI, BNT, CG>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_BYTES);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tc_kernel<EPI, BNT, CG, MC>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         Cfg<EPI, BNT, CG>::SMEM_BYTES);
     if (e != cudaSuccess) return e;
     attr_done = true;
   }
-  const int units = num_sms / CG;
-  const int grid = (p.total_tiles < units ? p.total_tiles : units) * CG;
+  const int units = gemm_units(CG, MC, num_sms);
+  const int grid = (p.total_tiles < units ? p.total_tiles : units) * CG * MC;
   if (grid <= 0) return cudaSuccess;
-  return launch_k(gemm_tc_kernel<EPI, BNT, CG>, dim3(grid), dim3(NTHREADS), SMEM_BYTES, s, CG, p);
+  return launch_k(gemm_tc_kernel<EPI, BNT, CG, MC>, dim3(grid), dim3(NTHREADS),
+                  Cfg<EPI, BNT, CG>::SMEM_BYTES, s, CG * MC, p);
 }
 
 template <int EPI, int BNT>
 cudaError_t launch_cg(const GemmParams& p, int num_sms, cudaStream_t s) {
+  if (p.cg == 2 && p.mc == 2) return launch_t<EPI, BNT, 2, 2>(p, num_sms, s);
   if (p.cg == 2) return launch_t<EPI, BNT, 2>(p, num_sms, s);
   return launch_t<EPI, BNT, 1>(p, num_sms, s);
 }
@@ -536,11 +631,55 @@ cudaError_t launch_cg(const GemmParams& p, int num_sms, cudaStream_t s) {
 
 int gemm_pick_cg(int M) { return M > GEMM_BM ? 2 : 1; }
 
+// Concurrently resident clusters of cg * mc CTAs (one CTA per SM): a
+// persistent grid larger than this would serialise whole clusters.
+int gemm_units(int cg, int mc, int num_sms) {
+  if (mc == 1) return num_sms / cg;
+  static int cached = -1;
+  if (cached < 0) {
+    int n = 0;
+    auto k = gemm_tc_kernel<EPI_RESID, 192, 2, 2>;
+    constexpr int smem = Cfg<EPI_RESID, 192, 2>::SMEM_BYTES;
+    cudaLaunchConfig_t cfg = {};
+    cudaLaunchAttribute attr;
+    attr.id = cudaLaunchAttributeClusterDimension;
+    attr.val.clusterDim.x = 4;
+    attr.val.clusterDim.y = 1;
+    attr.val.clusterDim.z = 1;
+    cfg.gridDim = dim3(num_sms / 4 * 4);
+    cfg.blockDim = dim3(NTHREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.attrs = &attr;
+    cfg.numAttrs = 1;
+    if (cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess ||
+        cudaOccupancyMaxActiveClusters(&n, k, &cfg) != cudaSuccess)
+      n = 0;
+    cudaGetLastError();
+    cached = n;
+  }
+  return cached;
+}
+
+// Two CTA pairs per cluster sharing the weight boxes (TMA multicast): opt-in
+// (TIDAL_GEMM_MC=2).  Measured at the 13B shapes it cuts L2->SM sectors by
+// 20-25% but only 33 four-CTA clusters are co-resident (132 of 148 SMs), and
+// per-SM tensor activity did not rise, so the pair-only grid is faster.
+int gemm_pick_mc(int M, int num_sms) {
+  static const bool on = [] {
+    const char* e = getenv("TIDAL_GEMM_MC");
+    return e && e[0] == '2';
+  }();
+  if (!on || gemm_pick_cg(M) != 2 || M <= 2 * GEMM_BM) return 1;
+  return gemm_units(2, 2, num_sms) > 0 ? 2 : 1;
+}
+
+int gemm_m_tiles(int M, int cg, int mc) { return (M + BM * cg * mc - 1) / (BM * cg * mc); }
+
 int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms) {
   if (epi == EPI_SILU) return 128;
-  const int cg = gemm_pick_cg(M);
-  const int mt = (M + BM * cg - 1) / (BM * cg);
-  const int units = num_sms / cg;
+  const int cg = gemm_pick_cg(M), mc = gemm_pick_mc(M, num_sms);
+  const int mt = gemm_m_tiles(M, cg, mc);
+  const int units = gemm_units(cg, mc, num_sms);
   static const int cands[] = {256, 192, 128};
   int best = 256;
   double best_cost = 1e30;
@@ -559,8 +698,45 @@ int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms) {
   return best;
 }
 
-int gemm_b_box(int epi, int bn, int cg) { return epi == EPI_SILU ? 128 : bn / cg; }
-int gemm_tb_box(int epi, int bn, int cg) { return epi == EPI_SILU ? 128 / cg : bn / cg; }
+// Residual (row-parallel) GEMMs are short in N (d_model) and often few waves
+// deep: choose the N-tile width and an ordered split-K jointly to minimise
+// rounds x (K-blocks per part + per-part overhead) x shared-memory bytes per
+// K-block.  The per-part overhead (epilogue reductions, flag hand-off) was
+// measured at ~11 K-blocks (tools/gemm_bench.py, 13B O/down shapes), so at
+// S = 2048 one part wins and splitting pays only for short prompts.
+void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out) {
+  const int cg = gemm_pick_cg(M), mc = gemm_pick_mc(M, num_sms);
+  const long mt = gemm_m_tiles(M, cg, mc);
+  const long units = gemm_units(cg, mc, num_sms);
+  const int nk = (K + BK - 1) / BK;
+  static const int cands[] = {256, 192, 128};
+  double best = 1e30;
+  int bb = 256, bk = 1;
+  for (int bn : cands) {
+    const long tiles = mt * ((N + bn - 1) / bn);
+    if (tiles * mc * cg > GEMM_MAX_FLAGS) continue;
+    const double kb_bytes = A_BYTES + (double)(bn / cg) * ROW_BYTES;
+    for (int ks = 1; ks <= 8 && ks <= nk; ++ks) {
+      const int kps = (nk + ks - 1) / ks;
+      const int ks_eff = (nk + kps - 1) / kps;  // every part non-empty
+      if (ks_eff != ks) continue;
+      const long rounds = (tiles * ks + units - 1) / units;
+      const double cost = (double)rounds * (kps + 11) * kb_bytes;
+      if (cost < best * 0.98) {  // prefer fewer parts unless clearly better
+        best = cost;
+        bb = bn;
+        bk = ks;
+      }
+    }
+  }
+  *bn_out = bb;
+  *ks_out = bk;
+}
+
+int gemm_b_box(int epi, int bn, int cg, int mc) { return (epi == EPI_SILU ? 128 : bn / cg) / mc; }
+int gemm_tb_box(int epi, int bn, int cg, int mc) {
+  return (epi == EPI_SILU ? 128 / cg : bn / cg) / mc;
+}
 
 bool tma_init() {
   std::call_once(g_once, [] {

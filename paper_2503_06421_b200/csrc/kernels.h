@@ -57,13 +57,24 @@ struct alignas(64) GemmParams {
   int vt_ld;
   int ksplit, kblocks_per_split, src_rows;  // EPI_PARTIAL
   int cg;              // 1: single-CTA 128-row tiles; 2: CTA pair, 256-row tiles (cta_group::2)
+  int mc;              // cg == 2: CTA pairs per cluster sharing W boxes (1 or 2; 0 = 1)
+  int* flags;          // EPI_RESID with ksplit > 1: per (tile, CTA) split counters, all 0
+                       // between launches (GEMM_MAX_FLAGS ints); parts add in split order
 };
 
 // CTA-group size for an M-row GEMM, and the TMA box rows of the W and lora_B
 // maps a CTA loads for (epi, bn, cg).
 int gemm_pick_cg(int M);
-int gemm_b_box(int epi, int bn, int cg);
-int gemm_tb_box(int epi, int bn, int cg);
+// 2: clusters of two CTA pairs stacked in M sharing the W boxes by TMA multicast
+int gemm_pick_mc(int M, int num_sms);
+int gemm_units(int cg, int mc, int num_sms);  // resident clusters of cg * mc CTAs
+int gemm_m_tiles(int M, int cg, int mc);      // M tiles of 128 * cg * mc rows
+int gemm_b_box(int epi, int bn, int cg, int mc = 1);
+// EPI_RESID: N-tile width and ordered split-K parts (GemmParams::ksplit and
+// kblocks_per_split = ceil(nk / ks)) for an M x N x K residual GEMM.
+constexpr int GEMM_MAX_FLAGS = 16384;
+void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn, int* ks);
+int gemm_tb_box(int epi, int bn, int cg, int mc = 1);
 
 // LoRA shrink on tensor cores: T_t = bf16(scale * X A_t^T) for nt targets
 // sharing X, as a split-K EPI_PARTIAL GEMM into ws plus a fixed-order reduce.

@@ -86,6 +86,17 @@ __device__ __forceinline__ void mma_bf16(uint32_t d_tmem, uint64_t adesc, uint64
       "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accum)
       : "memory");
 }
+// D[tmem] (+)= A[tmem] * B[smem]^T ("TS" form): A is M x K bf16 in TMEM, lane
+// = row, K packed two per 32-bit column (16 K = 8 columns per instruction).
+__device__ __forceinline__ void mma_bf16_ts(uint32_t d_tmem, uint32_t a_tmem, uint64_t bdesc,
+                                            uint32_t idesc, uint32_t accum) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n\t}" ::"r"(d_tmem),
+      "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(accum)
+      : "memory");
+}
 // Arrive on an mbarrier once every previously issued tcgen05 op of this thread is done.
 __device__ __forceinline__ void mma_commit(uint32_t bar) {
   asm volatile(
@@ -145,6 +156,21 @@ __host__ __device__ constexpr uint32_t idesc_bf16(int M, int N) {
 }
 
 __device__ __forceinline__ uint32_t elect_lane0() { return (threadIdx.x & 31) == 0; }
+
+// 2^x as ONE MUFU.EX2 (flush-to-zero).  exp2f() without fast-math wraps the
+// MUFU in a denormal-range check and two FMULs; softmax arguments are <= 0
+// and results below 2^-126 contribute nothing at bf16/fp32 accumulation.
+__device__ __forceinline__ float ex2(float x) {
+  float y;
+  asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+// 1/x as ONE MUFU.RCP (flush-to-zero), for epilogue activations.
+__device__ __forceinline__ float rcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
 
 // Programmatic dependent launch: wait until the previous kernel in the stream
 // has completed (no-op without the launch attribute), then let the next kernel

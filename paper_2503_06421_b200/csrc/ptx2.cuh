@@ -63,5 +63,27 @@ __device__ __forceinline__ void mma_commit_pair(uint32_t bar) {
       : "memory");
 }
 
+// 2-SM TMA multicast: the box lands at the same offset in every CTA of
+// ctamask; each destination's completion is counted on its own pair leader's
+// barrier (same offset).  Two CTA pairs of a 4-CTA cluster share one operand.
+__device__ __forceinline__ void tma_load_2d_pair_mc(const CUtensorMap* m, uint32_t dst,
+                                                    uint32_t local_bar, int c0, int c1,
+                                                    uint16_t ctamask) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.cta_group::2.shared::cluster.global.mbarrier::complete_tx::bytes"
+      ".multicast::cluster [%0], [%1, {%3, %4}], [%2], %5;" ::"r"(dst),
+      "l"(reinterpret_cast<uint64_t>(m)), "r"(local_bar & kPeerMask), "r"(c0), "r"(c1),
+      "h"(ctamask)
+      : "memory");
+}
+// arrive on the same barrier in every CTA of ctamask once prior MMAs complete
+__device__ __forceinline__ void mma_commit_mask(uint32_t bar, uint16_t ctamask) {
+  asm volatile(
+      "tcgen05.commit.cta_group::2.mbarrier::arrive::one.shared::cluster.multicast::cluster.b64"
+      " [%0], %1;" ::"r"(bar),
+      "h"(ctamask)
+      : "memory");
+}
+
 }  // namespace ptx
 }  // namespace tidal

@@ -61,6 +61,8 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   dalloc(key, 8 * kMaxBatch);
   dalloc(tok, S * 4);
   dalloc(shrink_ws, (size_t)SHRINK_MAX_SPLIT * S * 192 * 4);
+  dalloc(gemm_flags, GEMM_MAX_FLAGS * sizeof(int));
+  cuda_check(cudaMemset(gemm_flags, 0, GEMM_MAX_FLAGS * sizeof(int)), "memset flags");
   // V^T: batched prompts pad each sequence to 64 columns (<= 63 per prompt)
   vt_ld = (int)((S + 63) / 64 * 64 + 64 * (size_t)kMaxBatch);
   dalloc(Vt, nkv * (size_t)vt_ld * 2);
@@ -88,7 +90,7 @@ void Exec::destroy() {
   cudaSetDevice(device);
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
-  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws};
+  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws, gemm_flags};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int t = 0; t < kNumTargets; ++t)
@@ -117,8 +119,8 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
   const int nq = m.n_heads * hd / world, nkv = m.n_kv_heads * hd / world;
   const int F = m.d_ff / world;
   const int r = tt.lora_rank;
-  const int cg = gemm_pick_cg(S);
-  const int mt = (S + GEMM_BM * cg - 1) / (GEMM_BM * cg);
+  const int cg = gemm_pick_cg(S), mc = gemm_pick_mc(S, num_sms);
+  const int mt = gemm_m_tiles(S, cg, mc);
   std::vector<LayerLaunch> v(L);
   auto W = [&](int id) { return wptr[id]; };
   for (int l = 0; l < L; ++l) {
@@ -134,18 +136,19 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     q.total_tiles = 0;
     q.bn = gemm_pick_bn(EPI_ROPE, S, segn, 3, num_sms);
     q.cg = cg;
+    q.mc = mc;
     for (int s = 0; s < 3; ++s) {
       q.seg[s].n = segn[s];
       q.seg[s].out_col = col;
       q.seg[s].rope = s < 2;
       col += segn[s];
-      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, gemm_b_box(EPI_ROPE, q.bn, cg));
+      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, gemm_b_box(EPI_ROPE, q.bn, cg, mc));
       const int la = tt.lora_a[l][tg[s]];
       q.seg[s].lora = la >= 0;
       if (la >= 0) {
         q.lora_r = r;
         tmap(&q.ta[s], T[tg[s]], S, r, 128);
-        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, gemm_tb_box(EPI_ROPE, q.bn, cg));
+        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, gemm_tb_box(EPI_ROPE, q.bn, cg, mc));
       }
       q.n_tiles[s] = (segn[s] + q.bn - 1) / q.bn;
       q.total_tiles += q.n_tiles[s] * mt;
@@ -165,16 +168,21 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     // ---- O (+ residual) ----
     GemmParams& o = ll.o;
     memset(&o, 0, sizeof o);
-    o.bn = gemm_pick_bn(EPI_RESID, S, &d, 1, num_sms);
+    int ks = 1;
+    gemm_plan_resid(S, d, nq, num_sms, &o.bn, &ks);
+    o.ksplit = ks;
+    o.kblocks_per_split = ((nq + GEMM_BK - 1) / GEMM_BK + ks - 1) / ks;
+    o.flags = gemm_flags;
     o.cg = cg;
+    o.mc = mc;
     tmap(&o.a, O, S, nq, 128);
-    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, gemm_b_box(EPI_RESID, o.bn, cg));
+    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, gemm_b_box(EPI_RESID, o.bn, cg, mc));
     o.seg[0].n = d;
     o.seg[0].lora = tt.lora_a[l][T_O] >= 0;
     if (o.seg[0].lora) {
       o.lora_r = r;
       tmap(&o.ta[0], T[T_O], S, r, 128);
-      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, gemm_tb_box(EPI_RESID, o.bn, cg));
+      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, gemm_tb_box(EPI_RESID, o.bn, cg, mc));
     }
     o.nseg = 1;
     o.M = S;
@@ -188,20 +196,21 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     GemmParams& g = ll.gu;
     memset(&g, 0, sizeof g);
     tmap(&g.a, Xn, S, d, 128);
-    tmap(&g.b[0], W(tt.proj[l][T_GATE]), F, d, 128);
-    tmap(&g.b[1], W(tt.proj[l][T_UP]), F, d, 128);
+    tmap(&g.b[0], W(tt.proj[l][T_GATE]), F, d, gemm_b_box(EPI_SILU, 128, cg, mc));
+    tmap(&g.b[1], W(tt.proj[l][T_UP]), F, d, gemm_b_box(EPI_SILU, 128, cg, mc));
     g.seg[0].n = F;
     g.seg[0].lora = tt.lora_a[l][T_GATE] >= 0;
     if (g.seg[0].lora) {
       g.lora_r = r;
       tmap(&g.ta[0], T[T_GATE], S, r, 128);
       tmap(&g.ta[1], T[T_UP], S, r, 128);
-      tmap(&g.tb[0], W(tt.lora_b[l][T_GATE]), F, r, gemm_tb_box(EPI_SILU, 128, cg));
-      tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, gemm_tb_box(EPI_SILU, 128, cg));
+      tmap(&g.tb[0], W(tt.lora_b[l][T_GATE]), F, r, gemm_tb_box(EPI_SILU, 128, cg, mc));
+      tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, gemm_tb_box(EPI_SILU, 128, cg, mc));
     }
     g.nseg = 1;
     g.bn = 128;
     g.cg = cg;
+    g.mc = mc;
     g.M = S;
     g.K = d;
     g.m_tiles = mt;
@@ -212,16 +221,20 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     // ---- down (+ residual) ----
     GemmParams& dn = ll.down;
     memset(&dn, 0, sizeof dn);
-    dn.bn = gemm_pick_bn(EPI_RESID, S, &d, 1, num_sms);
+    gemm_plan_resid(S, d, F, num_sms, &dn.bn, &ks);
+    dn.ksplit = ks;
+    dn.kblocks_per_split = ((F + GEMM_BK - 1) / GEMM_BK + ks - 1) / ks;
+    dn.flags = gemm_flags;
     dn.cg = cg;
+    dn.mc = mc;
     tmap(&dn.a, Hb, S, F, 128);
-    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, gemm_b_box(EPI_RESID, dn.bn, cg));
+    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, gemm_b_box(EPI_RESID, dn.bn, cg, mc));
     dn.seg[0].n = d;
     dn.seg[0].lora = tt.lora_a[l][T_DOWN] >= 0;
     if (dn.seg[0].lora) {
       dn.lora_r = r;
       tmap(&dn.ta[0], T[T_DOWN], S, r, 128);
-      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, gemm_tb_box(EPI_RESID, dn.bn, cg));
+      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, gemm_tb_box(EPI_RESID, dn.bn, cg, mc));
     }
     dn.nseg = 1;
     dn.M = S;

@@ -50,6 +50,7 @@ struct Exec {
   int32_t* tok = nullptr;
   float2* rope = nullptr;
   float* shrink_ws = nullptr;  // split-K partials of the LoRA shrink
+  int* gemm_flags = nullptr;   // ordered split-K counters of the residual GEMMs (all 0 at rest)
   bf16* Vt = nullptr;  // V^T [KV*hd][vt_ld] (tcgen05 attention, hd = 128)
   int vt_ld = 0;
   std::map<std::pair<int, int>, AttnParams> attn_cache;  // per (rows, prompts)

@@ -95,6 +95,67 @@ def test_gemm_tile_widths(T, bn, epi, cg):
         assert np.abs(X.cpu().numpy() - (X0 + ref)).max() <= 2e-4 * np.abs(X0 + ref).max()
 
 
+@pytest.mark.parametrize("mc", [1, 2])
+@pytest.mark.parametrize("epi,bn", [(0, 128), (0, 192), (0, 256), (3, 192), (3, 256), (2, 128)])
+@pytest.mark.parametrize("M", [300, 700, 1100])
+def test_gemm_multicast_clusters(T, epi, bn, M, mc):
+    """CTA-pair tiles with and without 4-CTA clusters whose two pairs share the
+    W / lora_B boxes by TMA multicast (mc = 2): M spans 1-3 cluster tiles of
+    512 rows with ragged tails (the second pair of the last cluster partly or
+    wholly past M), ragged N, LoRA, for the store, residual and SiLU epilogues."""
+    rng = np.random.default_rng(M + bn + 10 * epi + mc)
+    epi_code = epi | (bn << 8) | (2 << 20) | (mc << 22)
+    K, r = 448, 16
+    N = 3 * bn - 64 if epi != 2 else 640 - 64
+    A = _bf(rng, (M, K))
+    if epi == 2:
+        Wg, Wu = _bf(rng, (N, K), 1 / math.sqrt(K)), _bf(rng, (N, K), 1 / math.sqrt(K))
+        Tg, Tu = _bf(rng, (M, r)), _bf(rng, (M, r))
+        Bg, Bu = _bf(rng, (N, r), 0.2), _bf(rng, (N, r), 0.2)
+        out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+        T.k_gemm(epi_code, _dev(A), [_dev(Wg), _dev(Wu)], [N], out, N, M, K,
+                 [_dev(Tg), _dev(Tu)], [_dev(Bg), _dev(Bu)], r)
+        _close_bf16(_host(out), F.silu(A @ Wg.T + Tg @ Bg.T) * (A @ Wu.T + Tu @ Bu.T))
+        return
+    W = _bf(rng, (N, K), 1 / math.sqrt(K))
+    Tm, B = _bf(rng, (M, r)), _bf(rng, (N, r), 0.3)
+    ref = A @ W.T + Tm @ B.T
+    if epi == 0:
+        out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+        T.k_gemm(epi_code, _dev(A), [_dev(W)], [N], out, N, M, K, [_dev(Tm)], [_dev(B)], r)
+        _close_bf16(_host(out), ref)
+    else:
+        X0 = rng.standard_normal((M, N)).astype(np.float32)
+        X = torch.from_numpy(X0.copy()).cuda()
+        T.k_gemm(epi_code, _dev(A), [_dev(W)], [N], X, N, M, K, [_dev(Tm)], [_dev(B)], r)
+        assert np.abs(X.cpu().numpy() - (X0 + ref)).max() <= 2e-4 * np.abs(X0 + ref).max()
+
+
+@pytest.mark.parametrize("cg,M", [(1, 100), (2, 260), (2, 777)])
+@pytest.mark.parametrize("ks", [1, 2, 3, 5])
+@pytest.mark.parametrize("bn", [192, 256])
+def test_gemm_residual_split_k(T, bn, ks, cg, M):
+    """Residual GEMM as ordered split-K parts (each K range adds its partial sum
+    into X after the previous part of the same tile, flags in split order),
+    LoRA on the last part only; repeated launches check the flags return to 0
+    and that the sum order is fixed (bit-identical results run to run)."""
+    rng = np.random.default_rng(bn + ks + M)
+    K, r = 1344, 16          # 21 K-blocks: ks = 2, 3, 5 give unequal last parts
+    N = 3 * bn - 64
+    epi_code = 3 | (bn << 8) | (cg << 20) | (ks << 24)
+    A, W = _bf(rng, (M, K)), _bf(rng, (N, K), 1 / math.sqrt(K))
+    Tm, B = _bf(rng, (M, r)), _bf(rng, (N, r), 0.3)
+    X0 = rng.standard_normal((M, N)).astype(np.float32)
+    ref = X0 + A @ W.T + Tm @ B.T
+    outs = []
+    for _ in range(2):
+        X = torch.from_numpy(X0.copy()).cuda()
+        T.k_gemm(epi_code, _dev(A), [_dev(W)], [N], X, N, M, K, [_dev(Tm)], [_dev(B)], r)
+        outs.append(X.cpu().numpy())
+    assert np.abs(outs[0] - ref).max() <= 2e-4 * np.abs(ref).max()
+    assert np.array_equal(outs[0], outs[1])
+
+
 @pytest.mark.parametrize("r", [8, 16, 64])
 def test_gemm_lora_k_extension(T, r):
     rng = np.random.default_rng(r)
