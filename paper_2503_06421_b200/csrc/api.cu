@@ -913,7 +913,11 @@ tidal_status tidal_k_attention_tc(const void* qkv, const void* vt, int vt_ld, vo
   memset(&p, 0, sizeof p);
   require(attn_tc_params(&p, (const bf16*)qkv, (const bf16*)vt, vt_ld, (bf16*)O, S, H, KV),
           "attention tensor maps");
-  tidal_status s = sync_status(attn_tc_launch(p, 0), "attention_tc");
+  const char* rep = getenv("TIDAL_K_REPEAT");  // timing harness: n launches back to back
+  const int reps = rep && atoi(rep) > 0 ? atoi(rep) : 1;
+  cudaError_t e = cudaSuccess;
+  for (int i = 0; i < reps && e == cudaSuccess; ++i) e = attn_tc_launch(p, 0);
+  tidal_status s = sync_status(e, "attention_tc");
   if (s != TIDAL_OK) return s;
   TIDAL_CATCH
 }

@@ -22,6 +22,8 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--S", type=int, default=2048)
 ap.add_argument("--lora", type=int, default=16)
+ap.add_argument("--resid-sweep", action="store_true",
+                help="O/down only: bn x split-K grid, 3 interleaved passes, median")
 args = ap.parse_args()
 M, r = args.S, args.lora
 d, F = 5120, 13824
@@ -64,6 +66,23 @@ def bench(name, epi, bn, cg, mc, N_list, K, flops, ks=0):
     print(f"{name:8s} bn={bn:3d} cg={cg} mc={mc} ks={ks}  {best * 1e3:8.1f} us  {flops / best / 1e9:7.0f} TF/s",
           flush=True)
 
+
+if args.resid_sweep:
+    import statistics
+    res = {}
+    for _ in range(3):
+        for name, N, K in (("o", d, d), ("down", d, F)):
+            for bn in (192, 256):
+                for ks in (1, 2, 3, 4):
+                    import io, contextlib
+                    buf = io.StringIO()
+                    with contextlib.redirect_stdout(buf):
+                        bench(name, 3, bn, 2, 1, [N], K, 2.0 * M * N * K, ks)
+                    us = float(buf.getvalue().split("us")[0].split()[-1])
+                    res.setdefault((name, bn, ks), []).append(us)
+    for k, v in sorted(res.items()):
+        print(k, "median us", round(statistics.median(v), 1), [round(x, 1) for x in v])
+    sys.exit(0)
 
 shapes = [
     ("qkv", 1, [d, d, d], d, [256]),
