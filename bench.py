@@ -365,6 +365,15 @@ def main():
         "sweep_ms": sweep,
         "clocks": clk.summary(),
         "eq1": {"t_warm_ms": t_warm, "b_h2d_GBps": b_h2d / 1e9},
+        # the compute-bound regime (fully template-resident, rho = 1): warm TTFT
+        # against the tensor roof at the burst and at the sustained (power-cap)
+        # measured bf16 peak; north_star's bar is frac >= 1/1.3
+        "compute_bound_rho1": {
+            "warm_ms": t_warm,
+            "t_tensor_burst_ms": flops / (P["bf16_tflops"] * 1e12) * 1e3,
+            "t_tensor_sustained_ms": flops / (P.get("bf16_tflops_sustained", P["bf16_tflops"]) * 1e12) * 1e3,
+            "frac_burst": flops / (P["bf16_tflops"] * 1e12) * 1e3 / t_warm,
+            "frac_sustained": flops / (P.get("bf16_tflops_sustained", P["bf16_tflops"]) * 1e12) * 1e3 / t_warm},
         "setup_s": setup_s,
         "first_token": s0["token"],
     }

@@ -795,8 +795,15 @@ __global__ void shrink_reduce_kernel(const float* __restrict__ ws, int ksplit, i
   ptx::pdl_begin();
   const int e = blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= M * RT) return;
+  // all parts' loads in flight at once, then summed in part order (deterministic)
+  float pv[SHRINK_MAX_SPLIT];
+#pragma unroll
+  for (int k = 0; k < SHRINK_MAX_SPLIT; ++k)
+    if (k < ksplit) pv[k] = __ldcs(ws + (size_t)k * M * RT + e);
   float s = 0.f;
-  for (int k = 0; k < ksplit; ++k) s += __ldcs(ws + (size_t)k * M * RT + e);
+#pragma unroll
+  for (int k = 0; k < SHRINK_MAX_SPLIT; ++k)
+    if (k < ksplit) s += pv[k];
   const int m = e / RT, c = e - m * RT, t = c / r;
   bf16* T = t == 0 ? T0 : (t == 1 ? T1 : T2);
   T[(size_t)m * r + (c - t * r)] = __float2bfloat16_rn(s * scale);

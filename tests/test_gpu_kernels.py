@@ -285,8 +285,12 @@ def test_embed_and_vocab_shard(T):
 
 
 @pytest.mark.parametrize("M,K,r", [(64, 256, 8), (300, 5120, 16), (77, 688, 64), (2048, 13824, 16),
-                                   (1, 64, 32)])
+                                   (1, 64, 32), (4096, 5120, 64), (20000, 256, 32),
+                                   (19000, 128, 16)])
 def test_lora_shrink(T, M, K, r):
+    """Split-K parts of a 128-row block reduced over DSMEM in part order
+    (cluster of <= 8 CTAs); past 148 row blocks one CTA takes the whole K and
+    walks several blocks (no reduction), for r a multiple of 32 or not."""
     rng = np.random.default_rng(K)
     X, A = _bf(rng, (M, K)), _bf(rng, (r, K), 1 / math.sqrt(K))
     out = torch.zeros(M, r, dtype=torch.bfloat16, device="cuda")
