@@ -215,6 +215,36 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tpl, const tidal_adapter
                                         float* host_logits_out, int32_t* host_tokens_out,
                                         tidal_stats* stats);
 
+/* ---- decode continuation (§7 l.831, 849-851) ----
+ * Greedy decoding after the first token.  tidal_template_enable_decode
+ * allocates a KV cache of (max_tokens + max_new_tokens) rows per layer on the
+ * template's device (K after RoPE and V, bf16, [L][rows][n_kv_heads*head_dim])
+ * and extends the RoPE table; from then on every single-prompt
+ * tidal_invoke_prefill also stores its K and V into the cache (from the QKV
+ * GEMM epilogue).  tidal_invoke_decode continues the most recent such prefill:
+ * it feeds the prefill's first token at position n_tokens and generates
+ * n_steps further tokens, each step a captured CUDA graph (embed, per layer
+ * LoRA shrinks + HBM-bound GEMVs with fused RMSNorm / RoPE / SiLU*mul /
+ * residual + attention over the cache, head + argmax) replayed without a host
+ * round trip.  All weights are read from the device (the prefill left the
+ * streamed ones in the arena), so a step is bound by model bytes / HBM
+ * bandwidth.  Outputs: tokens_out[n_steps] (token i generated by step i);
+ * logits_out (nullable) [n_steps][vocab] fp32.  Synchronous.
+ * Errors: TIDAL_ERR_INVALID when decode is not enabled, no single-prompt
+ * prefill preceded, the adapter differs from the prefill's, n_steps is out of
+ * [1, max_new_tokens], or the template is tensor-parallel (not implemented). */
+typedef struct {
+  double device_ms;                  /* all steps, CUDA events */
+  double per_token_ms;
+  uint64_t weight_bytes_per_token;   /* weights read per step (embedding: one row) */
+  uint64_t kv_bytes_last_token;      /* K and V read by the last step */
+  int n_kernels;                     /* kernels launched (graph nodes x steps + 1) */
+} tidal_decode_stats;
+tidal_status tidal_template_enable_decode(tidal_template* tpl, int max_new_tokens);
+tidal_status tidal_invoke_decode(tidal_template* tpl, const tidal_adapter* a, int n_steps,
+                                 int32_t* tokens_out, float* logits_out,
+                                 tidal_decode_stats* stats);
+
 /* ---- pinned host memory for adapters / pools (cudaHostAlloc) ---- */
 tidal_status tidal_host_alloc(uint64_t bytes, void** out);
 void tidal_host_free(void* p);

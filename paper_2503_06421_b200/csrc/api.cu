@@ -708,6 +708,10 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
   cuda_check(cudaEventRecord(tp->e_end, ex.compute), "event");
   cuda_check(cudaEventSynchronize(tp->e_end), "invoke");
   tp->suffix_valid = skip < 0;
+  // decode continuation: the cache now holds this prompt's K/V (single prompt)
+  ex.dec.prompt_len = (ex.dec.kc && n_seqs == 1) ? n_tokens : 0;
+  ex.dec.prompt_akey = ra.akey;
+  ex.dec.prompt_gen = tp->gen;
   if (ex.profile) ex.prof_collect();
   for (int b = 0; b < n_seqs; ++b)  // packed key: low word = ~token
     host_tokens_out[b] = (int32_t)(0xFFFFFFFFu - (uint32_t)(ex.h_key[b] & 0xFFFFFFFFu));
@@ -747,6 +751,75 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
     memcpy(&best, &bits, 4);
     if (key == 0 || std::isnan(best)) fail(TIDAL_ERR_NUMERIC, "NaN in logits (argmax undefined)");
   }
+  TIDAL_CATCH
+}
+
+tidal_status tidal_template_enable_decode(tidal_template* tp, int max_new_tokens) {
+  TIDAL_TRY
+  require(tp, "null template");
+  require(!tp->dry, "dry template cannot decode");
+  require(tp->world == 1, "decode with tensor parallelism is not implemented");
+  require(max_new_tokens >= 1 && max_new_tokens <= (1 << 20), "max_new_tokens out of range");
+  tp->ex.enable_decode(max_new_tokens);
+  TIDAL_CATCH
+}
+
+tidal_status tidal_invoke_decode(tidal_template* tp, const tidal_adapter* ca, int n_steps,
+                                 int32_t* tokens_out, float* logits_out,
+                                 tidal_decode_stats* stats) {
+  TIDAL_TRY
+  require(tp && tokens_out, "null argument");
+  require(!tp->dry, "dry template cannot decode");
+  Exec& ex = tp->ex;
+  require(ex.dec.kc != nullptr, "decode not enabled (tidal_template_enable_decode)");
+  require(ex.dec.prompt_len > 0, "decode must follow a single-prompt prefill");
+  require(tp->suffix_valid, "streamed weights are not all on the device");
+  auto* a = const_cast<tidal_adapter*>(ca);
+  if (a) require(a->tpl == tp, "adapter attached to another template");
+  const std::shared_ptr<AdapterPlan> hold = a ? a->ap : nullptr;
+  const TensorTable& tt = a ? hold->tt : tp->tt;
+  const void* akey = a ? (const void*)tp->arena : nullptr;
+  require(ex.dec.prompt_akey == akey && ex.dec.prompt_gen == tp->gen &&
+              (!a || a->ap->gen == tp->gen),
+          "decode must use the adapter of the preceding prefill");
+  require(n_steps >= 1 && n_steps <= ex.dec.max_new, "n_steps out of range (1..max_new_tokens)");
+  cuda_check(cudaSetDevice(tp->device), "cudaSetDevice");
+  ex.launches = 0;
+  cuda_check(cudaEventRecord(tp->e_start, ex.compute), "event");
+  run_decode(ex, tt, n_steps, a ? a->scale : 1.f, akey, tp->gen, logits_out != nullptr);
+  cuda_check(cudaEventRecord(tp->e_end, ex.compute), "event");
+  cuda_check(cudaMemcpyAsync(tokens_out, ex.dec.toks, 4ull * n_steps, cudaMemcpyDeviceToHost,
+                             ex.compute),
+             "D2H tokens");
+  if (logits_out)
+    cuda_check(cudaMemcpyAsync(logits_out, ex.dec.logits_all, 4ull * n_steps * tp->shape.vocab,
+                               cudaMemcpyDeviceToHost, ex.compute),
+               "D2H logits");
+  cuda_check(cudaStreamSynchronize(ex.compute), "decode");
+  if (stats) {
+    memset(stats, 0, sizeof *stats);
+    float ms = 0;
+    cudaEventElapsedTime(&ms, tp->e_start, tp->e_end);
+    stats->device_ms = ms;
+    stats->per_token_ms = ms / n_steps;
+    uint64_t wb = 0;
+    for (int id = 0; id < (int)tt.t.size(); ++id) {
+      const TensorInfo& ti = tt.t[id];
+      if (ti.role == R_EMBED && id != tt.head) {
+        wb += ti.bytes / std::max(1, ti.rows);  // one row gathered
+      } else if (!ti.adapter || tt.lora_rank) {
+        wb += ti.bytes;
+      }
+    }
+    stats->weight_bytes_per_token = wb;
+    const ModelShape& m = tp->shape;
+    stats->kv_bytes_last_token = 2ull * m.n_layers * (uint64_t)(ex.dec.prompt_len + n_steps) *
+                                 m.n_kv_heads * m.head_dim() * 2;
+    stats->n_kernels = ex.launches;
+  }
+  for (int i = 0; i < n_steps; ++i)
+    require(tokens_out[i] >= 0 && tokens_out[i] < tp->shape.vocab, "NaN in decode logits",
+            TIDAL_ERR_NUMERIC);
   TIDAL_CATCH
 }
 

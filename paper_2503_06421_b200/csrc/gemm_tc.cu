@@ -538,6 +538,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
             bf16* out = reinterpret_cast<bf16*>(p.out);
             store_chunk_bf16(v, stg, lane, out, p.ldo, row0, p.M, sg.out_col + n0 + c1, 32);
             store_chunk_bf16(w, stg, lane, out, p.ldo, row0, p.M, sg.out_col + n0 + c2, 32);
+            if (sg.out2) {
+              store_chunk_bf16(v, stg, lane, sg.out2, sg.ldo2, row0, p.M, n0 + c1, 32);
+              store_chunk_bf16(w, stg, lane, sg.out2, sg.ldo2, row0, p.M, n0 + c2, 32);
+            }
           }
         }
       } else {
@@ -548,6 +552,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           ld_chunk(tacc + j * 32, v);
           store_chunk_bf16(v, stg, lane, reinterpret_cast<bf16*>(p.out), p.ldo, row0, p.M,
                            sg.out_col + n0 + j * 32, ncols - j * 32);
+          if (EPI == EPI_ROPE && sg.out2)
+            store_chunk_bf16(v, stg, lane, sg.out2, sg.ldo2, row0, p.M, n0 + j * 32, ncols - j * 32);
           if (EPI == EPI_ROPE && sg.vt && m < p.M) {
             // V^T for the tcgen05 attention: lanes are consecutive tokens -> coalesced.
             // Batched prompts: sequence b's keys start at column b * round_up(seq_len, 64),

@@ -33,6 +33,8 @@ struct GemmSeg {
   int lora;     // LoRA K-extension present for this segment
   int rope;     // EPI_ROPE: rotate this segment
   int vt;       // EPI_ROPE: also store this segment transposed into GemmParams::vt
+  bf16* out2;   // EPI_ROPE (nullable): also store this segment row-major [M, n] (ld ldo2):
+  int ldo2;     //   the decode KV cache capturing K (after RoPE) and V during the prefill
 };
 
 struct alignas(64) GemmParams {
@@ -142,6 +144,65 @@ constexpr int HEAD_MAX_ROWS = 8;
 cudaError_t head_launch(const float* X_last, size_t x_stride, int nseq, const bf16* g, const bf16* W,
                         int V, int d, float eps, float* logits, int ldl, unsigned long long* key,
                         int vocab_offset, int num_sms, cudaStream_t s);
+// ------------------------------------------------------------------------
+// Decode continuation (decode.cu): one token per step, all HBM-bound GEMVs.
+// ------------------------------------------------------------------------
+struct DecodeState {           // device-resident, read by every kernel of a step
+  unsigned long long key;      // packed argmax of the last step (the next input token)
+  int step;                    // decode steps started
+  int pos;                     // position of the token fed in the current step
+  int pos0;                    // prompt length (position of the first decoded input)
+  int pad;
+};
+struct DecShrink {             // T_t[j] = scale * A_t[j, :] . x   (t < nt <= 3, j < r)
+  const bf16* A[3];
+  float* T[3];
+  int nt, r;
+};
+enum DecMode { DEC_QKV = 0, DEC_GU = 1, DEC_RESID = 2 };
+struct DecGemv {
+  // input: RMSNorm(X) * g (X fp32, g bf16) when X is set, else the bf16 vector xin
+  const float* X;
+  const bf16* g;
+  const bf16* xin;
+  float eps;
+  int K;                       // input length
+  int N;                       // output rows (DEC_RESID) / per-segment rows
+  int npairs;                  // row pairs (one per warp iteration)
+  const bf16* W[3];            // QKV: Wq, Wk, Wv; GU: Wgate, Wup; RESID: W
+  const bf16* B[3];            // LoRA B per segment [rows, r] (nullable)
+  const float* T[3];           // LoRA shrink outputs per segment (nullable)
+  int r;
+  // QKV
+  int nq, nkv, hd;
+  const float2* rope;          // [positions][hd/2] (cos, sin)
+  bf16* q;                     // [nq]
+  bf16 *kc, *vc;               // this layer's cache rows [cap][nkv]
+  const DecodeState* st;
+  // GU
+  bf16* h;                     // [F]
+  // RESID
+  float* Xout;                 // [N] += W . x
+};
+struct DecAttn {
+  const bf16* q;               // [H hd]
+  const bf16 *kc, *vc;         // this layer's cache [cap][ldkv]
+  int ldkv, H, KV, hd;
+  float scale_log2;
+  const DecodeState* st;       // keys 0 .. st->pos
+  float* part;                 // [H][chunks][2 + 128] partial (max, sum, o)
+  bf16* out;                   // [H hd]
+};
+cudaError_t dec_embed_launch(DecodeState* st, const bf16* E, float* X, int d, int32_t* toks_out,
+                             cudaStream_t s);
+cudaError_t dec_finish_launch(DecodeState* st, int32_t* toks_out, cudaStream_t s);
+cudaError_t dec_save_logits_launch(const DecodeState* st, const float* logits, float* all, int V,
+                                   cudaStream_t s);
+cudaError_t dec_shrink_launch(const DecShrink& a, const float* X, const bf16* g, const bf16* xin,
+                              int K, float eps, float scale, int num_sms, cudaStream_t s);
+cudaError_t dec_gemv_launch(const DecGemv& p, int mode, int num_sms, cudaStream_t s);
+cudaError_t dec_attn_launch(const DecAttn& a, int max_keys, cudaStream_t s);
+
 // Debug / invariants.
 cudaError_t poison_launch(void* p, size_t bytes, cudaStream_t s);           // bf16 NaN 0x7FC0
 cudaError_t checksum_launch(const void* p, size_t bytes, unsigned long long* out, cudaStream_t s);

@@ -67,17 +67,7 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   vt_ld = (int)((S + 63) / 64 * 64 + 64 * (size_t)kMaxBatch);
   dalloc(Vt, nkv * (size_t)vt_ld * 2);
   cuda_check(cudaMemset(Vt, 0, nkv * (size_t)vt_ld * 2), "memset V^T");  // padding stays finite
-  // RoPE table: angle = pos * theta^(-2i/hd), cos/sin in double, stored fp32
-  std::vector<float2> cs(S * (hd / 2));
-  for (size_t p = 0; p < S; ++p)
-    for (int i = 0; i < hd / 2; ++i) {
-      const double inv = std::pow((double)theta, -(2.0 * i) / hd);
-      const double ang = (double)p * inv;
-      cs[p * (hd / 2) + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
-    }
-  dalloc(rope, cs.size() * sizeof(float2));
-  cuda_check(cudaMemcpy(rope, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice),
-             "rope upload");
+  build_rope((int)S);
   cuda_check(cudaHostAlloc((void**)&h_tok, S * 4 + 16, cudaHostAllocDefault), "pinned tokens");
   cuda_check(cudaHostAlloc((void**)&h_logits, (size_t)kMaxBatch * m.vocab * 4 + 16,
                            cudaHostAllocDefault),
@@ -85,12 +75,64 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   cuda_check(cudaHostAlloc((void**)&h_key, 8 * kMaxBatch, cudaHostAllocDefault), "pinned key");
 }
 
+// RoPE table: angle = pos * theta^(-2i/hd), cos/sin in double, stored fp32
+void Exec::build_rope(int rows) {
+  const int hd = m.head_dim();
+  std::vector<float2> cs((size_t)rows * (hd / 2));
+  for (size_t p = 0; p < (size_t)rows; ++p)
+    for (int i = 0; i < hd / 2; ++i) {
+      const double inv = std::pow((double)theta, -(2.0 * i) / hd);
+      const double ang = (double)p * inv;
+      cs[p * (hd / 2) + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+    }
+  if (rope) cudaFree(rope);
+  rope = nullptr;
+  dalloc(rope, cs.size() * sizeof(float2));
+  cuda_check(cudaMemcpy(rope, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice),
+             "rope upload");
+}
+
+// KV cache [L][max_tokens + max_new][nkv] for K and V, decode scratch and the
+// RoPE table extended to the decoded positions.  Launch parameters are rebuilt
+// (the QKV epilogue now also stores K and V into the cache).
+void Exec::enable_decode(int max_new) {
+  if (world != 1) fail(1, "decode with tensor parallelism is not implemented");
+  if (max_new < 1) fail(1, "max_new_tokens must be >= 1");
+  cuda_check(cudaSetDevice(device), "cudaSetDevice");
+  cuda_check(cudaStreamSynchronize(compute), "sync");
+  Decode& D = dec;
+  void* ptrs[] = {D.kc, D.vc, D.q, D.att, D.h, D.T, D.part, D.st, D.toks, D.logits_all};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (D.gexec) cudaGraphExecDestroy(D.gexec);
+  D = Decode();
+  const int hd = m.head_dim();
+  const size_t nq = (size_t)m.n_heads * hd, nkv = (size_t)m.n_kv_heads * hd;
+  D.max_new = max_new;
+  D.cap = max_tokens + max_new;
+  dalloc(D.kc, (size_t)m.n_layers * D.cap * nkv * 2);
+  dalloc(D.vc, (size_t)m.n_layers * D.cap * nkv * 2);
+  dalloc(D.q, nq * 2);
+  dalloc(D.att, nq * 2);
+  dalloc(D.h, (size_t)m.d_ff * 2);
+  dalloc(D.T, 7 * 64 * 4);
+  dalloc(D.part, (size_t)m.n_heads * ((D.cap + 255) / 256) * 130 * 4);
+  dalloc(D.st, sizeof(DecodeState));
+  dalloc(D.toks, (size_t)max_new * 4);
+  dalloc(D.logits_all, (size_t)max_new * m.vocab * 4);
+  build_rope(D.cap);
+  cache.clear();
+}
+
 void Exec::destroy() {
   if (device < 0) return;
   cudaSetDevice(device);
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
-  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws, gemm_flags};
+  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws, gemm_flags,
+                  dec.kc, dec.vc, dec.q, dec.att, dec.h, dec.T, dec.part, dec.st, dec.toks,
+                  dec.logits_all};
+  if (dec.gexec) cudaGraphExecDestroy(dec.gexec);
   for (void* p : ptrs)
     if (p) cudaFree(p);
   for (int t = 0; t < kNumTargets; ++t)
@@ -155,6 +197,12 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     }
     q.nseg = 3;
     q.seg[2].vt = hd == 128;  // V^T for the tcgen05 attention
+    if (dec.kc && nseq == 1) {  // decode enabled: K (after RoPE) and V into the cache
+      q.seg[1].out2 = dec.kc + (size_t)l * dec.cap * nkv;
+      q.seg[1].ldo2 = nkv;
+      q.seg[2].out2 = dec.vc + (size_t)l * dec.cap * nkv;
+      q.seg[2].ldo2 = nkv;
+    }
     q.vt = Vt;
     q.vt_ld = vt_ld;
     q.M = S;
@@ -516,6 +564,182 @@ void run_forward(Exec& ex, const RunArgs& a) {
         break;
     }
   }
+}
+
+// ---------------- decode continuation ----------------
+// One step = embed, L x (shrink?, QKV, attention, shrink?, O, shrink?, GU,
+// shrink?, down), head (+ logits save): a fixed launch sequence over device
+// state, captured once per (adapter, scale, logits) as a CUDA graph.
+static void enqueue_decode_step(Exec& ex, const TensorTable& tt, float lora_scale,
+                                bool want_logits) {
+  const ModelShape& m = ex.m;
+  Exec::Decode& D = ex.dec;
+  cudaStream_t s = ex.compute;
+  const int L = m.n_layers, d = m.d_model, hd = m.head_dim(), F = m.d_ff;
+  const int nq = m.n_heads * hd, nkv = m.n_kv_heads * hd;
+  const int r = tt.lora_rank;
+  auto W = [&](int id) { return id >= 0 ? reinterpret_cast<const bf16*>(ex.wptr[id]) : nullptr; };
+  auto la = [&](int l, int t) { return r ? W(tt.lora_a[l][t]) : nullptr; };
+  auto lb = [&](int l, int t) { return r ? W(tt.lora_b[l][t]) : nullptr; };
+  float* T = D.T;  // [7][64]
+  auto Tp = [&](int t) { return T + 64 * t; };
+  cuda_check(dec_embed_launch(D.st, W(tt.embed), ex.X, d, D.toks, s), "dec_embed");
+  ++ex.launches;
+  auto shrink = [&](int l, std::initializer_list<int> ts, const float* X, const bf16* g,
+                    const bf16* xin, int K) {
+    DecShrink a;
+    memset(&a, 0, sizeof a);
+    for (int t : ts)
+      if (la(l, t)) {
+        a.A[a.nt] = la(l, t);
+        a.T[a.nt] = Tp(t);
+        ++a.nt;
+      }
+    if (!a.nt) return;
+    a.r = r;
+    cuda_check(dec_shrink_launch(a, X, g, xin, K, ex.eps, lora_scale, ex.num_sms, s), "dec_shrink");
+    ++ex.launches;
+  };
+  for (int l = 0; l < L; ++l) {
+    const bf16 *g1 = W(tt.norm1[l]), *g2 = W(tt.norm2[l]);
+    bf16* kc = D.kc + (size_t)l * D.cap * nkv;
+    bf16* vc = D.vc + (size_t)l * D.cap * nkv;
+    // ---- attention block ----
+    shrink(l, {T_Q, T_K, T_V}, ex.X, g1, nullptr, d);
+    DecGemv g;
+    memset(&g, 0, sizeof g);
+    g.X = ex.X;
+    g.g = g1;
+    g.eps = ex.eps;
+    g.K = d;
+    g.npairs = (nq + 2 * nkv) / 2;
+    const int tq[3] = {T_Q, T_K, T_V};
+    for (int i = 0; i < 3; ++i) {
+      g.W[i] = W(tt.proj[l][tq[i]]);
+      g.B[i] = lb(l, tq[i]);
+      g.T[i] = g.B[i] ? Tp(tq[i]) : nullptr;
+    }
+    g.r = r;
+    g.nq = nq;
+    g.nkv = nkv;
+    g.hd = hd;
+    g.rope = ex.rope;
+    g.q = D.q;
+    g.kc = kc;
+    g.vc = vc;
+    g.st = D.st;
+    cuda_check(dec_gemv_launch(g, DEC_QKV, ex.num_sms, s), "dec_qkv");
+    DecAttn at;
+    memset(&at, 0, sizeof at);
+    at.q = D.q;
+    at.kc = kc;
+    at.vc = vc;
+    at.ldkv = nkv;
+    at.H = m.n_heads;
+    at.KV = m.n_kv_heads;
+    at.hd = hd;
+    at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
+    at.st = D.st;
+    at.part = D.part;
+    at.out = D.att;
+    cuda_check(dec_attn_launch(at, D.cap, s), "dec_attn");
+    shrink(l, {T_O}, nullptr, nullptr, D.att, nq);
+    DecGemv o;
+    memset(&o, 0, sizeof o);
+    o.xin = D.att;
+    o.K = nq;
+    o.N = d;
+    o.npairs = (d + 1) / 2;
+    o.W[0] = W(tt.proj[l][T_O]);
+    o.B[0] = lb(l, T_O);
+    o.T[0] = o.B[0] ? Tp(T_O) : nullptr;
+    o.r = r;
+    o.Xout = ex.X;
+    cuda_check(dec_gemv_launch(o, DEC_RESID, ex.num_sms, s), "dec_o");
+    // ---- MLP block ----
+    shrink(l, {T_GATE, T_UP}, ex.X, g2, nullptr, d);
+    DecGemv gu;
+    memset(&gu, 0, sizeof gu);
+    gu.X = ex.X;
+    gu.g = g2;
+    gu.eps = ex.eps;
+    gu.K = d;
+    gu.npairs = F;
+    gu.W[0] = W(tt.proj[l][T_GATE]);
+    gu.W[1] = W(tt.proj[l][T_UP]);
+    gu.B[0] = lb(l, T_GATE);
+    gu.B[1] = lb(l, T_UP);
+    gu.T[0] = gu.B[0] ? Tp(T_GATE) : nullptr;
+    gu.T[1] = gu.B[1] ? Tp(T_UP) : nullptr;
+    gu.r = r;
+    gu.h = D.h;
+    cuda_check(dec_gemv_launch(gu, DEC_GU, ex.num_sms, s), "dec_gu");
+    shrink(l, {T_DOWN}, nullptr, nullptr, D.h, F);
+    DecGemv dn;
+    memset(&dn, 0, sizeof dn);
+    dn.xin = D.h;
+    dn.K = F;
+    dn.N = d;
+    dn.npairs = (d + 1) / 2;
+    dn.W[0] = W(tt.proj[l][T_DOWN]);
+    dn.B[0] = lb(l, T_DOWN);
+    dn.T[0] = dn.B[0] ? Tp(T_DOWN) : nullptr;
+    dn.r = r;
+    dn.Xout = ex.X;
+    cuda_check(dec_gemv_launch(dn, DEC_RESID, ex.num_sms, s), "dec_down");
+    ex.launches += 6;  // qkv, attention, combine, o, gu, down
+  }
+  cuda_check(head_launch(ex.X, 0, 1, W(tt.fnorm), W(tt.head), m.vocab, d, ex.eps, ex.logits,
+                         m.vocab, &D.st->key, 0, ex.num_sms, s),
+             "dec_head");
+  ++ex.launches;
+  if (want_logits) {
+    cuda_check(dec_save_logits_launch(D.st, ex.logits, D.logits_all, m.vocab, s), "dec_logits");
+    ++ex.launches;
+  }
+}
+
+void run_decode(Exec& ex, const TensorTable& tt, int n_steps, float lora_scale, const void* akey,
+                uint64_t gen, bool want_logits) {
+  Exec::Decode& D = ex.dec;
+  if (!D.kc) fail(1, "decode not enabled on this template (tidal_template_enable_decode)");
+  if (D.prompt_len <= 0) fail(1, "decode must follow a single-prompt prefill on this template");
+  if (D.prompt_akey != akey || D.prompt_gen != gen)
+    fail(1, "decode must use the adapter (and template state) of the preceding prefill");
+  if (n_steps < 1 || n_steps > D.max_new || D.prompt_len + n_steps > D.cap)
+    fail(1, "n_steps out of range (1..max_new_tokens, prompt + steps <= cache rows)");
+  cudaStream_t s = ex.compute;
+  // device state: the prefill's argmax key is the first decode input
+  DecodeState init;
+  memset(&init, 0, sizeof init);
+  init.pos0 = D.prompt_len;
+  cuda_check(cudaMemcpyAsync(D.st, &init, sizeof init, cudaMemcpyHostToDevice, s), "state");
+  cuda_check(cudaMemcpyAsync(&D.st->key, ex.key, 8, cudaMemcpyDeviceToDevice, s), "state key");
+  const auto gkey = std::make_tuple(akey, gen, tt.lora_rank, tt.lora_mask, lora_scale,
+                                    want_logits ? 1 : 0);
+  if (!D.gexec || D.gkey != gkey) {
+    if (D.gexec) cudaGraphExecDestroy(D.gexec);
+    D.gexec = nullptr;
+    cudaGraph_t graph = nullptr;
+    const int l0 = ex.launches;
+    cuda_check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+      enqueue_decode_step(ex, tt, lora_scale, want_logits);
+    } catch (...) {
+      cudaStreamEndCapture(s, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    cuda_check(cudaStreamEndCapture(s, &graph), "end capture");
+    cuda_check(cudaGraphInstantiate(&D.gexec, graph, 0), "graph instantiate");
+    cudaGraphDestroy(graph);
+    D.gkey = gkey;
+    D.launches_per_step = ex.launches - l0;
+    ex.launches = l0;
+  }
+  for (int i = 0; i < n_steps; ++i) cuda_check(cudaGraphLaunch(D.gexec, s), "graph launch");
+  cuda_check(dec_finish_launch(D.st, D.toks, s), "dec_finish");
+  ex.launches += n_steps * D.launches_per_step + 1;
 }
 
 // ---------------- NUMA binding ----------------

@@ -54,6 +54,24 @@ struct Exec {
   bf16* Vt = nullptr;  // V^T [KV*hd][vt_ld] (tcgen05 attention, hd = 128)
   int vt_ld = 0;
   std::map<std::pair<int, int>, AttnParams> attn_cache;  // per (rows, prompts)
+  // decode continuation (decode.cu): KV cache filled by the prefill's QKV
+  // epilogue, per-step scratch, device state, and the captured step graph
+  struct Decode {
+    int max_new = 0, cap = 0;         // cache rows per layer = max_tokens + max_new
+    bf16 *kc = nullptr, *vc = nullptr;  // [L][cap][nkv]
+    bf16 *q = nullptr, *att = nullptr, *h = nullptr;
+    float* T = nullptr;               // [7][64] LoRA shrink outputs
+    float* part = nullptr;            // attention chunk partials
+    DecodeState* st = nullptr;
+    int32_t* toks = nullptr;          // [max_new]
+    float* logits_all = nullptr;      // [max_new][V]
+    int prompt_len = 0;               // rows of the cache valid (last single-prompt prefill)
+    const void* prompt_akey = nullptr;
+    uint64_t prompt_gen = 0;
+    cudaGraphExec_t gexec = nullptr;
+    int launches_per_step = 0;
+    std::tuple<const void*, uint64_t, int, uint32_t, float, int> gkey;
+  } dec;
   // pinned host staging
   int32_t* h_tok = nullptr;
   float* h_logits = nullptr;
@@ -84,6 +102,8 @@ struct Exec {
 
   void init(int device, const ModelShape& m, float eps, float theta, int world, int rank,
             int max_tokens);
+  void enable_decode(int max_new);
+  void build_rope(int rows);
   void destroy();
   const std::vector<LayerLaunch>& layer_params(const TensorTable& tt, int S, int nseq,
                                                const void* akey, uint64_t gen);
@@ -137,6 +157,13 @@ struct RunArgs {
 
 // Enqueue the forward for one prompt on exec.compute (tokens already in exec.tok).
 void run_forward(Exec& ex, const RunArgs& a);
+
+// Greedy decode of n_steps tokens continuing the last single-prompt prefill
+// (whose argmax key is in ex.key[0]); all weights must be on the device.
+// Tokens (and, if want_logits, [n_steps][V] logits) are left in ex.dec.toks /
+// ex.dec.logits_all; returns after enqueueing (compute stream).
+void run_decode(Exec& ex, const TensorTable& tt, int n_steps, float lora_scale, const void* akey,
+                uint64_t gen, bool want_logits);
 
 // NUMA: bind the calling thread to the CPUs local to `device` (restored by the guard).
 struct NumaGuard {

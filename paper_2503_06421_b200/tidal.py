@@ -69,6 +69,15 @@ class Stats(C.Structure):
         return {k: getattr(self, k) for k, _ in self._fields_}
 
 
+class DecodeStats(C.Structure):
+    _fields_ = [("device_ms", C.c_double), ("per_token_ms", C.c_double),
+                ("weight_bytes_per_token", C.c_uint64), ("kv_bytes_last_token", C.c_uint64),
+                ("n_kernels", C.c_int)]
+
+    def as_dict(self) -> dict:
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 class KernelTime(C.Structure):
     _fields_ = [("name", C.c_char_p), ("total_ms", C.c_double), ("launches", C.c_long),
                 ("flops", C.c_double), ("bytes", C.c_double)]
@@ -98,6 +107,8 @@ SIGNATURES = [
     ("tidal_adapter_destroy", None, [VP]),
     ("tidal_plan_dump", C.c_int, [VP, VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("tidal_invoke_prefill", C.c_int, [VP, VP, VP, C.c_int, VP, VP, C.POINTER(Stats)]),
+    ("tidal_template_enable_decode", C.c_int, [VP, C.c_int]),
+    ("tidal_invoke_decode", C.c_int, [VP, VP, C.c_int, VP, VP, C.POINTER(DecodeStats)]),
     ("tidal_invoke_prefill_batch", C.c_int,
      [VP, VP, VP, C.c_int, C.c_int, VP, VP, C.POINTER(Stats)]),
     ("tidal_host_alloc", C.c_int, [C.c_uint64, C.POINTER(VP)]),
@@ -290,6 +301,23 @@ class Template:
                                                 logits.ctypes.data if want_logits else None,
                                                 out.ctypes.data, C.byref(st)))
         return out, logits, st.as_dict()
+
+    def enable_decode(self, max_new_tokens: int) -> None:
+        """Allocate the KV cache; later single-prompt invocations fill it."""
+        _check(lib().tidal_template_enable_decode(self.h, max_new_tokens))
+
+    def decode(self, n_steps: int, adapter: Optional["Adapter"] = None,
+               want_logits: bool = True) -> Tuple[np.ndarray, Optional[np.ndarray], dict]:
+        """Greedy decode continuing the last single-prompt invoke():
+        (tokens [n_steps], logits [n_steps, vocab] or None, stats)."""
+        toks = np.empty(n_steps, np.int32)
+        logits = np.empty((n_steps, self.vocab), np.float32) if want_logits else None
+        st = DecodeStats()
+        _check(lib().tidal_invoke_decode(self.h, adapter.h if adapter else None, n_steps,
+                                         toks.ctypes.data,
+                                         logits.ctypes.data if want_logits else None,
+                                         C.byref(st)))
+        return toks, logits, st.as_dict()
 
     def set_debug(self, flags: int, arg: int = -1) -> None:
         _check(lib().tidal_set_debug(self.h, flags, arg))
