@@ -164,6 +164,8 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
     ap.add_argument("--quick", action="store_true", help="profiling runs: minimal extra passes")
+    ap.add_argument("--decode-steps", type=int, default=64,
+                    help="greedy decode steps measured after the prefill (0: skip)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
@@ -287,6 +289,29 @@ def main():
             tpl.set_load_order(order)
             sweep[name] = max_over_ranks(step(T.DEBUG_SCRUB_L2)["device_ms"])
         tpl.set_load_order(T.ORDER_TRACED)
+    decode = None
+    if world == 1 and not args.quick and args.decode_steps > 0:
+        # decode continuation: greedy steps after the first
+        # token, every weight read from HBM once per token; roofline = (weight
+        # bytes + mean K/V bytes) / measured HBM bandwidth
+        n = args.decode_steps
+        tpl.enable_decode(n)
+        per_tok = []
+        for _ in range(3):
+            tpl.set_debug(0)
+            ad = attach()
+            tpl.invoke(tokens, ad, want_logits=False)
+            _, _, dst = tpl.decode(n, ad, want_logits=False)
+            per_tok.append(dst["per_token_ms"])
+        ms = statistics.median(per_tok)
+        kv_mean = dst["kv_bytes_last_token"] * (S + n / 2) / (S + n)
+        bytes_tok = dst["weight_bytes_per_token"] + kv_mean
+        roof_ms = bytes_tok / (P["hbm_gbs"] * 1e9) * 1e3
+        decode = {"steps": n, "after_prompt": S, "ms_per_token": ms, "tokens_per_s": 1e3 / ms,
+                  "bytes_per_token": bytes_tok, "hbm_gbs_achieved": bytes_tok / (ms / 1e3) / 1e9,
+                  "hbm_roof_ms_per_token": roof_ms, "frac": roof_ms / ms,
+                  "kernels_per_token": dst["n_kernels"] / n,
+                  "note": "CUDA-graph replay per token; weights resident after the prefill"}
     dev_ms = [max_over_ranks(s["device_ms"]) for s in stats]
     e2e_ms = [max_over_ranks(s["e2e_ms"]) for s in stats]
     s0 = stats[0]
@@ -376,6 +401,7 @@ def main():
             "frac_sustained": flops / (P.get("bf16_tflops_sustained", P["bf16_tflops"]) * 1e12) * 1e3 / t_warm},
         "setup_s": setup_s,
         "first_token": s0["token"],
+        "decode": decode,
     }
     print(json.dumps(out))
 

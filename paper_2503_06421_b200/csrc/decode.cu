@@ -50,73 +50,132 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 }
 
 // x (fp32, shared) <- RMSNorm(X) * g rounded to bf16 (as the prefill's Xn), or
-// <- a bf16 vector (attention output / H).  Every CTA builds its own copy.
+// <- a bf16 vector (attention output / H).  Every CTA builds its own copy;
+// 16-B vector loads, all of a thread's loads issued before any is consumed
+// (K <= 16384: at most 16 float4 per thread), the raw row parked in shared
+// memory between the two passes.
 __device__ __forceinline__ void load_input(float* xs, const float* X, const bf16* g,
                                            const bf16* xin, int K, float eps, float* red) {
-  if (X) {
+  if (X) {  // K = d_model <= 16384
+    const float4* X4 = reinterpret_cast<const float4*>(X);
+    float4* xs4 = reinterpret_cast<float4*>(xs);
+    const int n4 = K >> 2;
+    float4 v[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int i = threadIdx.x + k * DT;
+      if (i < n4) v[k] = X4[i];
+    }
     float ss = 0.f;
-    for (int i = threadIdx.x; i < K; i += DT) {
-      const float v = X[i];
-      ss += v * v;
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int i = threadIdx.x + k * DT;
+      if (i < n4) {
+        ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
+        xs4[i] = v[k];
+      }
     }
     const float inv = rsqrtf(block_sum(ss, red) / (float)K + eps);
-    for (int i = threadIdx.x; i < K; i += DT)
-      xs[i] = __bfloat162float(__float2bfloat16_rn(X[i] * inv * __bfloat162float(g[i])));
+    const uint2* g4 = reinterpret_cast<const uint2*>(g);
+#pragma unroll
+    for (int k = 0; k < 16; ++k) {
+      const int i = threadIdx.x + k * DT;
+      if (i < n4) {
+        const uint2 gw = g4[i];
+        const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gw);
+        const float2 g01 = __bfloat1622float2(gh[0]), g23 = __bfloat1622float2(gh[1]);
+        const float4 x = v[k];
+        xs4[i] = make_float4(__bfloat162float(__float2bfloat16_rn(x.x * inv * g01.x)),
+                             __bfloat162float(__float2bfloat16_rn(x.y * inv * g01.y)),
+                             __bfloat162float(__float2bfloat16_rn(x.z * inv * g23.x)),
+                             __bfloat162float(__float2bfloat16_rn(x.w * inv * g23.y)));
+      }
+    }
   } else {
-    for (int i = threadIdx.x; i < K; i += DT) xs[i] = __bfloat162float(xin[i]);
+    const uint4* x8 = reinterpret_cast<const uint4*>(xin);
+    const int n8 = K >> 3;
+    for (int base = 0; base < n8; base += 8 * DT) {  // rounds of 8 loads per thread
+    uint4 v[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = base + threadIdx.x + k * DT;
+      if (i < n8) v[k] = x8[i];
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const int i = base + threadIdx.x + k * DT;
+      if (i < n8) {
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
+        float4* d = reinterpret_cast<float4*>(xs + 8 * i);
+        const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+        const float2 c = __bfloat1622float2(h[2]), e = __bfloat1622float2(h[3]);
+        d[0] = make_float4(a.x, a.y, b.x, b.y);
+        d[1] = make_float4(c.x, c.y, e.x, e.y);
+      }
+    }
+    }
   }
   __syncthreads();
 }
 
-// dot products of two weight rows with xs (fp32 in shared memory): 16-B loads,
-// four per row in flight per lane, fp32 accumulation
+// Two weight rows against xs (fp32 in shared memory): 16-B loads in batches
+// of 4 per row per lane, the next batch issued before the current one is
+// consumed (16 loads in flight per lane), fp32 accumulation.  `ca`/`cb` hold
+// the first batch (loaded by the caller, possibly before the PDL wait).
+__device__ __forceinline__ void load_batch(const uint4* r0, const uint4* r1, int i, int n,
+                                           uint4 (&a)[4], uint4 (&b)[4]) {
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const int j = i + 32 * k;
+    if (j < n) {
+      a[k] = __ldcs(r0 + j);
+      b[k] = __ldcs(r1 + j);
+    } else {
+      a[k] = make_uint4(0, 0, 0, 0);
+      b[k] = a[k];
+    }
+  }
+}
+__device__ __forceinline__ void fma8(const uint4& u, const float* x, float& s) {
+  const float4 xa = reinterpret_cast<const float4*>(x)[0], xb = reinterpret_cast<const float4*>(x)[1];
+  const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&u);
+  float2 f;
+  f = __bfloat1622float2(h[0]); s = fmaf(f.x, xa.x, fmaf(f.y, xa.y, s));
+  f = __bfloat1622float2(h[1]); s = fmaf(f.x, xa.z, fmaf(f.y, xa.w, s));
+  f = __bfloat1622float2(h[2]); s = fmaf(f.x, xb.x, fmaf(f.y, xb.y, s));
+  f = __bfloat1622float2(h[3]); s = fmaf(f.x, xb.z, fmaf(f.y, xb.w, s));
+}
+// nx0/nx1 (nullable): the next pair's rows — their first batch is issued in
+// place of this pair's (empty) batch past the end, so the stream never drains
 __device__ __forceinline__ void dot2(const bf16* __restrict__ w0, const bf16* __restrict__ w1,
-                                     const float* xs, int K, float& a0, float& a1) {
+                                     const float* xs, int K, uint4 (&ca)[4], uint4 (&cb)[4],
+                                     float& a0, float& a1, const bf16* nx0 = nullptr,
+                                     const bf16* nx1 = nullptr) {
   const int lane = threadIdx.x & 31;
   const uint4* r0 = reinterpret_cast<const uint4*>(w0);
   const uint4* r1 = reinterpret_cast<const uint4*>(w1);
   const int n = K >> 3;
   float s0 = 0.f, s1 = 0.f;
-  int i = lane;
-  for (; i + 96 < n; i += 128) {
-    uint4 u0[4], u1[4];
+  for (int i = lane; i < n; i += 128) {
+    uint4 na[4], nb[4];
+    if (i + 128 < n || nx0 == nullptr)
+      load_batch(r0, r1, i + 128, n, na, nb);
+    else
+      load_batch(reinterpret_cast<const uint4*>(nx0), reinterpret_cast<const uint4*>(nx1), lane, n,
+                 na, nb);
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      u0[k] = __ldcs(r0 + i + 32 * k);
-      u1[k] = __ldcs(r1 + i + 32 * k);
+      const int j = i + 32 * k;
+      if (j < n) {
+        fma8(ca[k], xs + 8 * j, s0);
+        fma8(cb[k], xs + 8 * j, s1);
+      }
     }
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      const float4* xv = reinterpret_cast<const float4*>(xs + 8 * (i + 32 * k));
-      const float4 xa = xv[0], xb = xv[1];
-      const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&u0[k]);
-      const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&u1[k]);
-      float2 f;
-      f = __bfloat1622float2(h0[0]); s0 = fmaf(f.x, xa.x, fmaf(f.y, xa.y, s0));
-      f = __bfloat1622float2(h0[1]); s0 = fmaf(f.x, xa.z, fmaf(f.y, xa.w, s0));
-      f = __bfloat1622float2(h0[2]); s0 = fmaf(f.x, xb.x, fmaf(f.y, xb.y, s0));
-      f = __bfloat1622float2(h0[3]); s0 = fmaf(f.x, xb.z, fmaf(f.y, xb.w, s0));
-      f = __bfloat1622float2(h1[0]); s1 = fmaf(f.x, xa.x, fmaf(f.y, xa.y, s1));
-      f = __bfloat1622float2(h1[1]); s1 = fmaf(f.x, xa.z, fmaf(f.y, xa.w, s1));
-      f = __bfloat1622float2(h1[2]); s1 = fmaf(f.x, xb.x, fmaf(f.y, xb.y, s1));
-      f = __bfloat1622float2(h1[3]); s1 = fmaf(f.x, xb.z, fmaf(f.y, xb.w, s1));
+      ca[k] = na[k];
+      cb[k] = nb[k];
     }
-  }
-  for (; i < n; i += 32) {
-    const uint4 u0 = __ldcs(r0 + i), u1 = __ldcs(r1 + i);
-    const float4* xv = reinterpret_cast<const float4*>(xs + 8 * i);
-    const float4 xa = xv[0], xb = xv[1];
-    const __nv_bfloat162* h0 = reinterpret_cast<const __nv_bfloat162*>(&u0);
-    const __nv_bfloat162* h1 = reinterpret_cast<const __nv_bfloat162*>(&u1);
-    float2 f;
-    f = __bfloat1622float2(h0[0]); s0 = fmaf(f.x, xa.x, fmaf(f.y, xa.y, s0));
-    f = __bfloat1622float2(h0[1]); s0 = fmaf(f.x, xa.z, fmaf(f.y, xa.w, s0));
-    f = __bfloat1622float2(h0[2]); s0 = fmaf(f.x, xb.x, fmaf(f.y, xb.y, s0));
-    f = __bfloat1622float2(h0[3]); s0 = fmaf(f.x, xb.z, fmaf(f.y, xb.w, s0));
-    f = __bfloat1622float2(h1[0]); s1 = fmaf(f.x, xa.x, fmaf(f.y, xa.y, s1));
-    f = __bfloat1622float2(h1[1]); s1 = fmaf(f.x, xa.z, fmaf(f.y, xa.w, s1));
-    f = __bfloat1622float2(h1[2]); s1 = fmaf(f.x, xb.x, fmaf(f.y, xb.y, s1));
-    f = __bfloat1622float2(h1[3]); s1 = fmaf(f.x, xb.z, fmaf(f.y, xb.w, s1));
   }
   a0 = warp_sum(s0);
   a1 = warp_sum(s1);
@@ -131,6 +190,22 @@ __device__ __forceinline__ float lora_row(const bf16* B, int row, int r, const f
   if (lane < r) s = __bfloat162float(B[(size_t)row * r + lane]) * T[lane];
   if (lane + 32 < r) s = fmaf(__bfloat162float(B[(size_t)row * r + lane + 32]), T[lane + 32], s);
   return warp_sum(s);
+}
+
+// same, with this lane's T values in registers (t0 = T[lane], t1 = T[lane + 32])
+__device__ __forceinline__ float lora_row_r(const bf16* B, int row, int r, float t0, float t1) {
+  if (!B) return 0.f;
+  const int lane = threadIdx.x & 31;
+  float s = 0.f;
+  if (lane < r) s = __bfloat162float(B[(size_t)row * r + lane]) * t0;
+  if (lane + 32 < r) s = fmaf(__bfloat162float(B[(size_t)row * r + lane + 32]), t1, s);
+  return warp_sum(s);
+}
+
+__device__ __forceinline__ int ld_acquire_i32(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
 }
 
 // ---------------- embed (token from the previous argmax) ----------------
@@ -167,65 +242,135 @@ __global__ void dec_finish_kernel(DecodeState* st, int32_t* toks_out) {
     toks_out[st->step - 1] = (int)(0xFFFFFFFFu - (uint32_t)(key & 0xFFFFFFFFu));
 }
 
-// ---------------- LoRA shrink: T_t = s * A_t . x ----------------
-// one warp per output (nt * r <= 192 rows); x = RMSNorm(X)*g or a bf16 vector
-__global__ void __launch_bounds__(DT) dec_shrink_kernel(DecShrink a, const float* X, const bf16* g,
-                                                        const bf16* xin, int K, float eps,
-                                                        float scale) {
-  extern __shared__ float xs[];
-  __shared__ float red[32];
-  ptx::pdl_begin();
-  load_input(xs, X, g, xin, K, eps, red);
-  const int warp = threadIdx.x >> 5;
-  const int rows = a.nt * a.r;
-  for (int o = blockIdx.x * (DT / 32) + warp; o < rows; o += gridDim.x * (DT / 32)) {
-    const int t = o / a.r, j = o - t * a.r;
-    float s0, s1;
-    dot2(a.A[t] + (size_t)j * K, a.A[t] + (size_t)j * K, xs, K, s0, s1);
-    if ((threadIdx.x & 31) == 0) a.T[t][j] = s0 * scale;
+// ---------------- GEMV family ----------------
+// Row pairs per warp.  QKV: q/k pairs are RoPE partners (h*hd + i, h*hd + i +
+// hd/2), v pairs are adjacent rows; GU: (gate i, up i); RESID: adjacent rows.
+template <int MODE>
+__device__ __forceinline__ void pair_rows(const DecGemv& p, int pr, const bf16*& w0,
+                                          const bf16*& w1, int& seg, int& r0, int& r1) {
+  if (MODE == DEC_QKV) {
+    const int half = p.hd >> 1;
+    const int nqp = p.nq >> 1, nkp = p.nkv >> 1;
+    if (pr < nqp + nkp) {
+      seg = pr < nqp ? 0 : 1;
+      const int pp = seg == 0 ? pr : pr - nqp;
+      const int h = pp / half, i = pp - h * half;
+      r0 = h * p.hd + i;
+      r1 = r0 + half;
+    } else {
+      seg = 2;
+      r0 = 2 * (pr - nqp - nkp);
+      r1 = r0 + 1;
+    }
+    w0 = p.W[seg] + (size_t)r0 * p.K;
+    w1 = p.W[seg] + (size_t)r1 * p.K;
+  } else if (MODE == DEC_GU) {
+    seg = 0;
+    r0 = r1 = pr;
+    w0 = p.W[0] + (size_t)pr * p.K;
+    w1 = p.W[1] + (size_t)pr * p.K;
+  } else {
+    seg = 0;
+    r0 = 2 * pr;
+    r1 = r0 + 1 < p.N ? r0 + 1 : r0;
+    w0 = p.W[0] + (size_t)r0 * p.K;
+    w1 = p.W[0] + (size_t)r1 * p.K;
   }
 }
 
-// ---------------- GEMV family ----------------
-// Row pairs per warp.  QKV: q/k pairs are RoPE partners (h*hd + i, h*hd + i +
-// hd/2), v pairs are adjacent rows; GU: (gate i, up i); O / DOWN: adjacent rows.
+// The LoRA shrink of this GEMV's input rides in the same launch: CTAs
+// [0, nsh) compute T's K parts (8 rows x one part each) and count themselves
+// on sh_cnt; GEMV warps stream their first weights meanwhile and wait for the
+// count (monotonic over steps: nsh x step) only before their first LoRA term.
+// The whole grid is co-resident (<= 2 CTAs per SM), so the wait cannot block
+// a shrink CTA from being scheduled.
 template <int MODE>
 __global__ void __launch_bounds__(DT) dec_gemv_kernel(DecGemv p) {
   extern __shared__ float xs[];
   __shared__ float red[32];
-  __shared__ float Ts[3][64];
-  ptx::pdl_begin();
-  load_input(xs, p.X, p.g, p.xin, p.K, p.eps, red);
-  for (int i = threadIdx.x; i < 3 * 64; i += DT) {
-    const int t = i / 64, j = i - t * 64;
-    Ts[t][j] = (p.T[t] && j < p.r) ? p.T[t][j] : 0.f;
-  }
-  __syncthreads();
+  ptx::pdl_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if ((int)blockIdx.x < p.nsh) {  // ---- LoRA shrink role ----
+    const DecShrink& a = p.sh;
+    const int o = (blockIdx.x / DEC_TSPLIT) * (DT / 32) + warp, part = blockIdx.x % DEC_TSPLIT;
+    const int rows = a.nt * a.r, K = p.K;
+    const int t = o / a.r, j = o - t * a.r;
+    const int per = ((K >> 3) + DEC_TSPLIT - 1) / DEC_TSPLIT;
+    const int u0 = part * per, u1 = min(K >> 3, u0 + per);
+    uint4 w[4] = {};
+    const uint4* Ar = o < rows ? reinterpret_cast<const uint4*>(a.A[t] + (size_t)j * K) : nullptr;
+    if (Ar) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (u0 + lane + 32 * k < u1) w[k] = __ldcs(Ar + u0 + lane + 32 * k);
+    }
+    ptx::pdl_wait();
+    load_input(xs, p.X, p.g, p.xin, K, p.eps, red);
+    if (Ar) {
+      float sacc = 0.f;
+#pragma unroll
+      for (int k = 0; k < 4; ++k)
+        if (u0 + lane + 32 * k < u1) fma8(w[k], xs + 8 * (u0 + lane + 32 * k), sacc);
+      for (int i = u0 + lane + 128; i < u1; i += 32) fma8(__ldcs(Ar + i), xs + 8 * i, sacc);
+      sacc = warp_sum(sacc);
+      if (lane == 0) a.T[t][(size_t)part * DEC_TSTRIDE + j] = sacc * p.sh_scale;
+    }
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) atomicAdd(p.sh_cnt, 1);
+    return;
+  }
+  const int stride = (gridDim.x - p.nsh) * (DT / 32);
+  int pr = (blockIdx.x - p.nsh) * (DT / 32) + warp;
+  // the first pair's first batch of weights streams in while the previous
+  // kernel finishes (weights are read-only during the step)
+  uint4 ca[4], cb[4];
+  const bf16 *w0 = nullptr, *w1 = nullptr;
+  int seg = 0, r0 = 0, r1 = 0;
+  if (pr < p.npairs) {
+    pair_rows<MODE>(p, pr, w0, w1, seg, r0, r1);
+    load_batch(reinterpret_cast<const uint4*>(w0), reinterpret_cast<const uint4*>(w1), lane,
+               p.K >> 3, ca, cb);
+  }
+  ptx::pdl_wait();
+  load_input(xs, p.X, p.g, p.xin, p.K, p.eps, red);
+  // this lane's LoRA T values (j = lane, lane + 32) per segment, loaded once
+  float tv[3][2] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+  bool t_ready = p.nsh == 0;
+  auto fetch_t = [&]() {
+    if (lane == 0) {
+      const int want = p.nsh * p.st->step;
+      uint32_t n = 0;
+      while (ld_acquire_i32(p.sh_cnt) < want)
+        if (++n == (1u << 30)) __trap();
+    }
+    __syncwarp();
+    for (int t = 0; t < 3; ++t)
+      if (p.T[t])
+        for (int h = 0; h < 2; ++h) {
+          const int j = lane + 32 * h;
+          float v = 0.f;
+          if (j < p.r)
+            for (int q = 0; q < DEC_TSPLIT; ++q) v += __ldcg(p.T[t] + (size_t)q * DEC_TSTRIDE + j);
+          tv[t][h] = v;  // part order
+        }
+    t_ready = true;
+  };
   const int pos = p.st ? p.st->pos : 0;
-  for (int pr = blockIdx.x * (DT / 32) + warp; pr < p.npairs; pr += gridDim.x * (DT / 32)) {
+  for (; pr < p.npairs; pr += stride) {
+    // rows of the next pair: their first batch loads while this pair finishes
+    const bf16 *n0 = nullptr, *n1 = nullptr;
+    int nseg = 0, nr0 = 0, nr1 = 0;
+    if (pr + stride < p.npairs) pair_rows<MODE>(p, pr + stride, n0, n1, nseg, nr0, nr1);
+    float a0, a1;
+    dot2(w0, w1, xs, p.K, ca, cb, a0, a1, n0, n1);
+    if (!t_ready) fetch_t();
     if (MODE == DEC_QKV) {
-      const int half = p.hd >> 1;
-      const int nqp = p.nq >> 1, nkp = p.nkv >> 1;
-      int seg, r0, r1;
-      if (pr < nqp + nkp) {  // q or k: RoPE partners
-        seg = pr < nqp ? 0 : 1;
-        const int pp = seg == 0 ? pr : pr - nqp;
-        const int h = pp / half, i = pp - h * half;
-        r0 = h * p.hd + i;
-        r1 = r0 + half;
-      } else {
-        seg = 2;
-        r0 = 2 * (pr - nqp - nkp);
-        r1 = r0 + 1;
-      }
-      const bf16* W = p.W[seg];
-      float a0, a1;
-      dot2(W + (size_t)r0 * p.K, W + (size_t)r1 * p.K, xs, p.K, a0, a1);
-      a0 += lora_row(p.B[seg], r0, p.r, Ts[seg]);
-      a1 += lora_row(p.B[seg], r1, p.r, Ts[seg]);
+      a0 += lora_row_r(p.B[seg], r0, p.r, tv[seg][0], tv[seg][1]);
+      a1 += lora_row_r(p.B[seg], r1, p.r, tv[seg][0], tv[seg][1]);
       if (lane == 0) {
         if (seg < 2) {  // rotate-half RoPE at this token's position
+          const int half = p.hd >> 1;
           const float2 cs0 = p.rope[(size_t)pos * half + (r0 % p.hd)];
           const float x1 = a0, x2 = a1;
           a0 = x1 * cs0.x - x2 * cs0.y;
@@ -236,88 +381,84 @@ __global__ void __launch_bounds__(DT) dec_gemv_kernel(DecGemv p) {
         dst[r1] = __float2bfloat16_rn(a1);
       }
     } else if (MODE == DEC_GU) {
-      float a0, a1;
-      dot2(p.W[0] + (size_t)pr * p.K, p.W[1] + (size_t)pr * p.K, xs, p.K, a0, a1);
-      const float gt = a0 + lora_row(p.B[0], pr, p.r, Ts[0]);
-      const float up = a1 + lora_row(p.B[1], pr, p.r, Ts[1]);
+      const float gt = a0 + lora_row_r(p.B[0], pr, p.r, tv[0][0], tv[0][1]);
+      const float up = a1 + lora_row_r(p.B[1], pr, p.r, tv[1][0], tv[1][1]);
       if (lane == 0) p.h[pr] = __float2bfloat16_rn(gt / (1.f + __expf(-gt)) * up);
     } else {  // DEC_RESID: X[row] += W[row] . x
-      const int r0 = 2 * pr, r1 = r0 + 1 < p.N ? r0 + 1 : r0;
-      float a0, a1;
-      dot2(p.W[0] + (size_t)r0 * p.K, p.W[0] + (size_t)r1 * p.K, xs, p.K, a0, a1);
-      a0 += lora_row(p.B[0], r0, p.r, Ts[0]);
-      a1 += lora_row(p.B[0], r1, p.r, Ts[0]);
+      a0 += lora_row_r(p.B[0], r0, p.r, tv[0][0], tv[0][1]);
+      a1 += lora_row_r(p.B[0], r1, p.r, tv[0][0], tv[0][1]);
       if (lane == 0) {
         p.Xout[r0] += a0;
         if (r1 != r0) p.Xout[r1] += a1;
       }
     }
+    w0 = n0;
+    w1 = n1;
+    seg = nseg;
+    r0 = nr0;
+    r1 = nr1;
   }
 }
 
 // ---------------- attention over the cache (one query token) ----------------
-// CTA = (head, 256-key chunk): lane = key for the scores, lane = 4 dims for PV;
-// partial (max, sum, o[hd]) per chunk; dec_combine folds the chunks in order.
-constexpr int ACH = 256;
-__global__ void __launch_bounds__(DT) dec_attn_kernel(DecAttn a) {
+// CTA = (head, 128-key chunk), 128 threads: thread = key for the scores, lane =
+// hd/32 dims for PV; each chunk leaves (max, sum, o[hd]) and the last chunk of
+// a head to finish folds all chunks in chunk order (deterministic) into the
+// bf16 attention output, then re-arms the head's counter.
+constexpr int ACH = 128, ATH = 128;
+__global__ void __launch_bounds__(ATH) dec_attn_kernel(DecAttn a) {
   __shared__ float qs[128];
   __shared__ float ps[ACH];
-  __shared__ float red[32];
-  __shared__ float os[DT / 32][128];
-  ptx::pdl_begin();
+  __shared__ float red[ATH / 32];
+  __shared__ float os[ATH / 32][128];
+  __shared__ int last;
+  ptx::pdl_launch();
+  ptx::pdl_wait();
   const int h = blockIdx.x, c = blockIdx.y;
   const int g = h / (a.H / a.KV);
   const int nkeys = a.st->pos + 1;
   const int k0 = c * ACH, k1 = min(nkeys, k0 + ACH);
+  if (k0 >= k1) return;  // past the current position: not part of this step
+  const int nchunks = (nkeys + ACH - 1) / ACH;
   float* part = a.part + ((size_t)h * gridDim.y + c) * (2 + 128);
-  if (k0 >= k1) {
-    if (threadIdx.x == 0) {
-      part[0] = -INFINITY;
-      part[1] = 0.f;
-    }
-    return;
-  }
-  for (int i = threadIdx.x; i < a.hd; i += DT) qs[i] = __bfloat162float(a.q[h * a.hd + i]) * a.scale_log2;
+  for (int i = threadIdx.x; i < a.hd; i += ATH) qs[i] = __bfloat162float(a.q[h * a.hd + i]) * a.scale_log2;
   __syncthreads();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  // scores: thread t <-> key k0 + t
   float s = -INFINITY;
   const int k = k0 + threadIdx.x;
   if (k < k1) {
     const uint4* kr = reinterpret_cast<const uint4*>(a.kc + (size_t)k * a.ldkv + g * a.hd);
-    float acc = 0.f;
-#pragma unroll 4
-    for (int i = 0; i < a.hd / 8; ++i) {
-      const uint4 u = kr[i];
-      const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+    uint4 u[16];
+    const int nu = a.hd >> 3;
 #pragma unroll
-      for (int e = 0; e < 4; ++e) {
-        const float2 f = __bfloat1622float2(hh[e]);
-        acc = fmaf(f.x, qs[8 * i + 2 * e], fmaf(f.y, qs[8 * i + 2 * e + 1], acc));
-      }
-    }
+    for (int i = 0; i < 16; ++i)
+      if (i < nu) u[i] = kr[i];
+    float acc = 0.f;
+#pragma unroll
+    for (int i = 0; i < 16; ++i)
+      if (i < nu) fma8(u[i], qs + 8 * i, acc);
     s = acc;  // log2 domain (q pre-scaled)
   }
   float m = warp_max(s);
   if (lane == 0) red[warp] = m;
   __syncthreads();
   m = red[0];
-  for (int w = 1; w < DT / 32; ++w) m = fmaxf(m, red[w]);
+  for (int w = 1; w < ATH / 32; ++w) m = fmaxf(m, red[w]);
   const float pk = k < k1 ? ptx::ex2(s - m) : 0.f;
   ps[threadIdx.x] = pk;
-  __syncthreads();
-  float l = warp_sum(pk);
-  __syncthreads();
-  if (lane == 0) red[warp] = l;
-  // PV: warp w takes keys w, w+8, ...; lane owns dims dpl*lane .. (hd = 32 dpl)
+  const float lw = warp_sum(pk);
+  __syncthreads();  // every thread read red (max) and wrote ps
+  if (lane == 0) red[warp] = lw;
+  // PV: warp w takes keys w, w+4, ...; lane owns dims dpl*lane .. (hd = 32 dpl)
   const int dpl = a.hd >> 5;  // 2 or 4
   float o[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int kk = warp; kk < k1 - k0; kk += DT / 32) {
+#pragma unroll 8
+  for (int kk = warp; kk < k1 - k0; kk += ATH / 32) {
     const float pv = ps[kk];
     const bf16* vr = a.vc + (size_t)(k0 + kk) * a.ldkv + g * a.hd + dpl * lane;
     if (dpl == 4) {
-      const uint2 u = *reinterpret_cast<const uint2*>(vr);
-      const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&u);
+      const uint2 uu = *reinterpret_cast<const uint2*>(vr);
+      const __nv_bfloat162* hh = reinterpret_cast<const __nv_bfloat162*>(&uu);
       const float2 f0 = __bfloat1622float2(hh[0]), f1 = __bfloat1622float2(hh[1]);
       o[0] = fmaf(pv, f0.x, o[0]);
       o[1] = fmaf(pv, f0.y, o[1]);
@@ -333,32 +474,47 @@ __global__ void __launch_bounds__(DT) dec_attn_kernel(DecAttn a) {
   __syncthreads();
   if (threadIdx.x < a.hd) {
     float acc = 0.f;
-    for (int w = 0; w < DT / 32; ++w) acc += os[w][threadIdx.x];  // fixed order
+    for (int w = 0; w < ATH / 32; ++w) acc += os[w][threadIdx.x];  // fixed order
     part[2 + threadIdx.x] = acc;
   }
   if (threadIdx.x == 0) {
     float lt = 0.f;
-    for (int w = 0; w < DT / 32; ++w) lt += red[w];
+    for (int w = 0; w < ATH / 32; ++w) lt += red[w];
     part[0] = m;
     part[1] = lt;
   }
-}
-
-__global__ void dec_combine_kernel(DecAttn a, int nchunks) {
-  ptx::pdl_begin();
-  const int h = blockIdx.x, i = threadIdx.x;
-  const float* part = a.part + (size_t)h * nchunks * (2 + 128);
-  float m = -INFINITY;
-  for (int c = 0; c < nchunks; ++c) m = fmaxf(m, part[c * 130]);
-  float l = 0.f, o = 0.f;
-  for (int c = 0; c < nchunks; ++c) {  // chunk order: deterministic
-    const float mc = part[c * 130];
-    if (mc == -INFINITY) continue;
-    const float w = ptx::ex2(mc - m);
-    l = fmaf(w, part[c * 130 + 1], l);
-    o = fmaf(w, part[c * 130 + 2 + i], o);
+  // ---- the last chunk of this head combines ----
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) last = atomicAdd(a.cnt + h, 1) == nchunks - 1;
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  // chunk statistics in parallel (thread = chunk), then every output dim folds
+  // the chunks in chunk order with its loads batched
+  const float* hp = a.part + (size_t)h * gridDim.y * (2 + 128);
+  float* cw = ps;  // reuse: per-chunk weight 2^(m_c - max) and sums
+  float* cl = qs;
+  if (threadIdx.x < nchunks) {
+    cw[threadIdx.x] = __ldcg(hp + threadIdx.x * 130);
+    cl[threadIdx.x] = __ldcg(hp + threadIdx.x * 130 + 1);
   }
-  if (i < a.hd) a.out[h * a.hd + i] = __float2bfloat16_rn(o / l);
+  __syncthreads();
+  float mx = -INFINITY;
+  for (int cc = 0; cc < nchunks; ++cc) mx = fmaxf(mx, cw[cc]);
+  __syncthreads();
+  if (threadIdx.x < nchunks) cw[threadIdx.x] = ptx::ex2(cw[threadIdx.x] - mx);
+  __syncthreads();
+  float l = 0.f;
+  for (int cc = 0; cc < nchunks; ++cc) l = fmaf(cw[cc], cl[cc], l);  // chunk order
+  const int i = threadIdx.x;
+  float ov = 0.f;
+  if (i < a.hd) {
+#pragma unroll 8
+    for (int cc = 0; cc < nchunks; ++cc) ov = fmaf(cw[cc], __ldcg(hp + cc * 130 + 2 + i), ov);
+    a.out[h * a.hd + i] = __float2bfloat16_rn(ov / l);
+  }
+  if (i == 0) a.cnt[h] = 0;
 }
 
 __global__ void dec_save_logits_kernel(const DecodeState* st, const float* logits, float* all, int V) {
@@ -367,8 +523,6 @@ __global__ void dec_save_logits_kernel(const DecodeState* st, const float* logit
   for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < V; i += gridDim.x * blockDim.x)
     dst[i] = logits[i];
 }
-
-int gemv_grid(int num_sms) { return num_sms * 2; }
 
 }  // namespace
 
@@ -386,22 +540,6 @@ cudaError_t dec_save_logits_launch(const DecodeState* st, const float* logits, f
                   all, V);
 }
 
-cudaError_t dec_shrink_launch(const DecShrink& a, const float* X, const bf16* g, const bf16* xin,
-                              int K, float eps, float scale, int num_sms, cudaStream_t s) {
-  static bool attr = false;
-  if (!attr) {
-    cudaError_t e = cudaFuncSetAttribute(dec_shrink_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         160 * 1024);
-    if (e != cudaSuccess) return e;
-    attr = true;
-  }
-  const int rows = a.nt * a.r;
-  int grid = (rows + DT / 32 - 1) / (DT / 32);
-  (void)num_sms;
-  return launch_k(dec_shrink_kernel, dim3(grid), dim3(DT), (size_t)K * 4, s, 1, a, X, g, xin, K, eps,
-                  scale);
-}
-
 cudaError_t dec_gemv_launch(const DecGemv& p, int mode, int num_sms, cudaStream_t s) {
   static bool attr[3] = {false, false, false};
   auto k = mode == DEC_QKV ? dec_gemv_kernel<DEC_QKV>
@@ -411,17 +549,22 @@ cudaError_t dec_gemv_launch(const DecGemv& p, int mode, int num_sms, cudaStream_
     if (e != cudaSuccess) return e;
     attr[mode] = true;
   }
-  int grid = gemv_grid(num_sms);
-  const int need = (p.npairs + DT / 32 - 1) / (DT / 32);
-  if (grid > need) grid = need;
-  return launch_k(k, dim3(grid), dim3(DT), (size_t)p.K * 4, s, 1, p);
+  // every warp gets the same number of row pairs: as many CTAs as fit at
+  // once (<= 4 per SM, shared-memory limited for long inputs), the pairs
+  // spread evenly over their warps
+  const int per_sm = 2;  // ~125 registers x 256 threads: two CTAs per SM
+  const int cap = num_sms * per_sm;  // co-resident CTAs (the shrink wait needs them all)
+  const int g_max = cap - p.nsh;
+  if (g_max < 1) return cudaErrorInvalidConfiguration;
+  int iters = (p.npairs + g_max * (DT / 32) - 1) / (g_max * (DT / 32));
+  iters = iters < 1 ? 1 : iters;
+  const int grid = (p.npairs + iters * (DT / 32) - 1) / (iters * (DT / 32));
+  return launch_k(k, dim3(p.nsh + grid), dim3(DT), (size_t)p.K * 4, s, 1, p);
 }
 
 cudaError_t dec_attn_launch(const DecAttn& a, int max_keys, cudaStream_t s) {
   const int nchunks = (max_keys + ACH - 1) / ACH;
-  cudaError_t e = launch_k(dec_attn_kernel, dim3(a.H, nchunks), dim3(DT), 0, s, 1, a);
-  if (e != cudaSuccess) return e;
-  return launch_k(dec_combine_kernel, dim3(a.H), dim3(128), 0, s, 1, a, nchunks);
+  return launch_k(dec_attn_kernel, dim3(a.H, nchunks), dim3(ATH), 0, s, 1, a);
 }
 
 }  // namespace tidal

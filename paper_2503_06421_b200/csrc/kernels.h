@@ -154,9 +154,11 @@ struct DecodeState {           // device-resident, read by every kernel of a ste
   int pos0;                    // prompt length (position of the first decoded input)
   int pad;
 };
+constexpr int DEC_TSPLIT = 8;      // K parts of the decode LoRA shrink
+constexpr int DEC_TSTRIDE = 7 * 64;  // floats between parts: T[part][target][j]
 struct DecShrink {             // T_t[j] = scale * A_t[j, :] . x   (t < nt <= 3, j < r)
   const bf16* A[3];
-  float* T[3];
+  float* T[3];                 // target t's slot; part q at T[t] + q * DEC_TSTRIDE
   int nt, r;
 };
 enum DecMode { DEC_QKV = 0, DEC_GU = 1, DEC_RESID = 2 };
@@ -171,7 +173,7 @@ struct DecGemv {
   int npairs;                  // row pairs (one per warp iteration)
   const bf16* W[3];            // QKV: Wq, Wk, Wv; GU: Wgate, Wup; RESID: W
   const bf16* B[3];            // LoRA B per segment [rows, r] (nullable)
-  const float* T[3];           // LoRA shrink outputs per segment (nullable)
+  const float* T[3];           // LoRA shrink outputs per segment (nullable; DEC_TSPLIT parts)
   int r;
   // QKV
   int nq, nkv, hd;
@@ -183,7 +185,14 @@ struct DecGemv {
   bf16* h;                     // [F]
   // RESID
   float* Xout;                 // [N] += W . x
+  // the LoRA shrink of this GEMV's input, computed by the first nsh CTAs of
+  // the launch (0: none); T[seg] above point into sh.T's slots
+  DecShrink sh;
+  float sh_scale;
+  int nsh;
+  int* sh_cnt;                 // monotonic count of finished shrink CTAs (0 at decode start)
 };
+inline int dec_shrink_ctas(int nt, int r) { return ((nt * r + 7) / 8) * DEC_TSPLIT; }
 struct DecAttn {
   const bf16* q;               // [H hd]
   const bf16 *kc, *vc;         // this layer's cache [cap][ldkv]
@@ -191,6 +200,7 @@ struct DecAttn {
   float scale_log2;
   const DecodeState* st;       // keys 0 .. st->pos
   float* part;                 // [H][chunks][2 + 128] partial (max, sum, o)
+  int* cnt;                    // [H] chunks finished (0 at rest)
   bf16* out;                   // [H hd]
 };
 cudaError_t dec_embed_launch(DecodeState* st, const bf16* E, float* X, int d, int32_t* toks_out,
@@ -198,8 +208,6 @@ cudaError_t dec_embed_launch(DecodeState* st, const bf16* E, float* X, int d, in
 cudaError_t dec_finish_launch(DecodeState* st, int32_t* toks_out, cudaStream_t s);
 cudaError_t dec_save_logits_launch(const DecodeState* st, const float* logits, float* all, int V,
                                    cudaStream_t s);
-cudaError_t dec_shrink_launch(const DecShrink& a, const float* X, const bf16* g, const bf16* xin,
-                              int K, float eps, float scale, int num_sms, cudaStream_t s);
 cudaError_t dec_gemv_launch(const DecGemv& p, int mode, int num_sms, cudaStream_t s);
 cudaError_t dec_attn_launch(const DecAttn& a, int max_keys, cudaStream_t s);
 

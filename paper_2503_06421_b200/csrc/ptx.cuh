@@ -176,6 +176,10 @@ __device__ __forceinline__ float rcp(float x) {
 // has completed (no-op without the launch attribute), then let the next kernel
 // start its prologue on SMs this grid frees.  Every kernel of the forward calls
 // pdl_begin() before its first global-memory access.
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_launch() {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
 __device__ __forceinline__ void pdl_begin() {
   asm volatile("griddepcontrol.wait;" ::: "memory");
   asm volatile("griddepcontrol.launch_dependents;" ::: "memory");

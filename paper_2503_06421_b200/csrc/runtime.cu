@@ -101,7 +101,8 @@ void Exec::enable_decode(int max_new) {
   cuda_check(cudaSetDevice(device), "cudaSetDevice");
   cuda_check(cudaStreamSynchronize(compute), "sync");
   Decode& D = dec;
-  void* ptrs[] = {D.kc, D.vc, D.q, D.att, D.h, D.T, D.part, D.st, D.toks, D.logits_all};
+  void* ptrs[] = {D.kc, D.vc, D.q, D.att, D.h, D.T, D.part, D.cnt, D.shcnt, D.st, D.toks,
+                  D.logits_all};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (D.gexec) cudaGraphExecDestroy(D.gexec);
@@ -115,8 +116,11 @@ void Exec::enable_decode(int max_new) {
   dalloc(D.q, nq * 2);
   dalloc(D.att, nq * 2);
   dalloc(D.h, (size_t)m.d_ff * 2);
-  dalloc(D.T, 7 * 64 * 4);
-  dalloc(D.part, (size_t)m.n_heads * ((D.cap + 255) / 256) * 130 * 4);
+  dalloc(D.T, (size_t)DEC_TSPLIT * DEC_TSTRIDE * 4);
+  dalloc(D.part, (size_t)m.n_heads * ((D.cap + 127) / 128) * 130 * 4);
+  dalloc(D.cnt, (size_t)m.n_heads * 4);
+  dalloc(D.shcnt, (size_t)m.n_layers * 4 * 4);
+  cuda_check(cudaMemset(D.cnt, 0, (size_t)m.n_heads * 4), "memset");
   dalloc(D.st, sizeof(DecodeState));
   dalloc(D.toks, (size_t)max_new * 4);
   dalloc(D.logits_all, (size_t)max_new * m.vocab * 4);
@@ -130,7 +134,8 @@ void Exec::destroy() {
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
   void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws, gemm_flags,
-                  dec.kc, dec.vc, dec.q, dec.att, dec.h, dec.T, dec.part, dec.st, dec.toks,
+                  dec.kc, dec.vc, dec.q, dec.att, dec.h, dec.T, dec.part, dec.cnt, dec.shcnt, dec.st,
+                  dec.toks,
                   dec.logits_all};
   if (dec.gexec) cudaGraphExecDestroy(dec.gexec);
   for (void* p : ptrs)
@@ -576,6 +581,7 @@ static void enqueue_decode_step(Exec& ex, const TensorTable& tt, float lora_scal
   Exec::Decode& D = ex.dec;
   cudaStream_t s = ex.compute;
   const int L = m.n_layers, d = m.d_model, hd = m.head_dim(), F = m.d_ff;
+  if ((D.cap + 127) / 128 > 128) fail(1, "decode cache longer than 16384 positions");
   const int nq = m.n_heads * hd, nkv = m.n_kv_heads * hd;
   const int r = tt.lora_rank;
   auto W = [&](int id) { return id >= 0 ? reinterpret_cast<const bf16*>(ex.wptr[id]) : nullptr; };
@@ -585,9 +591,9 @@ static void enqueue_decode_step(Exec& ex, const TensorTable& tt, float lora_scal
   auto Tp = [&](int t) { return T + 64 * t; };
   cuda_check(dec_embed_launch(D.st, W(tt.embed), ex.X, d, D.toks, s), "dec_embed");
   ++ex.launches;
-  auto shrink = [&](int l, std::initializer_list<int> ts, const float* X, const bf16* g,
-                    const bf16* xin, int K) {
-    DecShrink a;
+  // the LoRA shrink of a GEMV's input rides in the GEMV's launch (first CTAs)
+  auto shrink = [&](DecGemv& gv, int l, int which, std::initializer_list<int> ts) {
+    DecShrink& a = gv.sh;
     memset(&a, 0, sizeof a);
     for (int t : ts)
       if (la(l, t)) {
@@ -595,19 +601,20 @@ static void enqueue_decode_step(Exec& ex, const TensorTable& tt, float lora_scal
         a.T[a.nt] = Tp(t);
         ++a.nt;
       }
-    if (!a.nt) return;
     a.r = r;
-    cuda_check(dec_shrink_launch(a, X, g, xin, K, ex.eps, lora_scale, ex.num_sms, s), "dec_shrink");
-    ++ex.launches;
+    gv.nsh = a.nt ? dec_shrink_ctas(a.nt, r) : 0;
+    gv.sh_scale = lora_scale;
+    gv.sh_cnt = D.shcnt + 4 * l + which;
+    gv.st = D.st;
   };
   for (int l = 0; l < L; ++l) {
     const bf16 *g1 = W(tt.norm1[l]), *g2 = W(tt.norm2[l]);
     bf16* kc = D.kc + (size_t)l * D.cap * nkv;
     bf16* vc = D.vc + (size_t)l * D.cap * nkv;
     // ---- attention block ----
-    shrink(l, {T_Q, T_K, T_V}, ex.X, g1, nullptr, d);
     DecGemv g;
     memset(&g, 0, sizeof g);
+    shrink(g, l, 0, {T_Q, T_K, T_V});
     g.X = ex.X;
     g.g = g1;
     g.eps = ex.eps;
@@ -641,11 +648,12 @@ static void enqueue_decode_step(Exec& ex, const TensorTable& tt, float lora_scal
     at.scale_log2 = 1.4426950408889634f / sqrtf((float)hd);
     at.st = D.st;
     at.part = D.part;
+    at.cnt = D.cnt;
     at.out = D.att;
     cuda_check(dec_attn_launch(at, D.cap, s), "dec_attn");
-    shrink(l, {T_O}, nullptr, nullptr, D.att, nq);
     DecGemv o;
     memset(&o, 0, sizeof o);
+    shrink(o, l, 1, {T_O});
     o.xin = D.att;
     o.K = nq;
     o.N = d;
@@ -657,9 +665,9 @@ static void enqueue_decode_step(Exec& ex, const TensorTable& tt, float lora_scal
     o.Xout = ex.X;
     cuda_check(dec_gemv_launch(o, DEC_RESID, ex.num_sms, s), "dec_o");
     // ---- MLP block ----
-    shrink(l, {T_GATE, T_UP}, ex.X, g2, nullptr, d);
     DecGemv gu;
     memset(&gu, 0, sizeof gu);
+    shrink(gu, l, 2, {T_GATE, T_UP});
     gu.X = ex.X;
     gu.g = g2;
     gu.eps = ex.eps;
@@ -674,9 +682,9 @@ static void enqueue_decode_step(Exec& ex, const TensorTable& tt, float lora_scal
     gu.r = r;
     gu.h = D.h;
     cuda_check(dec_gemv_launch(gu, DEC_GU, ex.num_sms, s), "dec_gu");
-    shrink(l, {T_DOWN}, nullptr, nullptr, D.h, F);
     DecGemv dn;
     memset(&dn, 0, sizeof dn);
+    shrink(dn, l, 3, {T_DOWN});
     dn.xin = D.h;
     dn.K = F;
     dn.N = d;
@@ -687,7 +695,7 @@ static void enqueue_decode_step(Exec& ex, const TensorTable& tt, float lora_scal
     dn.r = r;
     dn.Xout = ex.X;
     cuda_check(dec_gemv_launch(dn, DEC_RESID, ex.num_sms, s), "dec_down");
-    ex.launches += 6;  // qkv, attention, combine, o, gu, down
+    ex.launches += 5;  // qkv, attention (+ in-kernel combine), o, gu, down
   }
   cuda_check(head_launch(ex.X, 0, 1, W(tt.fnorm), W(tt.head), m.vocab, d, ex.eps, ex.logits,
                          m.vocab, &D.st->key, 0, ex.num_sms, s),
@@ -715,6 +723,7 @@ void run_decode(Exec& ex, const TensorTable& tt, int n_steps, float lora_scale, 
   init.pos0 = D.prompt_len;
   cuda_check(cudaMemcpyAsync(D.st, &init, sizeof init, cudaMemcpyHostToDevice, s), "state");
   cuda_check(cudaMemcpyAsync(&D.st->key, ex.key, 8, cudaMemcpyDeviceToDevice, s), "state key");
+  cuda_check(cudaMemsetAsync(D.shcnt, 0, 4ull * 4 * ex.m.n_layers, s), "shrink counters");
   const auto gkey = std::make_tuple(akey, gen, tt.lora_rank, tt.lora_mask, lora_scale,
                                     want_logits ? 1 : 0);
   if (!D.gexec || D.gkey != gkey) {

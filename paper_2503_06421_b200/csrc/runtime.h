@@ -60,8 +60,10 @@ struct Exec {
     int max_new = 0, cap = 0;         // cache rows per layer = max_tokens + max_new
     bf16 *kc = nullptr, *vc = nullptr;  // [L][cap][nkv]
     bf16 *q = nullptr, *att = nullptr, *h = nullptr;
-    float* T = nullptr;               // [7][64] LoRA shrink outputs
+    float* T = nullptr;               // [DEC_TSPLIT][7][64] LoRA shrink parts
     float* part = nullptr;            // attention chunk partials
+    int* cnt = nullptr;               // attention chunks finished per head (0 at rest)
+    int* shcnt = nullptr;             // [L][4] fused-shrink CTA counts (reset per decode)
     DecodeState* st = nullptr;
     int32_t* toks = nullptr;          // [max_new]
     float* logits_all = nullptr;      // [max_new][V]

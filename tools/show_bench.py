@@ -9,3 +9,8 @@ for k, v in d['kernels'].items():
 r = d['roofline']
 print('roofline', r['kernel'], r['bound'], round(r['achieved']), r['peak'], round(r['frac'], 3))
 print('clocks', d['clocks'], 'cpu', d['cpu_baseline'] and round(d['cpu_baseline']['value']))
+if d.get('decode'):
+    x = d['decode']
+    print('decode', {k: (round(v, 3) if isinstance(v, float) else v) for k, v in x.items() if k != 'note'})
+if d.get('compute_bound_rho1'):
+    print('rho1', {k: round(v, 3) for k, v in d['compute_bound_rho1'].items()})
