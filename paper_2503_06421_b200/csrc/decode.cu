@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "launch.cuh"
@@ -35,12 +36,13 @@ __device__ __forceinline__ float warp_max(float v) {
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
   return v;
 }
+template <int NT = DT>
 __device__ __forceinline__ float block_sum(float v, float* red) {
   v = warp_sum(v);
   const int w = threadIdx.x >> 5, l = threadIdx.x & 31;
   if (l == 0) red[w] = v;
   __syncthreads();
-  float t = (threadIdx.x < DT / 32) ? red[threadIdx.x] : 0.f;
+  float t = (threadIdx.x < NT / 32) ? red[threadIdx.x] : 0.f;
   if (w == 0) t = warp_sum(t);
   if (threadIdx.x == 0) red[0] = t;
   __syncthreads();
@@ -54,32 +56,33 @@ __device__ __forceinline__ float block_sum(float v, float* red) {
 // 16-B vector loads, all of a thread's loads issued before any is consumed
 // (K <= 16384: at most 16 float4 per thread), the raw row parked in shared
 // memory between the two passes.
+template <int NT = DT>
 __device__ __forceinline__ void load_input(float* xs, const float* X, const bf16* g,
                                            const bf16* xin, int K, float eps, float* red) {
   if (X) {  // K = d_model <= 16384
     const float4* X4 = reinterpret_cast<const float4*>(X);
     float4* xs4 = reinterpret_cast<float4*>(xs);
     const int n4 = K >> 2;
-    float4 v[16];
+    float4 v[16 * DT / NT];
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int i = threadIdx.x + k * DT;
+    for (int k = 0; k < 16 * DT / NT; ++k) {
+      const int i = threadIdx.x + k * NT;
       if (i < n4) v[k] = X4[i];
     }
     float ss = 0.f;
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int i = threadIdx.x + k * DT;
+    for (int k = 0; k < 16 * DT / NT; ++k) {
+      const int i = threadIdx.x + k * NT;
       if (i < n4) {
         ss += v[k].x * v[k].x + v[k].y * v[k].y + v[k].z * v[k].z + v[k].w * v[k].w;
         xs4[i] = v[k];
       }
     }
-    const float inv = rsqrtf(block_sum(ss, red) / (float)K + eps);
+    const float inv = rsqrtf(block_sum<NT>(ss, red) / (float)K + eps);
     const uint2* g4 = reinterpret_cast<const uint2*>(g);
 #pragma unroll
-    for (int k = 0; k < 16; ++k) {
-      const int i = threadIdx.x + k * DT;
+    for (int k = 0; k < 16 * DT / NT; ++k) {
+      const int i = threadIdx.x + k * NT;
       if (i < n4) {
         const uint2 gw = g4[i];
         const __nv_bfloat162* gh = reinterpret_cast<const __nv_bfloat162*>(&gw);
@@ -94,16 +97,16 @@ __device__ __forceinline__ void load_input(float* xs, const float* X, const bf16
   } else {
     const uint4* x8 = reinterpret_cast<const uint4*>(xin);
     const int n8 = K >> 3;
-    for (int base = 0; base < n8; base += 8 * DT) {  // rounds of 8 loads per thread
+    for (int base = 0; base < n8; base += 8 * NT) {  // rounds of 8 loads per thread
     uint4 v[8];
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int i = base + threadIdx.x + k * DT;
+      const int i = base + threadIdx.x + k * NT;
       if (i < n8) v[k] = x8[i];
     }
 #pragma unroll
     for (int k = 0; k < 8; ++k) {
-      const int i = base + threadIdx.x + k * DT;
+      const int i = base + threadIdx.x + k * NT;
       if (i < n8) {
         const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&v[k]);
         float4* d = reinterpret_cast<float4*>(xs + 8 * i);
@@ -552,7 +555,7 @@ cudaError_t dec_gemv_launch(const DecGemv& p, int mode, int num_sms, cudaStream_
   // every warp gets the same number of row pairs: as many CTAs as fit at
   // once (<= 4 per SM, shared-memory limited for long inputs), the pairs
   // spread evenly over their warps
-  const int per_sm = 2;  // ~125 registers x 256 threads: two CTAs per SM
+  const int per_sm = 2;  // ~125 registers x 256 threads: two CTAs per SM (a 3-CTA bound spills)
   const int cap = num_sms * per_sm;  // co-resident CTAs (the shrink wait needs them all)
   const int g_max = cap - p.nsh;
   if (g_max < 1) return cudaErrorInvalidConfiguration;

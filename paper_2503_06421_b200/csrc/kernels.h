@@ -154,7 +154,7 @@ struct DecodeState {           // device-resident, read by every kernel of a ste
   int pos0;                    // prompt length (position of the first decoded input)
   int pad;
 };
-constexpr int DEC_TSPLIT = 8;      // K parts of the decode LoRA shrink
+constexpr int DEC_TSPLIT = 2;      // K parts of the decode LoRA shrink (CTAs per 8 rows)
 constexpr int DEC_TSTRIDE = 7 * 64;  // floats between parts: T[part][target][j]
 struct DecShrink {             // T_t[j] = scale * A_t[j, :] . x   (t < nt <= 3, j < r)
   const bf16* A[3];
