@@ -222,3 +222,51 @@ def test_fp32_close_to_fp64():
     r32 = F.forward(cfg, w, tok, a, 0x7F, 1.0, dtype=np.float32)["logits"]
     r64 = F.forward(cfg, w, tok, a, 0x7F, 1.0, dtype=np.float64)["logits"]
     assert np.abs(r32 - r64).max() < 1e-4
+
+
+# ----------------------------------------------------------------------------
+# decode: the reference the GPU decode is checked against is
+# the oracle's causal forward over prompt ++ generated tokens; pin it to an
+# independent incremental (KV-cached) decoder: HF transformers' greedy generate
+# ----------------------------------------------------------------------------
+def test_greedy_decode_matches_hf_generate():
+    torch = pytest.importorskip("torch")
+    tr = pytest.importorskip("transformers")
+    cfg = synth.ModelConfig("gqa", 2, 256, 8, 2, 512, 512, rope_theta=500000.0)
+    w = F.synth_weights(cfg, 5)
+    a = F.synth_adapter(cfg, 8, 6)
+    mask, scale, n_new = 0x7F, 0.5, 6
+    prompt = synth.prompt(cfg, 11, 2)
+    # oracle: greedy loop over the full causal forward
+    seq = list(prompt)
+    ours = []
+    for _ in range(n_new):
+        out = F.forward(cfg, w, np.array(seq), a, mask, scale, dtype=np.float64)
+        ours.append(out["logits"])
+        seq.append(out["token"])
+    # HF: LoRA merged into the weights, greedy generate with the KV cache
+    hc = tr.LlamaConfig(vocab_size=cfg.vocab, hidden_size=cfg.d_model,
+                        intermediate_size=cfg.d_ff, num_hidden_layers=cfg.n_layers,
+                        num_attention_heads=cfg.n_heads, num_key_value_heads=cfg.n_kv_heads,
+                        rms_norm_eps=cfg.rms_eps, tie_word_embeddings=False,
+                        rope_parameters={"rope_type": "default", "rope_theta": cfg.rope_theta},
+                        max_position_embeddings=8192, attention_bias=False, mlp_bias=False)
+    model = tr.LlamaForCausalLM(hc).float().eval()
+    sd = {}
+    for k in model.state_dict():
+        W = np.asarray(w(k), dtype=np.float64)
+        if k.endswith("_proj.weight"):
+            m = k[: -len(".weight")]
+            W = W + scale * (np.asarray(a(m + ".lora_B"), np.float64)
+                             @ np.asarray(a(m + ".lora_A"), np.float64))
+        sd[k] = torch.tensor(W, dtype=torch.float32)
+    model.load_state_dict(sd, strict=False)
+    with torch.no_grad():
+        g = model.generate(torch.tensor(prompt[None, :].astype(np.int64)), max_new_tokens=n_new,
+                           min_new_tokens=n_new, do_sample=False, use_cache=True,
+                           output_scores=True, return_dict_in_generate=True,
+                           pad_token_id=0, eos_token_id=None)
+    hf_tokens = g.sequences[0, len(prompt):].numpy()
+    assert list(hf_tokens) == seq[len(prompt):]
+    for t in range(n_new):
+        assert np.abs(g.scores[t][0].numpy().astype(np.float64) - ours[t]).max() < 1e-4
