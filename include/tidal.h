@@ -245,6 +245,35 @@ tidal_status tidal_invoke_decode(tidal_template* tpl, const tidal_adapter* a, in
                                  int32_t* tokens_out, float* logits_out,
                                  tidal_decode_stats* stats);
 
+/* ---- cross-process templates (§3, §5.1: a
+ * template server keeps function templates on the GPU and function processes
+ * fork from them over CUDA IPC) ----
+ * Device templates live on CUDA virtual memory: one address range per
+ * template backed by equal physical chunks (~1/64 of the layout, a multiple of
+ * the allocation granularity, <= 512 MB) with POSIX-fd shareable handles.
+ *
+ * tidal_template_export: fds[0..n) of the chunks lying wholly inside the
+ * resident prefix (address order) and shared_bytes = n * chunk.  With
+ * fds == NULL only *n_fds / *shared_bytes are returned (size query).  The
+ * caller owns the fds (close them after passing them on, e.g. SCM_RIGHTS).
+ * From then on the template refuses a resize below shared_bytes (importers
+ * read those bytes as their template); it must outlive its importers.
+ * Errors: INVALID (dry / no VMM / re-export of an import), BUFSZ (cap < n).
+ *
+ * tidal_template_import: the importer builds the same plan from the same
+ * (model, trace, opts) and maps the n_fds chunks READ-ONLY at offset 0 of its
+ * own layout range; the rest of its resident prefix (less than one chunk)
+ * is copied from its pinned pool and its streaming arena is private, so an
+ * invocation writes only private memory (copy-on-write by construction).
+ * Errors: STRUCTURE if the chunks do not cover exactly shared_bytes of this
+ * layout or shared_bytes exceeds the plan's resident prefix; INVALID for dry
+ * / tensor-parallel opts.  Everything else is as tidal_template_create. */
+tidal_status tidal_template_export(tidal_template* tpl, int* fds, int cap, int* n_fds,
+                                   uint64_t* shared_bytes);
+tidal_status tidal_template_import(tidal_model* model, const tidal_trace_rec* trace,
+                                   const tidal_template_opts* opts, const int* fds, int n_fds,
+                                   uint64_t shared_bytes, tidal_template** out);
+
 /* ---- pinned host memory for adapters / pools (cudaHostAlloc) ---- */
 tidal_status tidal_host_alloc(uint64_t bytes, void** out);
 void tidal_host_free(void* p);

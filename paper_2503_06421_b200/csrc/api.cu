@@ -115,6 +115,9 @@ struct tidal_template {
   int max_tokens = 0;
   uint8_t* pool = nullptr;
   uint8_t* dev = nullptr;
+  VmmBuf vmm;                  // dev's backing when CUDA VMM is available
+  uint64_t exported_bytes = 0; // prefix bytes handed to other processes (never rewritten)
+  uint64_t shared_bytes = 0;   // importer: prefix bytes mapped read-only from the exporter
   Exec ex;
   std::vector<cudaEvent_t> ev;
   cudaEvent_t e_start = nullptr, e_h2d0 = nullptr, e_h2d1 = nullptr, e_c0 = nullptr, e_end = nullptr;
@@ -365,8 +368,9 @@ static void warm_kernels(tidal_template* tp) {
   ex.cache.clear();
 }
 
-tidal_status tidal_template_create(tidal_model* m, const tidal_trace_rec* t,
-                                   const tidal_template_opts* opts, tidal_template** out) {
+static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
+                                    const tidal_template_opts* opts, const int* fds, int n_fds,
+                                    uint64_t shared_bytes, tidal_template** out) {
   TIDAL_TRY
   require(m && t && opts && out, "null argument");
   require(t->tt.n_base == m->tt.n_base, "trace is from a different model", TIDAL_ERR_STRUCTURE);
@@ -405,9 +409,23 @@ tidal_status tidal_template_create(tidal_model* m, const tidal_trace_rec* t,
         prev_end = o + tp->tt.t[id].bytes;
       }
     }
-    cuda_check(cudaMalloc((void**)&tp->dev, L), "cudaMalloc(template+arena)");
-    if (tp->plan.resident_end)
-      cuda_check(cudaMemcpy(tp->dev, tp->pool, tp->plan.resident_end, cudaMemcpyHostToDevice),
+    if (vmm_available()) {
+      vmm_alloc(tp->vmm, L, tp->device, fds, n_fds);
+      tp->dev = reinterpret_cast<uint8_t*>(tp->vmm.va);
+      if (n_fds)
+        require((uint64_t)n_fds * tp->vmm.chunk == shared_bytes &&
+                    shared_bytes <= tp->plan.resident_end,
+                "imported chunks do not match this template's layout / resident prefix",
+                TIDAL_ERR_STRUCTURE);
+    } else {
+      require(n_fds == 0, "CUDA virtual memory management unavailable: cannot import");
+      cuda_check(cudaMalloc((void**)&tp->dev, L), "cudaMalloc(template+arena)");
+    }
+    tp->shared_bytes = shared_bytes;
+    // the shared prefix is already on the device (the exporter's bytes)
+    if (tp->plan.resident_end > shared_bytes)
+      cuda_check(cudaMemcpy(tp->dev + shared_bytes, tp->pool + shared_bytes,
+                            tp->plan.resident_end - shared_bytes, cudaMemcpyHostToDevice),
                  "H2D resident prefix");
     for (cudaEvent_t* e : {&tp->e_start, &tp->e_h2d0, &tp->e_h2d1, &tp->e_c0, &tp->e_end})
       cuda_check(cudaEventCreate(e), "cudaEventCreate");
@@ -429,6 +447,36 @@ tidal_status tidal_template_create(tidal_model* m, const tidal_trace_rec* t,
   TIDAL_CATCH
 }
 
+tidal_status tidal_template_create(tidal_model* m, const tidal_trace_rec* t,
+                                   const tidal_template_opts* opts, tidal_template** out) {
+  return template_create(m, t, opts, nullptr, 0, 0, out);
+}
+
+tidal_status tidal_template_import(tidal_model* m, const tidal_trace_rec* t,
+                                   const tidal_template_opts* opts, const int* fds, int n_fds,
+                                   uint64_t shared_bytes, tidal_template** out) {
+  if (!opts || opts->device < 0) return set_err(TIDAL_ERR_INVALID, "import needs a device template");
+  if (n_fds < 1 || !fds) return set_err(TIDAL_ERR_INVALID, "no chunks to import");
+  if (opts->comm) return set_err(TIDAL_ERR_INVALID, "tensor-parallel import is not implemented");
+  return template_create(m, t, opts, fds, n_fds, shared_bytes, out);
+}
+
+tidal_status tidal_template_export(tidal_template* tp, int* fds, int cap, int* n_fds,
+                                   uint64_t* shared_bytes) {
+  TIDAL_TRY
+  require(tp && n_fds && shared_bytes, "null argument");
+  require(!tp->dry && tp->vmm.va, "export needs a device template on CUDA VMM");
+  require(tp->shared_bytes == 0, "an imported template cannot be re-exported");
+  const size_t n = tp->plan.resident_end / tp->vmm.chunk;  // chunks wholly inside the prefix
+  *n_fds = (int)n;
+  *shared_bytes = (uint64_t)n * tp->vmm.chunk;
+  if (!fds) return TIDAL_OK;  // size query
+  require(cap >= (int)n, "fd buffer too small", TIDAL_ERR_BUFSZ);
+  for (size_t i = 0; i < n; ++i) fds[i] = vmm_export_fd(tp->vmm, i);
+  tp->exported_bytes = std::max<uint64_t>(tp->exported_bytes, *shared_bytes);
+  TIDAL_CATCH
+}
+
 tidal_status tidal_template_resize(tidal_template* tp, const tidal_template_opts* opts) {
   TIDAL_TRY
   require(tp && opts, "null argument");
@@ -439,6 +487,9 @@ tidal_status tidal_template_resize(tidal_template* tp, const tidal_template_opts
   c.b_pcie_Bps = opts->b_pcie_Bps;
   const uint64_t old_end = tp->plan.resident_end;
   Plan p = make_plan(tp->tt, tp->tr, c);
+  // exported / imported prefix bytes are a shared template: they must stay resident
+  require(p.resident_end >= std::max(tp->exported_bytes, tp->shared_bytes),
+          "resize would stream into a prefix shared with other processes");
   if (!tp->dry) {
     cuda_check(cudaSetDevice(tp->device), "cudaSetDevice");
     cuda_check(cudaDeviceSynchronize(), "sync");
@@ -482,7 +533,10 @@ void tidal_template_destroy(tidal_template* tp) {
     for (cudaEvent_t e : tp->ev) cudaEventDestroy(e);
     for (cudaEvent_t e : {tp->e_start, tp->e_h2d0, tp->e_h2d1, tp->e_c0, tp->e_end})
       if (e) cudaEventDestroy(e);
-    if (tp->dev) cudaFree(tp->dev);
+    if (tp->vmm.va)
+      vmm_free(tp->vmm);
+    else if (tp->dev)
+      cudaFree(tp->dev);
     if (tp->arena) cudaFree(tp->arena);
     if (tp->scrub) cudaFree(tp->scrub);
     if (tp->d_sum) cudaFree(tp->d_sum);

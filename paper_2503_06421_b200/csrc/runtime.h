@@ -1,5 +1,6 @@
 // runtime.h — device execution context and the op launcher.
 #pragma once
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <map>
@@ -166,6 +167,20 @@ void run_forward(Exec& ex, const RunArgs& a);
 // ex.dec.logits_all; returns after enqueueing (compute stream).
 void run_decode(Exec& ex, const TensorTable& tt, int n_steps, float lora_scale, const void* akey,
                 uint64_t gen, bool want_logits);
+
+// Template device memory on CUDA VMM (vmm.cu): one virtual range backed by
+// equal physical chunks with POSIX-fd handles; the first n_shared chunks may
+// be imported read-only from another process's template.
+struct VmmBuf {
+  CUdeviceptr va = 0;
+  size_t size = 0, chunk = 0;
+  std::vector<CUmemGenericAllocationHandle> h;
+  int n_shared = 0, device = -1;
+};
+bool vmm_available();
+void vmm_alloc(VmmBuf& b, size_t bytes, int device, const int* fds, int n_shared);
+void vmm_free(VmmBuf& b);
+int vmm_export_fd(const VmmBuf& b, size_t chunk);
 
 // NUMA: bind the calling thread to the CPUs local to `device` (restored by the guard).
 struct NumaGuard {

@@ -16,6 +16,7 @@ _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtidal.so")
 
 OK = 0
+ERR_INVALID, ERR_STRUCTURE, ERR_BUFSZ = 1, 5, 8
 ERR_NAMES = {0: "OK", 1: "INVALID", 2: "OOM", 3: "CUDA", 4: "NCCL", 5: "STRUCTURE",
              6: "RESIDENCY", 7: "COW", 8: "BUFSZ", 9: "NUMERIC"}
 GROUPS_PER_LAYER, GROUPS_MAX_TRANSFERS, GROUPS_PER_TENSOR = 0, 1, 2
@@ -97,6 +98,10 @@ SIGNATURES = [
     ("tidal_trace_destroy", None, [VP]),
     ("tidal_trace_dump", C.c_int, [VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("tidal_template_create", C.c_int, [VP, VP, C.POINTER(TemplateOpts), C.POINTER(VP)]),
+    ("tidal_template_export", C.c_int, [VP, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int),
+                                        C.POINTER(C.c_uint64)]),
+    ("tidal_template_import", C.c_int, [VP, VP, C.POINTER(TemplateOpts), C.POINTER(C.c_int),
+                                        C.c_int, C.c_uint64, C.POINTER(VP)]),
     ("tidal_template_resize", C.c_int, [VP, C.POINTER(TemplateOpts)]),
     ("tidal_template_keep_alive", C.c_int, [VP]),
     ("tidal_set_load_order", C.c_int, [VP, C.c_int]),
@@ -246,12 +251,31 @@ def template_opts(resident_bytes: int = U64_MAX, eq1: bool = False, t_ttft_s: fl
 
 
 class Template:
-    def __init__(self, model: Model, trace: Trace, opts: TemplateOpts):
+    def __init__(self, model: Model, trace: Trace, opts: TemplateOpts,
+                 shared: Optional[Tuple[List[int], int]] = None):
+        """shared = (fds, shared_bytes) from another process's export(): map
+        those template chunks read-only instead of building the prefix."""
         h = VP()
         self._opts = opts
-        _check(lib().tidal_template_create(model.h, trace.h, C.byref(opts), C.byref(h)))
+        if shared is None:
+            _check(lib().tidal_template_create(model.h, trace.h, C.byref(opts), C.byref(h)))
+        else:
+            fds, nbytes = shared
+            arr = (C.c_int * len(fds))(*fds)
+            _check(lib().tidal_template_import(model.h, trace.h, C.byref(opts), arr, len(fds),
+                                               nbytes, C.byref(h)))
         self.h = h
         self.vocab = model.vocab
+
+    def export(self) -> Tuple[List[int], int]:
+        """(fds of the chunks inside the resident prefix, shared_bytes); the
+        caller owns the fds (pass them with socket.send_fds, then close)."""
+        n = C.c_int(0)
+        nb = C.c_uint64(0)
+        _check(lib().tidal_template_export(self.h, None, 0, C.byref(n), C.byref(nb)))
+        arr = (C.c_int * max(1, n.value))()
+        _check(lib().tidal_template_export(self.h, arr, n.value, C.byref(n), C.byref(nb)))
+        return list(arr[:n.value]), nb.value
 
     def resize(self, opts: TemplateOpts) -> None:
         _check(lib().tidal_template_resize(self.h, C.byref(opts)))
