@@ -391,7 +391,7 @@ cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
   const long items = (long)((p.S + BQ - 1) / BQ) * p.H * p.nseq;  // persistent: <= one CTA per SM
   const int grid = (int)(items < sms ? items : sms);
   if (grid <= 0) return cudaSuccess;
-  return launch_k(attn_tc_kernel, dim3(grid), dim3(NTH), SMEM, s, 1, p);
+  return launch_kt("attn", attn_tc_kernel, dim3(grid), dim3(NTH), SMEM, s, 1, p);
 }
 
 }  // namespace tidal

@@ -622,7 +622,7 @@ cudaError_t launch_t(const GemmParams& p, int num_sms, cudaStream_t s) {
   const int units = gemm_units(CG, MC, num_sms);
   const int grid = (p.total_tiles < units ? p.total_tiles : units) * CG * MC;
   if (grid <= 0) return cudaSuccess;
-  return launch_k(gemm_tc_kernel<EPI, BNT, CG, MC>, dim3(grid), dim3(NTHREADS),
+  return launch_kt(EPI == EPI_PARTIAL ? "shrink" : "gemm", gemm_tc_kernel<EPI, BNT, CG, MC>, dim3(grid), dim3(NTHREADS),
                   Cfg<EPI, BNT, CG>::SMEM_BYTES, s, CG * MC, p);
 }
 
@@ -710,6 +710,11 @@ int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms) {
 // K-block.  The per-part overhead (epilogue reductions, flag hand-off) was
 // measured at ~11 K-blocks (tools/gemm_bench.py, 13B O/down shapes), so at
 // S = 2048 one part wins and splitting pays only for short prompts.
+static void gemm_plan_resid_single(int M, int N, int K, int num_sms, int* bn_out) {
+  (void)K;
+  *bn_out = gemm_pick_bn(EPI_RESID, M, &N, 1, num_sms);
+}
+
 void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out) {
   const int cg = gemm_pick_cg(M), mc = gemm_pick_mc(M, num_sms);
   const long mt = gemm_m_tiles(M, cg, mc);
@@ -734,6 +739,15 @@ void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out)
         bk = ks;
       }
     }
+  }
+  static const bool no_split = [] {
+    const char* e = getenv("TIDAL_RESID_SPLIT");
+    return e && e[0] == '0';
+  }();
+  if (no_split && bk > 1) {  // best single-part width instead
+    gemm_plan_resid_single(M, N, K, num_sms, bn_out);
+    *ks_out = 1;
+    return;
   }
   *bn_out = bb;
   *ks_out = bk;
@@ -855,7 +869,7 @@ cudaError_t shrink_run(const ShrinkPlan& sp, float scale, int num_sms, cudaStrea
   cudaError_t e = gemm_launch(sp.g, EPI_PARTIAL, num_sms, s);
   if (e != cudaSuccess) return e;
   const int n = sp.M * sp.RT;
-  return launch_k(shrink_reduce_kernel, dim3((n + 255) / 256), dim3(256), 0, s, 1, sp.ws,
+  return launch_kt("reduce", shrink_reduce_kernel, dim3((n + 255) / 256), dim3(256), 0, s, 1, sp.ws,
                   sp.g.ksplit, sp.M, sp.RT, sp.r, sp.T[0], sp.T[1], sp.T[2], scale);
 }
 

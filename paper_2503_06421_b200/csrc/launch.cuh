@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdlib>
+#include <cstring>
 #include <utility>
 
 namespace tidal {
@@ -18,9 +19,29 @@ inline bool pdl_enabled() {
   return on;
 }
 
+// No PDL attribute for launches whose tag is in TIDAL_PDL_OFF (default
+// "shrink,reduce"): with early launch on the LoRA shrink and its reduce, the
+// 13B-width S = 4096 / r = 64 parity sweep hung intermittently (mbarrier
+// watchdog trap, 4 of 5 runs); with those two launched in plain stream
+// order it passed 8 of 8 and the same-box TTFT did not change.
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kt(const char* tag, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t s, int cluster_x, Args&&... args);
+
+inline bool pdl_off_for(const char* tag) {
+  static const char* off = getenv("TIDAL_PDL_OFF") ? getenv("TIDAL_PDL_OFF") : "shrink,reduce";
+  return tag && off && strstr(off, tag) != nullptr;
+}
+
 template <typename... KArgs, typename... Args>
 cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                      int cluster_x, Args&&... args) {
+  return launch_kt(nullptr, kernel, grid, block, smem, s, cluster_x, std::forward<Args>(args)...);
+}
+
+template <typename... KArgs, typename... Args>
+cudaError_t launch_kt(const char* tag, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
+                      cudaStream_t s, int cluster_x, Args&&... args) {
   cudaLaunchConfig_t cfg = {};
   cfg.gridDim = grid;
   cfg.blockDim = block;
@@ -35,7 +56,7 @@ cudaError_t launch_k(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t sme
     attr[n].val.clusterDim.z = 1;
     ++n;
   }
-  if (pdl_enabled()) {
+  if (pdl_enabled() && !pdl_off_for(tag)) {
     attr[n].id = cudaLaunchAttributeProgrammaticStreamSerialization;
     attr[n].val.programmaticStreamSerializationAllowed = 1;
     ++n;

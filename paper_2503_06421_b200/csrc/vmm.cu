@@ -15,6 +15,7 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <string>
 
@@ -94,7 +95,14 @@ void set_access(CUdeviceptr va, size_t bytes, int device, bool read_only) {
 
 }  // namespace
 
-bool vmm_available() { return drv().ok; }
+// TIDAL_VMM=0 falls back to cudaMalloc'd templates (no export / import)
+bool vmm_available() {
+  static const bool off = [] {
+    const char* e = getenv("TIDAL_VMM");
+    return e && e[0] == '0';
+  }();
+  return !off && drv().ok;
+}
 
 // chunk size: about 1/64 of the buffer, a multiple of the allocation
 // granularity, at most 512 MB (so an exported template is <= ~64 fds)
