@@ -424,9 +424,9 @@ __global__ void __launch_bounds__(ATH) dec_attn_kernel(DecAttn a) {
   if (k0 >= k1) return;  // past the current position: not part of this step
   const int nchunks = (nkeys + ACH - 1) / ACH;
   float* part = a.part + ((size_t)h * gridDim.y + c) * (2 + 128);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   for (int i = threadIdx.x; i < a.hd; i += ATH) qs[i] = __bfloat162float(a.q[h * a.hd + i]) * a.scale_log2;
   __syncthreads();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   float s = -INFINITY;
   const int k = k0 + threadIdx.x;
   if (k < k1) {
@@ -559,6 +559,8 @@ cudaError_t dec_gemv_launch(const DecGemv& p, int mode, int num_sms, cudaStream_
   const int cap = num_sms * per_sm;  // co-resident CTAs (the shrink wait needs them all)
   const int g_max = cap - p.nsh;
   if (g_max < 1) return cudaErrorInvalidConfiguration;
+  // every warp the same number of row pairs (measured equal or better than
+  // filling all co-resident CTAs with some warps one pair longer)
   int iters = (p.npairs + g_max * (DT / 32) - 1) / (g_max * (DT / 32));
   iters = iters < 1 ? 1 : iters;
   const int grid = (p.npairs + iters * (DT / 32) - 1) / (iters * (DT / 32));
