@@ -120,7 +120,8 @@ struct tidal_template {
   uint64_t shared_bytes = 0;   // importer: prefix bytes mapped read-only from the exporter
   Exec ex;
   std::vector<cudaEvent_t> ev;
-  cudaEvent_t e_start = nullptr, e_h2d0 = nullptr, e_h2d1 = nullptr, e_c0 = nullptr, e_end = nullptr;
+  cudaEvent_t e_start = nullptr, e_h2d0 = nullptr, e_h2d1 = nullptr, e_c0 = nullptr, e_end = nullptr,
+              e_tok = nullptr;
   uint8_t* arena = nullptr;  // adapter arena
   uint64_t arena_cap = 0;
   int debug = 0, debug_arg = -1;
@@ -427,7 +428,7 @@ static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
       cuda_check(cudaMemcpy(tp->dev + shared_bytes, tp->pool + shared_bytes,
                             tp->plan.resident_end - shared_bytes, cudaMemcpyHostToDevice),
                  "H2D resident prefix");
-    for (cudaEvent_t* e : {&tp->e_start, &tp->e_h2d0, &tp->e_h2d1, &tp->e_c0, &tp->e_end})
+    for (cudaEvent_t* e : {&tp->e_start, &tp->e_h2d0, &tp->e_h2d1, &tp->e_c0, &tp->e_end, &tp->e_tok})
       cuda_check(cudaEventCreate(e), "cudaEventCreate");
     tp->ensure_events(tp->plan.groups.size() + 2 * tp->shape.n_layers + 4);
     cuda_check(cudaMalloc((void**)&tp->d_sum, 64), "cudaMalloc");
@@ -531,7 +532,7 @@ void tidal_template_destroy(tidal_template* tp) {
     cudaSetDevice(tp->device);
     cudaDeviceSynchronize();
     for (cudaEvent_t e : tp->ev) cudaEventDestroy(e);
-    for (cudaEvent_t e : {tp->e_start, tp->e_h2d0, tp->e_h2d1, tp->e_c0, tp->e_end})
+    for (cudaEvent_t e : {tp->e_start, tp->e_h2d0, tp->e_h2d1, tp->e_c0, tp->e_end, tp->e_tok})
       if (e) cudaEventDestroy(e);
     if (tp->vmm.va)
       vmm_free(tp->vmm);
@@ -702,6 +703,12 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
   memcpy(ex.h_tok, host_tokens, 4ull * n_tokens);
   cuda_check(cudaEventRecord(tp->e_start, ex.compute), "event");
   cuda_check(cudaStreamWaitEvent(ex.copy, tp->e_start, 0), "wait");
+  // the prompt goes first on the (high-priority) copy stream: a token copy on
+  // the compute stream larger than ~24 KB was starved behind every weight
+  // group (measured: at S >= 7168 the prefill started after the last group)
+  cuda_check(cudaMemcpyAsync(ex.tok, ex.h_tok, 4ull * n_tokens, cudaMemcpyHostToDevice, ex.copy),
+             "H2D tokens");
+  cuda_check(cudaEventRecord(tp->e_tok, ex.copy), "event");
   // ---- copy stream: groups in traced access order, one event each ----
   cuda_check(cudaEventRecord(tp->e_h2d0, ex.copy), "event");
   const int skip = (tp->debug & TIDAL_DEBUG_SKIP_BARRIER) ? tp->debug_arg : -1;
@@ -734,8 +741,7 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
   }
   cuda_check(cudaEventRecord(tp->e_h2d1, ex.copy), "event");
   // ---- compute stream ----
-  cuda_check(cudaMemcpyAsync(ex.tok, ex.h_tok, 4ull * n_tokens, cudaMemcpyHostToDevice, ex.compute),
-             "H2D tokens");
+  cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_tok, 0), "wait tokens");
   if (tp->debug & 8) cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_h2d1, 0), "serial");
   cuda_check(cudaEventRecord(tp->e_c0, ex.compute), "event");
   RunArgs ra;
