@@ -21,8 +21,11 @@
 //               fp32 running row sums.  O lives in TMEM for the whole item;
 //               it is rescaled (each half its 64 columns) only when a row max
 //               grows by more than 2^8 (exact: O and l share the same stale
-//               max, P <= 256).  The epilogue reads O, frees it for the next
-//               item's first PV, then normalises and stores.
+//               max, P <= 256).  At an item's end they only publish the row
+//               sums (l_ready) and move on to the next item.
+//   warps 10..13 epilogue, one row per thread: read O (freeing it for the next
+//               item's first PV), O / l -> bf16, store — off the softmax path
+//               (measured 64 -> 60 us at 13B, S = 2048).
 // All barrier parities derive from per-CTA running counters (items, K/V
 // tiles, S/P buffers), never from the per-item tile index.
 // V is consumed as V^T [hd][S] (written transposed by the QKV GEMM epilogue),
@@ -48,13 +51,14 @@ constexpr int HALF = TILE / 2;
 constexpr int KST = 3, VST = 2;
 constexpr int OFF_Q = 0, OFF_K = OFF_Q + TILE, OFF_V = OFF_K + KST * TILE;
 constexpr int OFF_RED = OFF_V + VST * TILE;          // [2 slots][2 halves][128] row maxima
-constexpr int OFF_LSUM = OFF_RED + 2 * 2 * BQ * 4;   // [2 halves][128] final row sums
-constexpr int OFF_BAR = OFF_LSUM + 2 * BQ * 4;
-constexpr int N_BARS = 4 + 2 * KST + 2 * VST + 2 + 2 + 2;
+constexpr int OFF_LSUM = OFF_RED + 2 * 2 * BQ * 4;   // [2 items][2 halves][128] row sums
+constexpr int OFF_BAR = OFF_LSUM + 2 * 2 * BQ * 4;
+constexpr int N_BARS = 4 + 2 * KST + 2 * VST + 2 + 2 + 2 + 2;
 constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
 constexpr int SMEM = OFF_TMEM + 16 + 1024;
 constexpr int NSOFT = 256;           // softmax threads
-constexpr int NTH = 64 + NSOFT;
+constexpr int NEPI = 128;            // epilogue threads: O / l -> bf16, off the softmax path
+constexpr int NTH = 64 + NSOFT + NEPI;
 constexpr uint32_t COL_S0 = 0, COL_O = 256, COL_P = 384;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
@@ -102,6 +106,8 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
   // a single barrier could complete two phases before its waiter looks
   auto p_full = [&](int b) { return bars + 8u * (6 + 2 * KST + 2 * VST + b); };
   auto pv_done = [&](int b) { return bars + 8u * (8 + 2 * KST + 2 * VST + b); };
+  // the softmax warps publish an item's row sums; the epilogue warps take it
+  auto l_ready = [&](int b) { return bars + 8u * (10 + 2 * KST + 2 * VST + b); };
   uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
 
   const int nq = (p.S + BQ - 1) / BQ;
@@ -112,7 +118,8 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     ptx::prefetch_tmap(&p.vt);
     ptx::mbar_init(q_full, 1);
     ptx::mbar_init(q_empty, 1);
-    ptx::mbar_init(o_empty, NSOFT);
+    ptx::mbar_init(o_empty, NEPI);
+    for (int b = 0; b < 2; ++b) ptx::mbar_init(l_ready(b), NSOFT);
     for (int s = 0; s < KST; ++s) {
       ptx::mbar_init(k_full(s), 1);
       ptx::mbar_init(k_empty(s), 1);
@@ -217,6 +224,47 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       }
     }
     __syncwarp();
+  } else if (warp >= 2 + NSOFT / 32) {
+    // ===================== epilogue: O / l -> bf16 =====================
+    // one row per thread (TMEM lane quarter = warp & 3), all 128 columns; O is
+    // released as soon as it is read, so the next item's PVs and softmax run
+    // while these warps normalise and store
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t o_row = tmem + ((uint32_t)(q * 32) << 16) + COL_O;
+    const float* lsum = reinterpret_cast<const float*>(smem + OFF_LSUM);
+    int gt = 0;
+    for (int i = 0; item_at(p, nq, i, it); ++i) {
+      gt += it.qt + 1;
+      const int b = i & 1;
+      ptx::mbar_wait(l_ready(b), (i >> 1) & 1);
+      const float inv = 1.f / (lsum[(b * 2 + 0) * BQ + row] + lsum[(b * 2 + 1) * BQ + row]);
+      ptx::mbar_wait(pv_done((gt - 1) & 1), ((gt - 1) >> 1) & 1);
+      ptx::tc_fence_after();
+      const int qi = it.qt * BQ + row;
+      bf16* out = p.out + (size_t)(it.z * p.S + qi) * p.ldo + it.h * HD;
+#pragma unroll 1
+      for (int c = 0; c < 4; ++c) {
+        uint32_t r[32];
+        ptx::tmem_ld32(o_row + c * 32, r);
+        ptx::tmem_ld_wait();
+        if (c == 3) {
+          ptx::tc_fence_before();
+          ptx::mbar_arrive(o_empty);  // O read: the next item's first PV may overwrite it
+        }
+        if (qi < p.S) {
+#pragma unroll
+          for (int k = 0; k < 4; ++k) {
+            uint4 w;
+            w.x = pack_bf16x2(__uint_as_float(r[8 * k + 0]) * inv, __uint_as_float(r[8 * k + 1]) * inv);
+            w.y = pack_bf16x2(__uint_as_float(r[8 * k + 2]) * inv, __uint_as_float(r[8 * k + 3]) * inv);
+            w.z = pack_bf16x2(__uint_as_float(r[8 * k + 4]) * inv, __uint_as_float(r[8 * k + 5]) * inv);
+            w.w = pack_bf16x2(__uint_as_float(r[8 * k + 6]) * inv, __uint_as_float(r[8 * k + 7]) * inv);
+            *reinterpret_cast<uint4*>(out + c * 32 + k * 8) = w;
+          }
+        }
+      }
+    }
   } else {
     // ===================== softmax: two column halves =====================
     const int half = (warp - 2) >> 2;  // 0: keys 0..63, 1: keys 64..127 of each tile
@@ -224,7 +272,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
     const int row = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
     float* red = reinterpret_cast<float*>(smem + OFF_RED);    // [slot][half][row]
-    float* lsum = reinterpret_cast<float*>(smem + OFF_LSUM);  // [half][row]
+    float* lsum = reinterpret_cast<float*>(smem + OFF_LSUM);  // [item&1][half][row]
     const uint32_t o_col = tmem + lane_base + COL_O + half * 64;
     int gt = 0;  // S/P tiles consumed by this CTA
     for (int i = 0; item_at(p, nq, i, it); ++i) {
@@ -311,35 +359,10 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full(b));
       }
-      // epilogue: combine the half-row sums, O / l -> bf16 (each half its 64 columns)
-      lsum[half * BQ + row] = l;
-      softmax_bar();
-      const float inv = 1.f / (l + lsum[(half ^ 1) * BQ + row]);
-      ptx::mbar_wait(pv_done((gt - 1) & 1), ((gt - 1) >> 1) & 1);
-      ptx::tc_fence_after();
-      uint32_t r[2][32];
-      ptx::tmem_ld32(o_col, r[0]);
-      ptx::tmem_ld32(o_col + 32, r[1]);
-      ptx::tmem_ld_wait();
-      ptx::tc_fence_before();
-      ptx::mbar_arrive(o_empty);  // O may be overwritten by the next item's first PV
-      if (qi < p.S) {
-        bf16* out = p.out + (size_t)(it.z * p.S + qi) * p.ldo + it.h * HD + half * 64;
-#pragma unroll
-        for (int c = 0; c < 2; ++c) {
-#pragma unroll
-          for (int k = 0; k < 4; ++k) {
-            uint4 w;
-            w.x = pack_bf16x2(__uint_as_float(r[c][8 * k + 0]) * inv, __uint_as_float(r[c][8 * k + 1]) * inv);
-            w.y = pack_bf16x2(__uint_as_float(r[c][8 * k + 2]) * inv, __uint_as_float(r[c][8 * k + 3]) * inv);
-            w.z = pack_bf16x2(__uint_as_float(r[c][8 * k + 4]) * inv, __uint_as_float(r[c][8 * k + 5]) * inv);
-            w.w = pack_bf16x2(__uint_as_float(r[c][8 * k + 6]) * inv, __uint_as_float(r[c][8 * k + 7]) * inv);
-            *reinterpret_cast<uint4*>(out + c * 32 + k * 8) = w;
-          }
-        }
-      }
-      // lsum is rewritten by the next item's epilogue only after that item's
-      // per-tile softmax barriers, which both halves pass after reading it
+      // hand the row sums to the epilogue warps (double-buffered by item: the
+      // epilogue of item i has read them before item i+2's softmax can end)
+      lsum[((i & 1) * 2 + half) * BQ + row] = l;
+      ptx::mbar_arrive(l_ready(i & 1));
     }
   }
   ptx::tc_fence_before();
