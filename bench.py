@@ -126,6 +126,12 @@ def oracle_sample(cfg, S, r, seed=0):
     return time.perf_counter() - t
 
 
+def workload_name(config, S, r):
+    """The workload label both arms report (BASELINE.json configs[2] shape)."""
+    return (f"Llama2-{config.upper()}-shaped prefill, S={S}, LoRA r{r} attach, template-start "
+            f"(BASELINE.json configs[2])")
+
+
 def run_reference(args):
     """--impl reference: the oracle (numpy fp32, plain definition) on the host
     cores, bounded samples of the same workload (1 of L layers, extrapolated)."""
@@ -144,7 +150,12 @@ def run_reference(args):
         "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded splitmix64 weights, uniform prompt)",
-        "config": {"workload": f"{args.config} S={args.seq} LoRA r{args.rank} (oracle sample)"},
+        "config": {"workload": workload_name(args.config, args.seq, args.rank),
+                   "seq_len": args.seq, "lora_rank": args.rank,
+                   "parallelism": f"tp{args.gpus}" if args.gpus > 1 else "single",
+                   "reference": "oracle/ (numpy fp32 plain-definition forward) on the host "
+                                "cores: the paper ships no code, so the oracle is this tier's "
+                                "reference arm (DESIGN.md §10)"},
         "cpu_baseline": {"value": ms, "unit": "ms", "cores": cores, "kind": "oracle",
                          "sample": sample},
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
@@ -365,8 +376,7 @@ def main():
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ttft,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded splitmix64 random-init bf16 weights + LoRA, uniform prompt)",
-        "config": {"workload": f"Llama2-{args.config.upper()}-shaped prefill, S={S}, "
-                               f"LoRA r{r} attach, template-start (BASELINE.json configs[2])",
+        "config": {"workload": workload_name(args.config, S, r),
                    "seq_len": S, "lora_rank": r, "resident_rule": args.rho,
                    "rho": s0["bytes_resident"] / max(1, s0["bytes_resident"] + s0["bytes_streamed"]),
                    "group_policy": args.policy, "parallelism": f"tp{world}" if world > 1 else "single",
