@@ -20,16 +20,16 @@ inline bool pdl_enabled() {
 }
 
 // No PDL attribute for launches whose tag is in TIDAL_PDL_OFF (default
-// "shrink,reduce"): with early launch on the LoRA shrink and its reduce, the
-// 13B-width S = 4096 / r = 64 parity sweep hung intermittently (mbarrier
-// watchdog trap, 4 of 5 runs); with those two launched in plain stream
-// order it passed 8 of 8 and the same-box TTFT did not change.
+// "reduce"): with early launch on the LoRA-shrink reduce, the 13B-width
+// S = 4096 / r = 64 parity sweep hung intermittently (watchdog trap, 4 of 5
+// runs); bisected per kernel class, the reduce alone in plain stream order
+// passes 10 of 10 with the same-box TTFT unchanged.
 template <typename... KArgs, typename... Args>
 cudaError_t launch_kt(const char* tag, void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem,
                       cudaStream_t s, int cluster_x, Args&&... args);
 
 inline bool pdl_off_for(const char* tag) {
-  static const char* off = getenv("TIDAL_PDL_OFF") ? getenv("TIDAL_PDL_OFF") : "shrink,reduce";
+  static const char* off = getenv("TIDAL_PDL_OFF") ? getenv("TIDAL_PDL_OFF") : "reduce";
   return tag && off && strstr(off, tag) != nullptr;
 }
 
