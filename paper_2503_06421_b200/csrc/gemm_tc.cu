@@ -681,26 +681,33 @@ int gemm_pick_mc(int M, int num_sms) {
 
 int gemm_m_tiles(int M, int cg, int mc) { return (M + BM * cg * mc - 1) / (BM * cg * mc); }
 
-int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms) {
-  if (epi == EPI_SILU) return 128;
-  const int cg = gemm_pick_cg(M), mc = gemm_pick_mc(M, num_sms);
-  const int mt = gemm_m_tiles(M, cg, mc);
-  const int units = gemm_units(cg, mc, num_sms);
-  static const int cands[] = {256, 192, 128};
-  int best = 256;
+int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms, int* cg_out) {
+  const int cg0 = gemm_pick_cg(M);
+  int best = 256, best_cg = cg0;
   double best_cost = 1e30;
-  for (int bn : cands) {
-    if (epi == EPI_ROPE && bn == 192) continue;  // RoPE tiles must hold whole heads
-    long tiles = 0;
-    for (int s = 0; s < nseg; ++s) tiles += (long)mt * ((seg_n[s] + bn - 1) / bn);
-    const long waves = (tiles + units - 1) / units;
-    // 128-wide tiles pay ~15% more per MAC (A-operand smem traffic per MMA doubles)
-    const double cost = (double)waves * bn * (bn == 128 ? 1.15 : 1.0);
-    if (cost < best_cost - 1e-9) {
-      best_cost = cost;
-      best = bn;
+  for (int cg = cg0; cg >= (cg_out ? 1 : cg0); --cg) {
+    const int mc = cg == 2 ? gemm_pick_mc(M, num_sms) : 1;
+    const int mt = gemm_m_tiles(M, cg, mc);
+    const int units = gemm_units(cg, mc, num_sms);
+    static const int cands[] = {256, 192, 128};
+    for (int bn : cands) {
+      if (epi == EPI_SILU && bn != 128) continue;
+      if (epi == EPI_ROPE && bn == 192) continue;  // RoPE tiles must hold whole heads
+      long tiles = 0;
+      for (int s = 0; s < nseg; ++s) tiles += (long)mt * ((seg_n[s] + bn - 1) / bn);
+      const long waves = (tiles + units - 1) / units;
+      // 128-wide tiles pay ~15% more per MAC (A-operand smem traffic per MMA
+      // doubles); single-CTA tiles ~10% (each CTA loads its whole B tile)
+      const double cost = (double)waves * bn * (bn == 128 ? 1.15 : 1.0) *
+                          (cg == 1 && cg0 == 2 ? 1.1 : 1.0);
+      if (cost < best_cost - 1e-9) {
+        best_cost = cost;
+        best = bn;
+        best_cg = cg;
+      }
     }
   }
+  if (cg_out) *cg_out = best_cg;
   return best;
 }
 
@@ -715,7 +722,8 @@ static void gemm_plan_resid_single(int M, int N, int K, int num_sms, int* bn_out
   *bn_out = gemm_pick_bn(EPI_RESID, M, &N, 1, num_sms);
 }
 
-void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out) {
+void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out, int* cg_out) {
+  if (cg_out) *cg_out = gemm_pick_cg(M);
   const int cg = gemm_pick_cg(M), mc = gemm_pick_mc(M, num_sms);
   const long mt = gemm_m_tiles(M, cg, mc);
   const long units = gemm_units(cg, mc, num_sms);
@@ -737,6 +745,22 @@ void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out)
         best = cost;
         bb = bn;
         bk = ks;
+      }
+    }
+  }
+  // short prompts: one wave of whole-K single-CTA tiles beats rounds of pairs
+  // and split-K (13B O/down, tools/gemm_bench.py --small-sweep: S = 867
+  // 42 / 103 us against 57 / 137 us; S = 640 35 / 84 against 38 / 88); the
+  // narrower tile first (more SMs streaming), 128-wide tiles never pay
+  if (cg_out && cg == 2) {
+    const long mt1 = (M + BM - 1) / BM;
+    for (int bn : {192, 256}) {
+      const long tiles = mt1 * ((N + bn - 1) / bn);
+      if (tiles <= num_sms && tiles <= GEMM_MAX_FLAGS) {
+        *bn_out = bn;
+        *ks_out = 1;
+        *cg_out = 1;
+        return;
       }
     }
   }

@@ -75,7 +75,9 @@ int gemm_b_box(int epi, int bn, int cg, int mc = 1);
 // EPI_RESID: N-tile width and ordered split-K parts (GemmParams::ksplit and
 // kblocks_per_split = ceil(nk / ks)) for an M x N x K residual GEMM.
 constexpr int GEMM_MAX_FLAGS = 16384;
-void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn, int* ks);
+// cg_out (optional): also choose the CTA group — single-CTA tiles when they fit
+// one wave and pair tiles would not (short prompts); else the pair default.
+void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn, int* ks, int* cg_out = nullptr);
 int gemm_tb_box(int epi, int bn, int cg, int mc = 1);
 
 // LoRA shrink on tensor cores: T_t = bf16(scale * X A_t^T) for nt targets
@@ -109,7 +111,9 @@ cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s);
 
 // N-tile width minimising (waves x tile width) on num_sms SMs; the W/lora_B
 // tensor maps must use box rows = the returned value (128 for EPI_SILU).
-int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms);
+// cg_out (optional): choose the CTA group too (pairs pay less shared-memory
+// traffic per MAC; single CTAs double the tile count for short prompts).
+int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms, int* cg_out = nullptr);
 
 // Host helpers (gemm_tc.cu).
 bool tma_init();  // resolve cuTensorMapEncodeTiled through the runtime

@@ -166,8 +166,6 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
   const int nq = m.n_heads * hd / world, nkv = m.n_kv_heads * hd / world;
   const int F = m.d_ff / world;
   const int r = tt.lora_rank;
-  const int cg = gemm_pick_cg(S), mc = gemm_pick_mc(S, num_sms);
-  const int mt = gemm_m_tiles(S, cg, mc);
   std::vector<LayerLaunch> v(L);
   auto W = [&](int id) { return wptr[id]; };
   for (int l = 0; l < L; ++l) {
@@ -181,24 +179,24 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     int col = 0;
     q.lora_r = 0;
     q.total_tiles = 0;
-    q.bn = gemm_pick_bn(EPI_ROPE, S, segn, 3, num_sms);
-    q.cg = cg;
-    q.mc = mc;
+    q.bn = gemm_pick_bn(EPI_ROPE, S, segn, 3, num_sms, &q.cg);
+    q.mc = q.cg == 2 ? gemm_pick_mc(S, num_sms) : 1;
+    const int qmt = gemm_m_tiles(S, q.cg, q.mc);
     for (int s = 0; s < 3; ++s) {
       q.seg[s].n = segn[s];
       q.seg[s].out_col = col;
       q.seg[s].rope = s < 2;
       col += segn[s];
-      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, gemm_b_box(EPI_ROPE, q.bn, cg, mc));
+      tmap(&q.b[s], W(tt.proj[l][tg[s]]), segn[s], d, gemm_b_box(EPI_ROPE, q.bn, q.cg, q.mc));
       const int la = tt.lora_a[l][tg[s]];
       q.seg[s].lora = la >= 0;
       if (la >= 0) {
         q.lora_r = r;
         tmap(&q.ta[s], T[tg[s]], S, r, 128);
-        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, gemm_tb_box(EPI_ROPE, q.bn, cg, mc));
+        tmap(&q.tb[s], W(tt.lora_b[l][tg[s]]), segn[s], r, gemm_tb_box(EPI_ROPE, q.bn, q.cg, q.mc));
       }
       q.n_tiles[s] = (segn[s] + q.bn - 1) / q.bn;
-      q.total_tiles += q.n_tiles[s] * mt;
+      q.total_tiles += q.n_tiles[s] * qmt;
     }
     q.nseg = 3;
     q.seg[2].vt = hd == 128;  // V^T for the tcgen05 attention
@@ -212,7 +210,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     q.vt_ld = vt_ld;
     q.M = S;
     q.K = d;
-    q.m_tiles = mt;
+    q.m_tiles = qmt;
     q.out = QKV;
     q.ldo = nq + 2 * nkv;
     q.rope = rope;
@@ -222,79 +220,83 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     GemmParams& o = ll.o;
     memset(&o, 0, sizeof o);
     int ks = 1;
-    gemm_plan_resid(S, d, nq, num_sms, &o.bn, &ks);
+    gemm_plan_resid(S, d, nq, num_sms, &o.bn, &ks, &o.cg);
     o.ksplit = ks;
     o.kblocks_per_split = ((nq + GEMM_BK - 1) / GEMM_BK + ks - 1) / ks;
     o.flags = gemm_flags;
-    o.cg = cg;
-    o.mc = mc;
+    o.mc = o.cg == 2 ? gemm_pick_mc(S, num_sms) : 1;
+    const int omt = gemm_m_tiles(S, o.cg, o.mc);
     tmap(&o.a, O, S, nq, 128);
-    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, gemm_b_box(EPI_RESID, o.bn, cg, mc));
+    tmap(&o.b[0], W(tt.proj[l][T_O]), d, nq, gemm_b_box(EPI_RESID, o.bn, o.cg, o.mc));
     o.seg[0].n = d;
     o.seg[0].lora = tt.lora_a[l][T_O] >= 0;
     if (o.seg[0].lora) {
       o.lora_r = r;
       tmap(&o.ta[0], T[T_O], S, r, 128);
-      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, gemm_tb_box(EPI_RESID, o.bn, cg, mc));
+      tmap(&o.tb[0], W(tt.lora_b[l][T_O]), d, r, gemm_tb_box(EPI_RESID, o.bn, o.cg, o.mc));
     }
     o.nseg = 1;
     o.M = S;
     o.K = nq;
-    o.m_tiles = mt;
+    o.m_tiles = omt;
     o.n_tiles[0] = (d + o.bn - 1) / o.bn;
-    o.total_tiles = o.n_tiles[0] * mt;
+    o.total_tiles = o.n_tiles[0] * omt;
     o.out = X;
     o.ldo = d;
     // ---- gate/up + SiLU*mul ----
     GemmParams& g = ll.gu;
     memset(&g, 0, sizeof g);
+    {
+      const int fn = F;
+      g.bn = gemm_pick_bn(EPI_SILU, S, &fn, 1, num_sms, &g.cg);
+    }
+    g.mc = g.cg == 2 ? gemm_pick_mc(S, num_sms) : 1;
+    const int gmt = gemm_m_tiles(S, g.cg, g.mc);
     tmap(&g.a, Xn, S, d, 128);
-    tmap(&g.b[0], W(tt.proj[l][T_GATE]), F, d, gemm_b_box(EPI_SILU, 128, cg, mc));
-    tmap(&g.b[1], W(tt.proj[l][T_UP]), F, d, gemm_b_box(EPI_SILU, 128, cg, mc));
+    tmap(&g.b[0], W(tt.proj[l][T_GATE]), F, d, gemm_b_box(EPI_SILU, 128, g.cg, g.mc));
+    tmap(&g.b[1], W(tt.proj[l][T_UP]), F, d, gemm_b_box(EPI_SILU, 128, g.cg, g.mc));
     g.seg[0].n = F;
     g.seg[0].lora = tt.lora_a[l][T_GATE] >= 0;
     if (g.seg[0].lora) {
       g.lora_r = r;
       tmap(&g.ta[0], T[T_GATE], S, r, 128);
       tmap(&g.ta[1], T[T_UP], S, r, 128);
-      tmap(&g.tb[0], W(tt.lora_b[l][T_GATE]), F, r, gemm_tb_box(EPI_SILU, 128, cg, mc));
-      tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, gemm_tb_box(EPI_SILU, 128, cg, mc));
+      tmap(&g.tb[0], W(tt.lora_b[l][T_GATE]), F, r, gemm_tb_box(EPI_SILU, 128, g.cg, g.mc));
+      tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, gemm_tb_box(EPI_SILU, 128, g.cg, g.mc));
     }
     g.nseg = 1;
     g.bn = 128;
-    g.cg = cg;
-    g.mc = mc;
     g.M = S;
     g.K = d;
-    g.m_tiles = mt;
+    g.m_tiles = gmt;
     g.n_tiles[0] = (F + 127) / 128;
-    g.total_tiles = g.n_tiles[0] * mt;
+    g.total_tiles = g.n_tiles[0] * gmt;
     g.out = Hb;
     g.ldo = F;
     // ---- down (+ residual) ----
     GemmParams& dn = ll.down;
     memset(&dn, 0, sizeof dn);
-    gemm_plan_resid(S, d, F, num_sms, &dn.bn, &ks);
+    gemm_plan_resid(S, d, F, num_sms, &dn.bn, &ks, &dn.cg);
     dn.ksplit = ks;
     dn.kblocks_per_split = ((F + GEMM_BK - 1) / GEMM_BK + ks - 1) / ks;
     dn.flags = gemm_flags;
-    dn.cg = cg;
-    dn.mc = mc;
+    dn.mc = dn.cg == 2 ? gemm_pick_mc(S, num_sms) : 1;
+    const int dmt = gemm_m_tiles(S, dn.cg, dn.mc);
     tmap(&dn.a, Hb, S, F, 128);
-    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, gemm_b_box(EPI_RESID, dn.bn, cg, mc));
+    tmap(&dn.b[0], W(tt.proj[l][T_DOWN]), d, F, gemm_b_box(EPI_RESID, dn.bn, dn.cg, dn.mc));
     dn.seg[0].n = d;
     dn.seg[0].lora = tt.lora_a[l][T_DOWN] >= 0;
     if (dn.seg[0].lora) {
       dn.lora_r = r;
       tmap(&dn.ta[0], T[T_DOWN], S, r, 128);
-      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, gemm_tb_box(EPI_RESID, dn.bn, cg, mc));
+      tmap(&dn.tb[0], W(tt.lora_b[l][T_DOWN]), d, r, gemm_tb_box(EPI_RESID, dn.bn, dn.cg, dn.mc));
     }
     dn.nseg = 1;
     dn.M = S;
     dn.K = F;
-    dn.m_tiles = mt;
+    dn.m_tiles = dmt;
     dn.n_tiles[0] = (d + dn.bn - 1) / dn.bn;
-    dn.total_tiles = dn.n_tiles[0] * mt;
+    dn.total_tiles = dn.n_tiles[0] * dmt;
     dn.out = X;
     dn.ldo = d;
     // ---- LoRA shrinks (T = s x A^T) for the targets sharing each input ----

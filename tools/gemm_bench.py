@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--S", type=int, default=2048)
 ap.add_argument("--lora", type=int, default=16)
+ap.add_argument("--small-sweep", action="store_true", help="all bn x cg x split-K variants")
 ap.add_argument("--resid-sweep", action="store_true",
                 help="O/down only: bn x split-K grid, 3 interleaved passes, median")
 args = ap.parse_args()
@@ -66,6 +67,15 @@ def bench(name, epi, bn, cg, mc, N_list, K, flops, ks=0):
     print(f"{name:8s} bn={bn:3d} cg={cg} mc={mc} ks={ks}  {best * 1e3:8.1f} us  {flops / best / 1e9:7.0f} TF/s",
           flush=True)
 
+
+if args.small_sweep:  # every (bn, cg, ks) for the given S (short prompts)
+    for name, epi, N, K, bns in (("qkv", 1, [d, d, d], d, (128, 256)), ("gate_up", 2, [F], d, (128,)),
+                                 ("o", 3, [d], d, (128, 192, 256)), ("down", 3, [d], F, (128, 192, 256))):
+        for bn in bns:
+            for cg in (1, 2):
+                for ks in ((0,) if epi != 3 else (1, 2, 3, 4)):
+                    bench(name, epi, bn, cg, 1, N, K, 2.0 * M * sum(N) * K * (2 if epi == 2 else 1), ks)
+    sys.exit(0)
 
 if args.resid_sweep:
     import statistics
