@@ -131,7 +131,7 @@ def test_gemm_multicast_clusters(T, epi, bn, M, mc):
         assert np.abs(X.cpu().numpy() - (X0 + ref)).max() <= 2e-4 * np.abs(X0 + ref).max()
 
 
-@pytest.mark.parametrize("cg,M", [(1, 100), (2, 260), (2, 777)])
+@pytest.mark.parametrize("cg,M", [(1, 100), (2, 260), (2, 777), (1, 867)])
 @pytest.mark.parametrize("ks", [1, 2, 3, 5])
 @pytest.mark.parametrize("bn", [192, 256])
 def test_gemm_residual_split_k(T, bn, ks, cg, M):
