@@ -22,6 +22,7 @@ ap = argparse.ArgumentParser()
 ap.add_argument("--reps", type=int, default=20)
 ap.add_argument("--S", type=int, default=2048)
 ap.add_argument("--lora", type=int, default=16)
+ap.add_argument("--mc-sweep", action="store_true", help="residual GEMMs, mc 1 vs 2")
 ap.add_argument("--small-sweep", action="store_true", help="all bn x cg x split-K variants")
 ap.add_argument("--resid-sweep", action="store_true",
                 help="O/down only: bn x split-K grid, 3 interleaved passes, median")
@@ -67,6 +68,14 @@ def bench(name, epi, bn, cg, mc, N_list, K, flops, ks=0):
     print(f"{name:8s} bn={bn:3d} cg={cg} mc={mc} ks={ks}  {best * 1e3:8.1f} us  {flops / best / 1e9:7.0f} TF/s",
           flush=True)
 
+
+if args.mc_sweep:  # CTA-pair clusters sharing the A tile (TMA multicast), residual GEMMs
+    for name, N, K in (("o", d, d), ("down", d, F)):
+        for bn in (192, 256):
+            for mc in (1, 2):
+                for ks in (1, 2, 3):
+                    bench(name, 3, bn, 2, mc, [N], K, 2.0 * M * N * K, ks)
+    sys.exit(0)
 
 if args.small_sweep:  # every (bn, cg, ks) for the given S (short prompts)
     for name, epi, N, K, bns in (("qkv", 1, [d, d, d], d, (128, 256)), ("gate_up", 2, [F], d, (128,)),
