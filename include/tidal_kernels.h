@@ -37,7 +37,8 @@ tidal_status tidal_k_head(const float* xlast, const void* g, const void* W, int 
 /* tcgen05 GEMM out = A[M,K] . [W_0;W_1;W_2]^T (+ LoRA K-extension T_s . B_s^T).
  * epi: 0 store bf16, 1 store bf16 with RoPE on segments 0,1 (rope = float2
  * [M, head_dim/2] cos/sin), 2 SiLU(W_0 part) * (W_1 part) with seg_n[0] = F,
- * 3 fp32 out += acc.  T/B nullable (no LoRA).  K % 8 == 0, seg_n % 8 == 0.
+ * 3 fp32 out += acc.  T/B nullable (no LoRA).  K % 8 == 0, seg_n % 8 == 0 and
+ * ldo (elements) keeps output rows 16-byte aligned, else TIDAL_ERR_INVALID.
  * Bits 8-16 of epi optionally force the N-tile width (128, 192 or 256) and
  * bits 20-21 the CTA group (1 single-SM, 2 CTA pair with cta_group::2);
  * 0 lets the library pick them as the runtime does. */

@@ -1073,6 +1073,9 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
   const int bn_req = (epi >> 8) & 0x1FF;  // bits 8-16: N tile (0 = auto)
   epi &= 0xFF;
   require(epi >= 0 && epi <= 3 && nseg >= 1 && nseg <= 3, "bad gemm arguments");
+  for (int i = 0; i < nseg; ++i) require(seg_n[i] > 0 && seg_n[i] % 8 == 0, "seg_n must be a positive multiple of 8");
+  require(K > 0 && K % 8 == 0 && M > 0, "K must be a positive multiple of 8, M positive");
+  require(ldo % (epi == 3 ? 4 : 8) == 0, "ldo must keep output rows 16-byte aligned");
   GemmParams p;
   memset(&p, 0, sizeof p);
   p.bn = bn_req ? bn_req : gemm_pick_bn(epi, M, seg_n, epi == EPI_SILU ? 1 : nseg, sms());

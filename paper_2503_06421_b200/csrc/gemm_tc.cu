@@ -96,7 +96,7 @@ __device__ __forceinline__ void store_chunk_bf16(const float (&v)[32], uint8_t* 
       if (c + 8 <= nvalid) {
         *reinterpret_cast<uint4*>(dst) = w;
       } else {
-        const bf16* src = reinterpret_cast<const bf16*>(&w);
+        const bf16* src = reinterpret_cast<const bf16*>(stg + r * 80 + ch * 16);
         for (int e = 0; e < nvalid - c; ++e) dst[e] = src[e];
       }
     }
@@ -132,7 +132,8 @@ __device__ __forceinline__ void add_chunk_f32(const float (&v)[32], uint8_t* stg
       if (c + 4 <= nvalid) {
         red_add_f32x4(dst, a);
       } else {
-        const float* sa = reinterpret_cast<const float*>(&a);
+        // ragged tail: scalars straight from staging (no local copy of `a`)
+        const float* sa = reinterpret_cast<const float*>(stg + r * STG_ROW + ch * 16);
         for (int e = 0; e < nvalid - c; ++e) atomicAdd(dst + e, sa[e]);
       }
     }
@@ -159,7 +160,7 @@ __device__ __forceinline__ void store_chunk_f32(const float (&v)[32], uint8_t* s
       if (c + 4 <= nvalid) {
         *reinterpret_cast<float4*>(dst) = a;
       } else {
-        const float* s = reinterpret_cast<const float*>(&a);
+        const float* s = reinterpret_cast<const float*>(stg + r * STG_ROW + ch * 16);
         for (int e = 0; e < nvalid - c; ++e) dst[e] = s[e];
       }
     }

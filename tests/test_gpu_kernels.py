@@ -59,6 +59,20 @@ def test_gemm_store(T, M, N, K):
     _close_bf16(_host(out), F.linear(A, W, None, 1.0))
 
 
+@pytest.mark.parametrize("epi,N,ldo,K", [(0, 204, 204, 320), (0, 256, 260, 320), (3, 256, 258, 320),
+                                         (3, 256, 256, 300)])
+def test_gemm_rejects_unaligned_shapes(T, epi, N, ldo, K):
+    """seg_n, K multiples of 8 and 16-byte-aligned output rows are the GEMM's
+    contract (include/tidal_kernels.h): violations are refused up front with
+    TIDAL_ERR_INVALID instead of faulting in the epilogue's vector stores."""
+    rng = np.random.default_rng(1)
+    A, W = _bf(rng, (128, K)), _bf(rng, (N, K))
+    out = torch.zeros(128 * ldo + 64, dtype=torch.float32 if epi == 3 else torch.bfloat16, device="cuda")
+    with pytest.raises(T.TidalError) as ei:
+        T.k_gemm(epi, _dev(A), [_dev(W)], [N], out, ldo, 128, K)
+    assert ei.value.code == T.ERR_INVALID
+
+
 @pytest.mark.parametrize("M,N,K", [(256, 512, 512), (130, 256, 1376)])
 def test_gemm_residual_fp32(T, M, N, K):
     rng = np.random.default_rng(7)
