@@ -350,10 +350,18 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           } else {
             bytes = A_BYTES + (EPI == EPI_SILU ? SILU_LORA_ROWS : BROWS) * ROW_BYTES;
           }
+          if (p.noload) bytes = 0;
           if (rank == 0)
             ptx::mbar_expect_tx(fb, bytes * CG);
           else
             ptx::mbar_arrive_leader(fb);
+          if (p.noload) {
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+            continue;
+          }
           if (EPI == EPI_PARTIAL) {
             tma(&p.a, sa, fb, kb * BK, ma);
             for (int s = 0; s < p.nseg; ++s)
@@ -388,25 +396,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     __syncwarp();
   } else if (warp == 1) {
     // ===================== MMA issuer (leader CTA) =====================
-    if (lane == 0 && rank == 0) {
+    if (rank == 0) {  // whole warp: uniform control flow, one elected lane issues
       constexpr uint32_t IDESC = ptx::idesc_bf16(BM * CG, BNX);
       constexpr uint32_t IDESC_HALF = ptx::idesc_bf16(BM * CG, 128);
       const int nmma_lora = (p.lora_r + 15) / 16;
       auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
-        if (CG == 2)
-          ptx::mma_bf16_pair(d, a, b, id, acc);
-        else
-          ptx::mma_bf16(d, a, b, id, acc);
+        ptx::mma_bf16_ws<CG>(d, a, b, id, acc);
       };
       auto commit = [&](uint32_t bar) {  // this pair's two CTAs
         if (CG == 2)
-          ptx::mma_commit_mask(bar, (uint16_t)(3u << (2 * pr)));
+          ptx::mma_commit_mask_ws(bar, (uint16_t)(3u << (2 * pr)));
         else
-          ptx::mma_commit(bar);
+          ptx::mma_commit_ws(bar);
       };
       auto commit_stage = [&](uint32_t bar) {  // a stage slot is shared by all pairs
         if (MC == 2)
-          ptx::mma_commit_mask(bar, (uint16_t)0xF);
+          ptx::mma_commit_mask_ws(bar, (uint16_t)0xF);
         else
           commit(bar);
       };
@@ -809,7 +814,13 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
   return r == CUDA_SUCCESS;
 }
 
-cudaError_t gemm_launch(const GemmParams& p, int epi, int num_sms, cudaStream_t s) {
+cudaError_t gemm_launch(const GemmParams& p0, int epi, int num_sms, cudaStream_t s) {
+  static const int noload = [] {
+    const char* e = getenv("TIDAL_GEMM_NOLOAD");
+    return e ? atoi(e) : 0;
+  }();
+  GemmParams p = p0;
+  p.noload = noload;
   switch (epi) {
     case EPI_STORE:
       if (p.bn == 192) return launch_cg<EPI_STORE, 192>(p, num_sms, s);
