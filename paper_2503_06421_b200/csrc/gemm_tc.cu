@@ -350,18 +350,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           } else {
             bytes = A_BYTES + (EPI == EPI_SILU ? SILU_LORA_ROWS : BROWS) * ROW_BYTES;
           }
-          if (p.noload) bytes = 0;
           if (rank == 0)
             ptx::mbar_expect_tx(fb, bytes * CG);
           else
             ptx::mbar_arrive_leader(fb);
-          if (p.noload) {
-            if (++stage == STAGES) {
-              stage = 0;
-              phase ^= 1;
-            }
-            continue;
-          }
           if (EPI == EPI_PARTIAL) {
             tma(&p.a, sa, fb, kb * BK, ma);
             for (int s = 0; s < p.nseg; ++s)
@@ -815,12 +807,7 @@ bool make_tmap(CUtensorMap* m, const void* base, uint64_t rows, uint64_t cols,
 }
 
 cudaError_t gemm_launch(const GemmParams& p0, int epi, int num_sms, cudaStream_t s) {
-  static const int noload = [] {
-    const char* e = getenv("TIDAL_GEMM_NOLOAD");
-    return e ? atoi(e) : 0;
-  }();
-  GemmParams p = p0;
-  p.noload = noload;
+  const GemmParams& p = p0;
   switch (epi) {
     case EPI_STORE:
       if (p.bn == 192) return launch_cg<EPI_STORE, 192>(p, num_sms, s);

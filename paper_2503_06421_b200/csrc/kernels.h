@@ -60,7 +60,6 @@ struct alignas(64) GemmParams {
   int ksplit, kblocks_per_split, src_rows;  // EPI_PARTIAL
   int cg;              // 1: single-CTA 128-row tiles; 2: CTA pair, 256-row tiles (cta_group::2)
   int mc;              // cg == 2: CTA pairs per cluster sharing W boxes (1 or 2; 0 = 1)
-  int noload;          // diagnostics (TIDAL_GEMM_NOLOAD=1): no TMA, MMAs on stale smem
   int* flags;          // EPI_RESID with ksplit > 1: per (tile, CTA) split counters, all 0
                        // between launches (GEMM_MAX_FLAGS ints); parts add in split order
 };
