@@ -20,6 +20,7 @@ from __future__ import annotations
 import argparse
 import json
 import os
+import socket
 import statistics
 import subprocess
 import sys
@@ -161,6 +162,48 @@ def run_reference(args):
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+def _free_port():
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        return sk.getsockname()[1]
+
+
+def self_launch(args):
+    """--gpus N > 1 outside torchrun: one rank per GPU via torch.distributed.run
+    (127.0.0.1 rendezvous).  Fails loudly when fewer than N GPUs are visible:
+    a silent world = 1 run would report n_gpus = 1 under an N-GPU request."""
+    import torch
+    n = torch.cuda.device_count()
+    if n < args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} needs {args.gpus} visible GPUs, "
+                         f"found {n}; refusing to run a smaller world\n")
+        return 2
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+           f"--nproc-per-node={args.gpus}", "--master-addr", "127.0.0.1",
+           f"--master-port={_free_port()}", os.path.abspath(__file__)] + sys.argv[1:]
+    return subprocess.call(cmd)
+
+
+def h2d_bandwidth(torch, dist, nbytes=1 << 30, reps=10):
+    """B_h2d(N) of SURVEY §8(d): per-GPU pinned->device copy of 1 GiB with all
+    ranks copying at once (barrier before each rep), best of `reps`; bytes/s."""
+    h = torch.empty(nbytes, dtype=torch.uint8, pin_memory=True)
+    dv = torch.empty(nbytes, dtype=torch.uint8, device="cuda")
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    best = 0.0
+    for _ in range(reps):
+        torch.cuda.synchronize()
+        if dist:
+            dist.barrier()
+        e0.record()
+        dv.copy_(h, non_blocking=True)
+        e1.record()
+        e1.synchronize()
+        best = max(best, nbytes / (e0.elapsed_time(e1) / 1e3))
+    del h, dv
+    return best
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -177,15 +220,25 @@ def main():
     ap.add_argument("--quick", action="store_true", help="profiling runs: minimal extra passes")
     ap.add_argument("--decode-steps", type=int, default=64,
                     help="greedy decode steps measured after the prefill (0: skip)")
+    ap.add_argument("--allreduce", default="f32", choices=["f32", "bf16"],
+                    help="TP row-parallel allreduce precision (N > 1)")
     args = ap.parse_args()
     if args.impl == "reference":
         return run_reference(args)
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        return self_launch(args)
 
     import torch
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local = int(os.environ.get("LOCAL_RANK", "0"))
-    assert world == args.gpus or "WORLD_SIZE" not in os.environ, "--gpus must match torchrun"
+    if world != args.gpus:
+        sys.stderr.write(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}\n")
+        return 2
+    if not torch.cuda.is_available() or torch.cuda.device_count() <= local:
+        sys.stderr.write(f"bench.py: rank {rank} needs cuda:{local}, "
+                         f"{torch.cuda.device_count()} GPU(s) visible\n")
+        return 2
     torch.cuda.set_device(local)
     dist = None
     if world > 1:
@@ -235,62 +288,96 @@ def main():
         st["token"] = tok
         return st
 
-    def max_over_ranks(x):
+    def reduce_ranks(x, op):
         if not dist:
             return x
         t = torch.tensor([x], dtype=torch.float64, device="cuda")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        dist.all_reduce(t, op=op)
         return float(t.item())
 
-    # (1) H2D bandwidth of this path and the load-then-infer baseline (rho = 0, serial)
+    def max_over_ranks(x):
+        return reduce_ranks(x, dist.ReduceOp.MAX if dist else None)
+
+    def min_over_ranks(x):
+        return reduce_ranks(x, dist.ReduceOp.MIN if dist else None)
+
+    def barrier():
+        if dist:
+            dist.barrier()
+
+    if world > 1:
+        tpl.set_allreduce_dtype(T.DTYPE_BF16 if args.allreduce == "bf16" else T.DTYPE_F32)
+    # (0) B_h2d(N): raw 1 GiB pinned copies, all ranks at once
+    b_raw_rank = h2d_bandwidth(torch, dist, reps=3 if args.quick else 10)
+    b_raw = min_over_ranks(b_raw_rank)
+    # (1) H2D bandwidth of this path and the load-then-infer baseline (rho = 0,
+    # serial), every rank streaming its own shard at the same time
     for _ in range(1 if args.quick else 2):
+        barrier()
         st0 = step(T.DEBUG_SERIAL | T.DEBUG_SCRUB_L2)
     h2d_ms = st0["h2d_last_ms"] - st0["h2d_first_ms"]
     stream_bytes = st0["bytes_streamed"] + st0["bytes_adapter"]
-    b_h2d = stream_bytes / (h2d_ms / 1e3)
-    b_h2d = min(b_h2d, max_over_ranks(b_h2d)) if dist else b_h2d
+    b_h2d_rank = stream_bytes / (h2d_ms / 1e3)
+    b_h2d = min_over_ranks(b_h2d_rank)   # the slowest link bounds a TP step
     cold_ms = max_over_ranks(st0["device_ms"])
     sweep = {"load_then_infer_rho0": cold_ms}
     if not args.no_sweep and not args.quick:
+        barrier()
         sweep["overlap_rho0"] = max_over_ranks(step(T.DEBUG_SCRUB_L2)["device_ms"])
-    # (2) warm TTFT (rho = 1), the T_TTFT of Eq. 1
+    # (2) warm TTFT (rho = 1), the T_TTFT of Eq. 1: same protocol as the timed
+    # region (W warm-up + K back-to-back steps, L2 flushed, no profiling events)
     tpl.resize(T.template_opts(resident_bytes=T.U64_MAX))
-    warm = [step(T.DEBUG_SCRUB_L2)["device_ms"] for _ in range(1 if args.quick else 3)]
-    t_warm = max_over_ranks(statistics.median(warm))
+    n_warm = 1 if args.quick else args.steps
+    for _ in range(0 if args.quick else args.warmup):
+        step(T.DEBUG_SCRUB_L2)
+    barrier()
+    warm = [step(T.DEBUG_SCRUB_L2)["device_ms"] for _ in range(n_warm)]
+    t_warm = max_over_ranks(statistics.mean(warm))
     sweep["warm_rho1"] = t_warm
+    tp_info = None
+    if world > 1 and not args.quick:
+        other = "bf16" if args.allreduce == "f32" else "f32"
+        tpl.set_allreduce_dtype(T.DTYPE_BF16 if other == "bf16" else T.DTYPE_F32)
+        step(T.DEBUG_SCRUB_L2)
+        barrier()
+        w2 = [step(T.DEBUG_SCRUB_L2)["device_ms"] for _ in range(n_warm)]
+        sweep[f"warm_rho1_allreduce_{other}"] = max_over_ranks(statistics.mean(w2))
+        tpl.set_allreduce_dtype(T.DTYPE_BF16 if args.allreduce == "bf16" else T.DTYPE_F32)
     # (3) template size
     if args.rho == "eq1":
         tpl.resize(T.template_opts(eq1=True, t_ttft_s=t_warm / 1e3, b_pcie_Bps=b_h2d))
     else:
         M = sum(s.nbytes for s in synth.base_tensors(cfg)) // world
         tpl.resize(T.template_opts(resident_bytes=int(float(args.rho) * M)))
-    # (4) timed region: CUDA events only around the tensor-core GEMMs (the
-    # dominant kernels), so the bracketing does not perturb the short kernels
-    dbg = T.DEBUG_SCRUB_L2 | T.DEBUG_PROFILE_GEMM
+    # (4) timed region: no events inside the forward (PDL overlap intact)
+    dbg = T.DEBUG_SCRUB_L2
     for _ in range(args.warmup):
         step(dbg)
-    tpl.profile(reset=True)
-    if dist:
-        dist.barrier()
+    barrier()
     torch.cuda.synchronize()
     stats = []
     with Clocks(local) as clk:
         for _ in range(args.steps):
             stats.append(step(dbg))
     torch.cuda.synchronize()
-    if dist:
-        dist.barrier()
+    barrier()
+    # (5) the same K steps again with CUDA events around each tensor-core GEMM
+    # (the dominant kernels): their per-launch time for `roofline`
+    tpl.profile(reset=True)
+    for _ in range(args.steps):
+        step(T.DEBUG_SCRUB_L2 | T.DEBUG_PROFILE_GEMM)
     prof = tpl.profile(reset=True)
-    # per-kernel-class table: a separate pass with events around every launch
+    # (6) per-kernel-class table: a separate pass with events around every launch
     # (bracketing adds a launch gap per kernel, so short kernels read high)
-    for _ in range(1 if args.quick else 3):
+    n_all = 1 if args.quick else 3
+    for _ in range(n_all):
         step(T.DEBUG_SCRUB_L2 | T.DEBUG_PROFILE)
     prof_all = tpl.profile(reset=True)
-    n_all = 1 if args.quick else 3
     if not args.quick and not args.no_sweep:
         # keep-alive with adapter hot-swap (Tidal-DK, §5.2): the streamed
         # weights of the previous invocation stay; only the adapter streams
         tpl.keep_alive()
+        barrier()
         sweep["keep_alive_hot_swap"] = max_over_ranks(
             statistics.median(step(T.DEBUG_SCRUB_L2)["device_ms"] for _ in range(3)))
         # loading-order ablation at rho = 0 (§7.4)
@@ -298,6 +385,7 @@ def main():
         for name, order in (("rho0_order_reverse", T.ORDER_REVERSE),
                             ("rho0_order_registration", T.ORDER_REGISTRATION)):
             tpl.set_load_order(order)
+            barrier()
             sweep[name] = max_over_ranks(step(T.DEBUG_SCRUB_L2)["device_ms"])
         tpl.set_load_order(T.ORDER_TRACED)
     decode = None
@@ -328,14 +416,18 @@ def main():
     s0 = stats[0]
     ttft = statistics.mean(dev_ms)
     if rank != 0:
-        return
+        return 0
 
-    # roofline of the whole step (north_star): max(streamed / B_h2d, FLOPs / peak)
+    # roofline of the whole step (north_star): max(streamed / B_h2d, FLOPs / peak),
+    # plus the HBM bound of reading every weight once (binds only for short prompts)
     flops = prefill_flops(cfg, S, r, world)
     streamed = s0["bytes_streamed"] + s0["bytes_adapter"]
     t_pcie = streamed / b_h2d * 1e3
     t_tc = flops / (P["bf16_tflops"] * 1e12) * 1e3
-    roof = max(t_pcie, t_tc)
+    w_bytes = s0["bytes_streamed"] + s0["bytes_resident"] + s0["bytes_adapter"]
+    t_hbm = w_bytes / (P["hbm_gbs"] * 1e9) * 1e3
+    roof = max(t_pcie, t_tc, t_hbm)
+    bound = max((("pcie", t_pcie), ("tensor", t_tc), ("hbm", t_hbm)), key=lambda kv: kv[1])[0]
     # dominant kernel (largest device time in the timed region)
     dom_name, dom = max(prof.items(), key=lambda kv: kv[1]["ms"])
     per_launch_ms = dom["ms"] / max(1, dom["launches"])
@@ -349,11 +441,14 @@ def main():
             traffic = None
     if tensor_bound:
         ach = dom["flops"] / (dom["ms"] / 1e3) / 1e12
-        pk = P.get("bf16_tflops_sustained", P["bf16_tflops"])
+        pk = P["bf16_tflops"]
+        pks = P.get("bf16_tflops_sustained", pk)
         rl = {"kernel": dom_name, "bound": "tensor", "achieved": ach, "peak": pk, "unit": "TFLOP/s",
-              "frac": ach / pk, "traffic": traffic,
+              "frac": ach / pk, "traffic": traffic, "frac_vs_sustained": ach / pks,
               "per_launch": {"ms": per_launch_ms, "flops": dom["flops"] / max(1, dom["launches"])},
-              "peak_source": peak_src + " bf16_tflops_sustained (kernel timed inside the step)"}
+              "timing": f"CUDA events around each launch on the compute stream, {args.steps} "
+                        "steps after the timed region (same inputs, L2 flushed per step)",
+              "peak_source": peak_src + " bf16_tflops (burst)"}
     else:
         ach = dom["bytes"] / (dom["ms"] / 1e3) / 1e9
         rl = {"kernel": dom_name, "bound": "hbm", "achieved": ach, "peak": P["hbm_gbs"],
@@ -364,6 +459,13 @@ def main():
                    "tflops": (v["flops"] / (v["ms"] / 1e3) / 1e12) if v["ms"] and v["flops"] else None,
                    "gbs": (v["bytes"] / (v["ms"] / 1e3) / 1e9) if v["ms"] else None}
                for k, v in prof_all.items() if v["launches"]}
+    if world > 1:
+        tot = sum(v["ms_per_step"] for v in kernels.values())
+        ar = kernels.get("allreduce", {}).get("ms_per_step", 0.0)
+        tp_info = {"allreduce_dtype": args.allreduce, "allreduce_ms_per_step": ar,
+                   "allreduce_share": ar / tot if tot else None,
+                   "note": "share of the all-kernel event pass (allreduce = NCCL on the "
+                           "compute stream, incl. bf16 pack/add kernels when bf16)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
         t1 = oracle_sample(cfg, S, r)
@@ -385,9 +487,15 @@ def main():
                     "p95": sorted(dev_ms)[max(0, int(np.ceil(0.95 * len(dev_ms))) - 1)],
                     "min": min(dev_ms)},
         "tokens_per_s": S / (ttft / 1e3),
-        "ttft_roofline": {"roof_ms": roof, "bound": "pcie" if t_pcie >= t_tc else "tensor",
-                          "t_pcie_ms": t_pcie, "t_tensor_ms": t_tc, "frac": roof / ttft,
+        "ttft_roofline": {"roof_ms": roof, "bound": bound,
+                          "t_pcie_ms": t_pcie, "t_tensor_ms": t_tc, "t_hbm_ms": t_hbm,
+                          "frac": roof / ttft,
                           "streamed_bytes_per_rank": streamed, "b_h2d_GBps": b_h2d / 1e9,
+                          "b_h2d_this_rank_GBps": b_h2d_rank / 1e9,
+                          "b_h2d_raw_GBps": b_raw / 1e9,
+                          "b_h2d_note": "b_h2d: this path's own streaming rate in the serial rho=0 "
+                                        "step, MIN over ranks, all ranks streaming at once; "
+                                        "raw: 1 GiB pinned copy, best of 10, all ranks at once",
                           "flops_per_rank": flops, "peak_tflops": P["bf16_tflops"]},
         "roofline": rl,
         "cpu_baseline": cpu,
@@ -399,7 +507,10 @@ def main():
         "kernels": kernels,
         "sweep_ms": sweep,
         "clocks": clk.summary(),
-        "eq1": {"t_warm_ms": t_warm, "b_h2d_GBps": b_h2d / 1e9},
+        "eq1": {"t_warm_ms": t_warm, "b_h2d_GBps": b_h2d / 1e9,
+                "t_warm_protocol": f"mean of {n_warm} back-to-back rho=1 steps after "
+                                   f"{args.warmup} warm-up, L2 flushed, no profiling events"},
+        "tp": tp_info,
         # the compute-bound regime (fully template-resident, rho = 1): warm TTFT
         # against the tensor roof at the burst and at the sustained (power-cap)
         # measured bf16 peak; north_star's bar is frac >= 1/1.3
@@ -417,4 +528,4 @@ def main():
 
 
 if __name__ == "__main__":
-    main()
+    sys.exit(main() or 0)

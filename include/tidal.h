@@ -292,6 +292,24 @@ tidal_status tidal_comm_create(int world, int rank, const void* unique_id128, in
 tidal_status tidal_comm_create_local(int world, int rank, const char* group, int device,
                                      tidal_comm** out);
 void tidal_comm_destroy(tidal_comm* c);
+/* Precision of the row-parallel allreduces C1/C2 (after o_proj and down_proj,
+ * "fp32 for parity, bf16 measured as an option").
+ * TIDAL_DTYPE_F32 (default): the fp32 residual stream itself is allreduced
+ * (rank 0 carries the residual, the other ranks their partial sums only).
+ * TIDAL_DTYPE_BF16: every rank's partial sum is rounded once to bf16, reduced
+ * in bf16 (half the NVLink bytes) and added to the fp32 residual.  The embed
+ * allreduce (C3) stays fp32.  No effect when world == 1.  Takes effect at the
+ * next invoke; all ranks must set the same value.  Errors: INVALID. */
+enum { TIDAL_DTYPE_F32 = 0, TIDAL_DTYPE_BF16 = 1 };
+/* Self-test of a communicator's collectives (allreduce f32 / bf16, u64 max,
+ * logits allgather) on n-element device buffers holding small integers, so
+ * every expected value is exact.  All ranks call it at once (NCCL ranks in
+ * their processes, local ranks on their threads).  tidal_comm_create also
+ * builds a one-rank NCCL communicator at world 1, so the NCCL binding can be
+ * exercised on a single GPU.  Errors: NCCL (mismatch or NCCL failure),
+ * INVALID (a world-1 local communicator has no implementation). */
+tidal_status tidal_comm_selftest(tidal_comm* c, uint64_t n);
+tidal_status tidal_set_allreduce_dtype(tidal_template* tpl, int dtype);
 
 /* ---- invariants and fault injection (test support) ---- */
 enum {
@@ -301,7 +319,11 @@ enum {
   TIDAL_DEBUG_SERIAL = 8,      /* load-then-infer: compute waits for every copy first
                                   (the paper's "PyTorch-pin" baseline) */
   TIDAL_DEBUG_PROFILE = 16,    /* CUDA events around every kernel on the compute stream */
-  TIDAL_DEBUG_PROFILE_GEMM = 32 /* events around the tensor-core GEMMs only (low overhead) */
+  TIDAL_DEBUG_PROFILE_GEMM = 32,/* events around the tensor-core GEMMs only (low overhead) */
+  TIDAL_DEBUG_NO_GRAPH = 64    /* enqueue the invocation eagerly instead of replaying its
+                                  captured CUDA graph (single-GPU invocations are captured
+                                  once per plan / shape / adapter buffer / scale and
+                                  replayed; profiling and fault injection are always eager) */
 };
 /* Per-kernel-class totals accumulated by invokes run with TIDAL_DEBUG_PROFILE:
  * device time (events on the launching stream), launches, and the ALGORITHMIC

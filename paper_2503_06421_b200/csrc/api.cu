@@ -26,6 +26,7 @@ namespace tidal {
 bool nccl_unique_id(void* out128);
 Comm* nccl_comm_create(int world, int rank, const void* id128, int device);
 Comm* local_comm_create(int world, int rank, const std::string& key, int device);
+void comm_selftest(Comm* c, size_t n);
 }  // namespace tidal
 
 namespace {
@@ -122,6 +123,16 @@ struct tidal_template {
   std::vector<cudaEvent_t> ev;
   cudaEvent_t e_start = nullptr, e_h2d0 = nullptr, e_h2d1 = nullptr, e_c0 = nullptr, e_end = nullptr,
               e_tok = nullptr;
+  cudaEvent_t e_fork = nullptr, e_join = nullptr;  // copy stream fork / join (graph edges)
+  // The whole invocation (copy stream + compute stream, event waits as edges)
+  // captured once per key and replayed (world == 1, no profiling / fault
+  // injection); TIDAL_GRAPH=0 disables it.
+  struct PrefillGraph {
+    cudaGraphExec_t exec = nullptr;
+    std::vector<uint64_t> key;
+    int launches = 0;
+  } graph;
+  bool use_graphs = true;
   uint8_t* arena = nullptr;  // adapter arena
   uint64_t arena_cap = 0;
   int debug = 0, debug_arg = -1;
@@ -149,7 +160,9 @@ struct tidal_adapter {
   uint32_t mask = 0;
   const uint8_t* host = nullptr;
   uint64_t bytes = 0;
+  uint64_t serial = 0;  // process-unique identity (decode must continue with the same adapter)
 };
+static std::atomic<uint64_t> g_adapter_serial{0};
 
 static ModelShape shape_of(const tidal_model_config* c) {
   ModelShape m;
@@ -397,6 +410,7 @@ static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
     require(m->world == 1 || (opts->comm && opts->comm->world == m->world && opts->comm->rank == m->rank),
             "tensor-parallel model needs a matching communicator");
     tp->ex.init(tp->device, tp->shape, tp->eps, tp->theta, tp->world, tp->rank, tp->max_tokens);
+    tp->ex.colocated = tp->comm && tp->comm->impl && tp->comm->impl->colocated;
     const uint64_t L = tp->plan.layout_bytes;
     {
       // pinned pool, NUMA-local to the device, whole image in layout order
@@ -430,6 +444,12 @@ static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
                  "H2D resident prefix");
     for (cudaEvent_t* e : {&tp->e_start, &tp->e_h2d0, &tp->e_h2d1, &tp->e_c0, &tp->e_end, &tp->e_tok})
       cuda_check(cudaEventCreate(e), "cudaEventCreate");
+    for (cudaEvent_t* e : {&tp->e_fork, &tp->e_join})
+      cuda_check(cudaEventCreateWithFlags(e, cudaEventDisableTiming), "cudaEventCreate");
+    {
+      const char* g = getenv("TIDAL_GRAPH");
+      tp->use_graphs = !(g && g[0] == '0');
+    }
     tp->ensure_events(tp->plan.groups.size() + 2 * tp->shape.n_layers + 4);
     cuda_check(cudaMalloc((void**)&tp->d_sum, 64), "cudaMalloc");
     // warm run streams nothing: make every weight valid once (prefix resident,
@@ -532,8 +552,10 @@ void tidal_template_destroy(tidal_template* tp) {
     cudaSetDevice(tp->device);
     cudaDeviceSynchronize();
     for (cudaEvent_t e : tp->ev) cudaEventDestroy(e);
-    for (cudaEvent_t e : {tp->e_start, tp->e_h2d0, tp->e_h2d1, tp->e_c0, tp->e_end, tp->e_tok})
+    for (cudaEvent_t e : {tp->e_start, tp->e_h2d0, tp->e_h2d1, tp->e_c0, tp->e_end, tp->e_tok,
+                          tp->e_fork, tp->e_join})
       if (e) cudaEventDestroy(e);
+    if (tp->graph.exec) cudaGraphExecDestroy(tp->graph.exec);
     if (tp->vmm.va)
       vmm_free(tp->vmm);
     else if (tp->dev)
@@ -551,8 +573,6 @@ static void adapter_table(const tidal_template* tp, int rank, uint32_t mask, Ten
                           const std::string& ckpt) {
   require(rank == 8 || rank == 16 || rank == 32 || rank == 64, "LoRA rank must be 8, 16, 32 or 64");
   require(mask != 0 && (mask & ~0x7Fu) == 0, "target_mask must be a non-empty subset of 0x7F");
-  require(((mask >> T_GATE) & 1u) == ((mask >> T_UP) & 1u),
-          "gate and up must be targeted together (paired tiles)");
   tt = tp->tt;
   add_adapter(tt, rank, mask, ckpt);
 }
@@ -614,6 +634,7 @@ tidal_status tidal_attach_lora(tidal_template* tp, const tidal_lora_desc* d, tid
   a->mask = d->target_mask;
   a->host = reinterpret_cast<const uint8_t*>(d->host_pinned);
   a->bytes = d->bytes;
+  a->serial = ++g_adapter_serial;
   *out = a;
   TIDAL_CATCH
 }
@@ -701,76 +722,123 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
   ex.profile_all = (tp->debug & TIDAL_DEBUG_PROFILE) != 0;
   ex.prof_pending.clear();
   memcpy(ex.h_tok, host_tokens, 4ull * n_tokens);
-  cuda_check(cudaEventRecord(tp->e_start, ex.compute), "event");
-  cuda_check(cudaStreamWaitEvent(ex.copy, tp->e_start, 0), "wait");
-  // the prompt goes first on the (high-priority) copy stream: a token copy on
-  // the compute stream larger than ~24 KB was starved behind every weight
-  // group (measured: at S >= 7168 the prefill started after the last group)
-  cuda_check(cudaMemcpyAsync(ex.tok, ex.h_tok, 4ull * n_tokens, cudaMemcpyHostToDevice, ex.copy),
-             "H2D tokens");
-  cuda_check(cudaEventRecord(tp->e_tok, ex.copy), "event");
-  // ---- copy stream: groups in traced access order, one event each ----
-  cuda_check(cudaEventRecord(tp->e_h2d0, ex.copy), "event");
   const int skip = (tp->debug & TIDAL_DEBUG_SKIP_BARRIER) ? tp->debug_arg : -1;
-  // copy order (traced by default; ablations reverse / registration order)
-  std::vector<int> order(P.groups.size());
-  for (size_t g = 0; g < order.size(); ++g) order[g] = (int)g;
-  if (tp->load_order == TIDAL_ORDER_REVERSE) {
-    std::reverse(order.begin(), order.end());
-  } else if (tp->load_order == TIDAL_ORDER_REGISTRATION) {
-    auto first_id = [&](int g) {
-      int m = INT32_MAX;
-      for (int id : P.groups[g].members) m = std::min(m, id);
-      return m;
-    };
-    std::stable_sort(order.begin(), order.end(),
-                     [&](int x, int y) { return first_id(x) < first_id(y); });
-  }
-  std::vector<int> copy_pos(P.groups.size());
-  for (size_t i = 0; i < order.size(); ++i) copy_pos[order[i]] = (int)i;
-  for (int g : order) {
-    const Group& G = P.groups[g];
-    const uint8_t* src = G.adapter ? a->host + G.offset : tp->pool + G.offset;
-    uint8_t* dst = G.adapter ? tp->arena + G.offset : tp->dev + G.offset;
-    if (g == skip) {
-      sleep_kernel<<<1, 1, 0, ex.copy>>>(20000);  // fault injection: late group
-      cuda_check(cudaGetLastError(), "sleep");
+  const bool graph_ok = tp->use_graphs && tp->world == 1 &&
+                        !(tp->debug & (TIDAL_DEBUG_PROFILE | TIDAL_DEBUG_PROFILE_GEMM |
+                                       TIDAL_DEBUG_SKIP_BARRIER | TIDAL_DEBUG_SERIAL |
+                                       TIDAL_DEBUG_NO_GRAPH));
+  // everything a captured invocation bakes in: plan, shapes, buffers, scale
+  float scale_v = a ? a->scale : 1.f;
+  uint32_t scale_bits = 0;
+  memcpy(&scale_bits, &scale_v, 4);
+  const std::vector<uint64_t> gkey = {
+      (uint64_t)(uintptr_t)&P, tp->gen, (uint64_t)n_tokens, (uint64_t)n_seqs,
+      (uint64_t)(uintptr_t)(a ? a->host : nullptr), (uint64_t)(uintptr_t)tp->arena, scale_bits,
+      (uint64_t)tp->load_order, (uint64_t)(host_logits_out != nullptr),
+      (uint64_t)(uintptr_t)ex.dec.kc, (uint64_t)ex.fuse_shrink, (uint64_t)ex.ar_bf16};
+  const unsigned rec_flags = graph_ok ? cudaEventRecordExternal : cudaEventRecordDefault;
+  auto rec = [&](cudaEvent_t e, cudaStream_t st) {  // timing events: real records in a graph
+    cuda_check(cudaEventRecordWithFlags(e, st, rec_flags), "event");
+  };
+  auto enqueue = [&]() {
+    rec(tp->e_start, ex.compute);
+    cuda_check(cudaEventRecord(tp->e_fork, ex.compute), "event");
+    cuda_check(cudaStreamWaitEvent(ex.copy, tp->e_fork, 0), "wait");
+    // the prompt goes first on the (high-priority) copy stream: a token copy on
+    // the compute stream larger than ~24 KB was starved behind every weight
+    // group (measured: at S >= 7168 the prefill started after the last group)
+    cuda_check(cudaMemcpyAsync(ex.tok, ex.h_tok, 4ull * n_tokens, cudaMemcpyHostToDevice, ex.copy),
+               "H2D tokens");
+    cuda_check(cudaEventRecord(tp->e_tok, ex.copy), "event");
+    // ---- copy stream: groups in traced access order, one event each ----
+    rec(tp->e_h2d0, ex.copy);
+    // copy order (traced by default; ablations reverse / registration order)
+    std::vector<int> order(P.groups.size());
+    for (size_t g = 0; g < order.size(); ++g) order[g] = (int)g;
+    if (tp->load_order == TIDAL_ORDER_REVERSE) {
+      std::reverse(order.begin(), order.end());
+    } else if (tp->load_order == TIDAL_ORDER_REGISTRATION) {
+      auto first_id = [&](int g) {
+        int m = INT32_MAX;
+        for (int id : P.groups[g].members) m = std::min(m, id);
+        return m;
+      };
+      std::stable_sort(order.begin(), order.end(),
+                       [&](int x, int y) { return first_id(x) < first_id(y); });
     }
-    cuda_check(cudaMemcpyAsync(dst, src, G.bytes, cudaMemcpyHostToDevice, ex.copy), "H2D group");
-    cuda_check(cudaEventRecord(tp->ev[g], ex.copy), "event");
+    std::vector<int> copy_pos(P.groups.size());
+    for (size_t i = 0; i < order.size(); ++i) copy_pos[order[i]] = (int)i;
+    for (int g : order) {
+      const Group& G = P.groups[g];
+      const uint8_t* src = G.adapter ? a->host + G.offset : tp->pool + G.offset;
+      uint8_t* dst = G.adapter ? tp->arena + G.offset : tp->dev + G.offset;
+      if (g == skip) {
+        sleep_kernel<<<1, 1, 0, ex.copy>>>(20000);  // fault injection: late group
+        cuda_check(cudaGetLastError(), "sleep");
+      }
+      cuda_check(cudaMemcpyAsync(dst, src, G.bytes, cudaMemcpyHostToDevice, ex.copy), "H2D group");
+      cuda_check(cudaEventRecord(tp->ev[g], ex.copy), "event");
+    }
+    rec(tp->e_h2d1, ex.copy);
+    cuda_check(cudaEventRecord(tp->e_join, ex.copy), "event");
+    // ---- compute stream ----
+    cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_tok, 0), "wait tokens");
+    if (tp->debug & 8) cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_join, 0), "serial");
+    rec(tp->e_c0, ex.compute);
+    RunArgs ra;
+    ra.tt = &tt;
+    ra.ops = &P.ops;
+    ra.barriers = &P.barriers;
+    ra.events = &tp->ev;
+    ra.copy_pos = &copy_pos;
+    ra.skip_group = skip;
+    ra.S = n_tokens;
+    ra.nseq = n_seqs;
+    ra.lora_scale = a ? a->scale : 1.f;
+    ra.akey = a ? (const void*)tp->arena : nullptr;
+    ra.gen = tp->gen;
+    ra.comm = tp->comm ? tp->comm->impl : nullptr;
+    run_forward(ex, ra);
+    cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_join, 0), "wait copies");
+    cuda_check(cudaMemcpyAsync(ex.h_key, ex.key, 8ull * n_seqs, cudaMemcpyDeviceToHost, ex.compute),
+               "D2H key");
+    if (host_logits_out)
+      cuda_check(cudaMemcpyAsync(ex.h_logits, ex.logits, 4ull * V * n_seqs, cudaMemcpyDeviceToHost,
+                                 ex.compute),
+                 "D2H logits");
+    rec(tp->e_end, ex.compute);
+  };
+  if (graph_ok && tp->graph.exec && tp->graph.key == gkey) {
+    cuda_check(cudaGraphLaunch(tp->graph.exec, ex.compute), "graph launch");
+    ex.launches = tp->graph.launches;
+  } else if (graph_ok) {
+    if (tp->graph.exec) cudaGraphExecDestroy(tp->graph.exec);
+    tp->graph.exec = nullptr;
+    cudaGraph_t graph = nullptr;
+    cuda_check(cudaStreamBeginCapture(ex.compute, cudaStreamCaptureModeThreadLocal), "begin capture");
+    try {
+      enqueue();
+    } catch (...) {
+      cudaStreamEndCapture(ex.compute, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    cuda_check(cudaStreamEndCapture(ex.compute, &graph), "end capture");
+    const cudaError_t ie = cudaGraphInstantiate(&tp->graph.exec, graph, 0);
+    cudaGraphDestroy(graph);
+    cuda_check(ie, "graph instantiate");
+    tp->graph.key = gkey;
+    tp->graph.launches = ex.launches;
+    cuda_check(cudaGraphLaunch(tp->graph.exec, ex.compute), "graph launch");
+  } else {
+    enqueue();
   }
-  cuda_check(cudaEventRecord(tp->e_h2d1, ex.copy), "event");
-  // ---- compute stream ----
-  cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_tok, 0), "wait tokens");
-  if (tp->debug & 8) cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_h2d1, 0), "serial");
-  cuda_check(cudaEventRecord(tp->e_c0, ex.compute), "event");
-  RunArgs ra;
-  ra.tt = &tt;
-  ra.ops = &P.ops;
-  ra.barriers = &P.barriers;
-  ra.events = &tp->ev;
-  ra.copy_pos = &copy_pos;
-  ra.skip_group = skip;
-  ra.S = n_tokens;
-  ra.nseq = n_seqs;
-  ra.lora_scale = a ? a->scale : 1.f;
-  ra.akey = a ? (const void*)tp->arena : nullptr;
-  ra.gen = tp->gen;
-  ra.comm = tp->comm ? tp->comm->impl : nullptr;
-  run_forward(ex, ra);
-  cuda_check(cudaStreamWaitEvent(ex.compute, tp->e_h2d1, 0), "wait copies");
-  cuda_check(cudaMemcpyAsync(ex.h_key, ex.key, 8ull * n_seqs, cudaMemcpyDeviceToHost, ex.compute),
-             "D2H key");
-  if (host_logits_out)
-    cuda_check(cudaMemcpyAsync(ex.h_logits, ex.logits, 4ull * V * n_seqs, cudaMemcpyDeviceToHost,
-                               ex.compute),
-               "D2H logits");
-  cuda_check(cudaEventRecord(tp->e_end, ex.compute), "event");
+  ex.dec.prompt_akey = a ? (const void*)tp->arena : nullptr;
   cuda_check(cudaEventSynchronize(tp->e_end), "invoke");
   tp->suffix_valid = skip < 0;
   // decode continuation: the cache now holds this prompt's K/V (single prompt)
   ex.dec.prompt_len = (ex.dec.kc && n_seqs == 1) ? n_tokens : 0;
-  ex.dec.prompt_akey = ra.akey;
+  ex.dec.prompt_adapter = a ? a->serial : 0;
   ex.dec.prompt_gen = tp->gen;
   if (ex.profile) ex.prof_collect();
   for (int b = 0; b < n_seqs; ++b)  // packed key: low word = ~token
@@ -840,7 +908,7 @@ tidal_status tidal_invoke_decode(tidal_template* tp, const tidal_adapter* ca, in
   const TensorTable& tt = a ? hold->tt : tp->tt;
   const void* akey = a ? (const void*)tp->arena : nullptr;
   require(ex.dec.prompt_akey == akey && ex.dec.prompt_gen == tp->gen &&
-              (!a || a->ap->gen == tp->gen),
+              ex.dec.prompt_adapter == (a ? a->serial : 0) && (!a || a->ap->gen == tp->gen),
           "decode must use the adapter of the preceding prefill");
   require(n_steps >= 1 && n_steps <= ex.dec.max_new, "n_steps out of range (1..max_new_tokens)");
   cuda_check(cudaSetDevice(tp->device), "cudaSetDevice");
@@ -908,7 +976,7 @@ tidal_status tidal_comm_create(int world, int rank, const void* id, int device, 
   c->world = world;
   c->rank = rank;
   c->device = device;
-  if (world > 1) {
+  {  // also at world 1 (a valid one-rank NCCL communicator; tidal_comm_selftest uses it)
     try {
       c->impl = nccl_comm_create(world, rank, id, device);
     } catch (...) {
@@ -940,6 +1008,14 @@ tidal_status tidal_comm_create_local(int world, int rank, const char* group, int
   TIDAL_CATCH
 }
 
+tidal_status tidal_comm_selftest(tidal_comm* c, uint64_t n) {
+  TIDAL_TRY
+  require(c != nullptr && c->impl != nullptr, "communicator has no implementation (world 1 local)");
+  require(n >= 1 && n <= (1ull << 26), "n out of range");
+  comm_selftest(c->impl, (size_t)n);
+  TIDAL_CATCH
+}
+
 void tidal_comm_destroy(tidal_comm* c) {
   if (!c) return;
   delete c->impl;
@@ -951,6 +1027,14 @@ tidal_status tidal_set_debug(tidal_template* tp, int flags, int arg) {
   require(tp != nullptr, "null template");
   tp->debug = flags;
   tp->debug_arg = arg;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_set_allreduce_dtype(tidal_template* tp, int dtype) {
+  TIDAL_TRY
+  require(tp != nullptr, "null template");
+  require(dtype == TIDAL_DTYPE_F32 || dtype == TIDAL_DTYPE_BF16, "dtype must be F32 or BF16");
+  tp->ex.ar_bf16 = dtype == TIDAL_DTYPE_BF16;
   TIDAL_CATCH
 }
 
@@ -1067,6 +1151,7 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
                           void* out, int ldo, int M, int K, const void* const* T,
                           const void* const* B, int r, const void* rope, int head_dim) {
   TIDAL_TRY
+  const int epi_code = epi;
   const int cg_req = (epi >> 20) & 0x3;  // bits 20-21: CTA group (0 = auto)
   const int mc_req = (epi >> 22) & 0x3;  // bits 22-23: CTA pairs per cluster (0 = auto)
   const int ks_req = (epi >> 24) & 0xF;  // bits 24-27: EPI_RESID split-K parts (0 = auto)
@@ -1087,14 +1172,27 @@ tidal_status tidal_k_gemm(int epi, const void* A, const void* const* W, const in
   p.mc = mc_req ? mc_req : (p.cg == 2 ? gemm_pick_mc(M, sms()) : 1);
   require(p.mc == 1 || (p.mc == 2 && p.cg == 2), "mc must be 1, or 2 with cg 2");
   if (epi == EPI_RESID) {
-    int bn_auto = 256, ks = 1;
-    gemm_plan_resid(M, seg_n[0], K, sms(), &bn_auto, &ks);
+    int bn_auto = 256, ks = 1, nfull = 0;
+    const bool tail_req = (epi_code >> 28) & 1;  // bit 28: tail split (whole tiles for full waves)
+    gemm_plan_resid(M, seg_n[0], K, sms(), &bn_auto, &ks, nullptr, true, &nfull);
     if (ks_req) ks = ks_req;
     const int nk = (K + GEMM_BK - 1) / GEMM_BK;
     require(ks >= 1 && ks <= nk, "bad split-K");
     p.kblocks_per_split = (nk + ks - 1) / ks;
     p.ksplit = (nk + p.kblocks_per_split - 1) / p.kblocks_per_split;  // parts non-empty
     if (!bn_req) p.bn = bn_auto;
+    if (ks_req) {  // explicit request: tail mode only with bit 28
+      nfull = 0;
+      if (tail_req && p.ksplit > 1) {
+        const int units = gemm_units(p.cg, p.mc, sms());
+        const int tiles = gemm_m_tiles(M, p.cg, p.mc) * ((seg_n[0] + p.bn - 1) / p.bn);
+        nfull = tiles / units * units;
+        if (nfull >= tiles) nfull = 0;
+      }
+    } else if (bn_req && bn_req != bn_auto) {
+      nfull = 0;
+    }
+    p.n_full = p.ksplit > 1 ? nfull : 0;
     static int* flags = nullptr;  // per process; this entry is synchronous
     if (!flags) {
       cudaError_t e = cudaMalloc(&flags, GEMM_MAX_FLAGS * sizeof(int));

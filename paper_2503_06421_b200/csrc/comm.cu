@@ -27,6 +27,7 @@
 #include <memory>
 #include <mutex>
 #include <string>
+#include <vector>
 
 #include "runtime.h"
 
@@ -38,7 +39,7 @@ typedef struct {
   char internal[128];
 } ncclUniqueId;
 enum { ncclSuccess = 0 };
-enum { ncclUint64 = 5, ncclFloat32 = 7 };
+enum { ncclUint64 = 5, ncclFloat32 = 7, ncclBfloat16 = 9 };
 enum { ncclSum = 0, ncclMax = 2 };
 
 struct NcclApi {
@@ -89,6 +90,9 @@ struct NcclComm final : Comm {
   void allreduce_f32(float* buf, size_t n, cudaStream_t s) override {
     nccl_check(g_nccl.AllReduce(buf, buf, n, ncclFloat32, ncclSum, c, s), "ncclAllReduce");
   }
+  void allreduce_bf16(bf16* buf, size_t n, cudaStream_t s) override {
+    nccl_check(g_nccl.AllReduce(buf, buf, n, ncclBfloat16, ncclSum, c, s), "ncclAllReduce(bf16)");
+  }
   void max_u64(unsigned long long* key, size_t n, cudaStream_t s) override {
     nccl_check(g_nccl.AllReduce(key, key, n, ncclUint64, ncclMax, c, s), "ncclAllReduce(max)");
   }
@@ -117,6 +121,25 @@ __global__ void sum_ranks_kernel(SrcPtrs src, float* __restrict__ out, size_t n4
       acc.w += v.w;
     }
     reinterpret_cast<float4*>(out)[i] = acc;
+  }
+}
+
+// bf16 sum in rank order, accumulated in fp32, rounded once (8 elements per thread)
+__global__ void sum_ranks_bf16_kernel(SrcPtrs src, bf16* __restrict__ out, size_t n8) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n8;
+       i += (size_t)gridDim.x * blockDim.x) {
+    float acc[8];
+    for (int k = 0; k < src.n; ++k) {
+      const uint4 v = reinterpret_cast<const uint4*>(src.p[k])[i];
+      const bf16* h = reinterpret_cast<const bf16*>(&v);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc[j] = k ? acc[j] + __bfloat162float(h[j]) : __bfloat162float(h[j]);
+    }
+    uint4 o;
+    bf16* ho = reinterpret_cast<bf16*>(&o);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) ho[j] = __float2bfloat16_rn(acc[j]);
+    reinterpret_cast<uint4*>(out)[i] = o;
   }
 }
 
@@ -208,6 +231,20 @@ struct LocalComm final : Comm {
     retire(s);
     cuda_check(cudaMemcpyAsync(buf, scratch, n * 4, cudaMemcpyDeviceToDevice, s), "D2D");
   }
+  void allreduce_bf16(bf16* buf, size_t n, cudaStream_t s) override {
+    if (n % 8) fail(1, "local allreduce: bf16 length must be a multiple of 8");
+    if (n * 2 > scratch_n * 4) {
+      if (scratch) cudaFree(scratch);
+      scratch = nullptr;
+      cuda_check(cudaMalloc(&scratch, n * 2), "cudaMalloc(comm scratch)");
+      scratch_n = (n * 2 + 3) / 4;
+    }
+    publish(buf, s);
+    sum_ranks_bf16_kernel<<<4 * 148, 256, 0, s>>>(srcs(), reinterpret_cast<bf16*>(scratch), n / 8);
+    cuda_check(cudaGetLastError(), "sum_ranks_bf16");
+    retire(s);
+    cuda_check(cudaMemcpyAsync(buf, scratch, n * 2, cudaMemcpyDeviceToDevice, s), "D2D");
+  }
   void max_u64(unsigned long long* key, size_t n, cudaStream_t s) override {
     if (n > kMaxBatch) fail(1, "local max-reduce: too many keys");
     publish(key, s);
@@ -277,6 +314,7 @@ Comm* local_comm_create(int world, int rank, const std::string& key, int device)
     ++g->joined;
   }
   auto* c = new LocalComm();
+  c->colocated = true;  // in-process ranks: assume they may share a device
   c->world = world;
   c->rank = rank;
   c->device = device;
@@ -296,10 +334,71 @@ Comm* local_comm_create(int world, int rank, const std::string& key, int device)
   return c;
 }
 
+// Exercise every collective of `c` on small buffers with exact expected values
+// (integers representable in fp32 / bf16): allreduce f32 and bf16, the u64 max
+// and the logits allgather.  Every rank of the communicator calls it at once.
+void comm_selftest(Comm* c, size_t n) {
+  n = (n + 7) / 8 * 8;
+  const int W = c->world, R = c->rank;
+  cuda_check(cudaSetDevice(c->device), "cudaSetDevice");
+  cudaStream_t s = nullptr;
+  cuda_check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+  std::vector<float> hf(n), hg((size_t)W * n, -1.f);
+  std::vector<bf16> hb(n);
+  std::vector<unsigned long long> hk(4);
+  for (size_t i = 0; i < n; ++i) {
+    hf[i] = (float)(R * 1000 + (int)(i % 997));
+    hb[i] = __float2bfloat16_rn((float)((int)(i % 13) + R));
+    hg[(size_t)R * n + i] = (float)(R + (int)(i % 100));
+  }
+  for (int j = 0; j < 4; ++j) hk[j] = (unsigned long long)j * 10 + R;
+  float *f = nullptr, *g = nullptr;
+  bf16* b = nullptr;
+  unsigned long long* k = nullptr;
+  cuda_check(cudaMalloc(&f, n * 4), "cudaMalloc");
+  cuda_check(cudaMalloc(&g, (size_t)W * n * 4), "cudaMalloc");
+  cuda_check(cudaMalloc(&b, n * 2), "cudaMalloc");
+  cuda_check(cudaMalloc(&k, 32), "cudaMalloc");
+  cuda_check(cudaMemcpy(f, hf.data(), n * 4, cudaMemcpyHostToDevice), "H2D");
+  cuda_check(cudaMemcpy(g, hg.data(), (size_t)W * n * 4, cudaMemcpyHostToDevice), "H2D");
+  cuda_check(cudaMemcpy(b, hb.data(), n * 2, cudaMemcpyHostToDevice), "H2D");
+  cuda_check(cudaMemcpy(k, hk.data(), 32, cudaMemcpyHostToDevice), "H2D");
+  c->allreduce_f32(f, n, s);
+  c->allreduce_bf16(b, n, s);
+  c->max_u64(k, 4, s);
+  c->allgather_f32(g, n, s);
+  cuda_check(cudaStreamSynchronize(s), "selftest");
+  cuda_check(cudaMemcpy(hf.data(), f, n * 4, cudaMemcpyDeviceToHost), "D2H");
+  cuda_check(cudaMemcpy(hg.data(), g, (size_t)W * n * 4, cudaMemcpyDeviceToHost), "D2H");
+  cuda_check(cudaMemcpy(hb.data(), b, n * 2, cudaMemcpyDeviceToHost), "D2H");
+  cuda_check(cudaMemcpy(hk.data(), k, 32, cudaMemcpyDeviceToHost), "D2H");
+  cudaFree(f);
+  cudaFree(g);
+  cudaFree(b);
+  cudaFree(k);
+  cudaStreamDestroy(s);
+  const int tri = W * (W - 1) / 2;
+  for (size_t i = 0; i < n; ++i) {
+    if (hf[i] != (float)(1000 * tri + W * (int)(i % 997))) fail(4, "selftest: allreduce f32 mismatch");
+    if (__bfloat162float(hb[i]) != (float)(W * (int)(i % 13) + tri))
+      fail(4, "selftest: allreduce bf16 mismatch");
+    for (int q = 0; q < W; ++q)
+      if (hg[(size_t)q * n + i] != (float)(q + (int)(i % 100))) fail(4, "selftest: allgather mismatch");
+  }
+  for (int j = 0; j < 4; ++j)
+    if (hk[j] != (unsigned long long)j * 10 + (W - 1)) fail(4, "selftest: max_u64 mismatch");
+}
+
 void tp_allreduce_f32(Exec& ex, Comm* comm, float* buf, size_t n) {
   if (ex.world <= 1) return;
   if (!comm) fail(1, "tensor-parallel template without a communicator");
   comm->allreduce_f32(buf, n, ex.compute);
+}
+
+void tp_allreduce_bf16(Exec& ex, Comm* comm, bf16* buf, size_t n) {
+  if (ex.world <= 1) return;
+  if (!comm) fail(1, "tensor-parallel template without a communicator");
+  comm->allreduce_bf16(buf, n, ex.compute);
 }
 
 void tp_argmax_reduce(Exec& ex, Comm* comm, unsigned long long* key, int nseq) {

@@ -215,6 +215,8 @@ struct Work {
   int kb0, kb1;     // main-loop K blocks [kb0, kb1)
   int lora;         // LoRA K-extension blocks follow (last split only)
   int split, tile;
+  int ks;           // split-K parts of this work's tile (1: whole tile)
+  int is_t;         // in-GEMM LoRA shrink tile (T = s A lora_A^T for this pair's rows)
 };
 
 template <int EPI, int BNT, int CG, int MC>
@@ -230,11 +232,42 @@ __device__ __forceinline__ Work decode_work(const GemmParams& p, int w, int pr, 
     r.lora = 0;
     r.split = 0;
     r.tile = w;
+    r.ks = 1;
+    r.is_t = 0;
     return r;
   }
-  const int ks = EPI == EPI_RESID && p.ksplit > 1 ? p.ksplit : 1;
-  r.split = ks > 1 ? w / p.total_tiles : 0;
-  r.tile = w - r.split * p.total_tiles;
+  if (w < 0) {  // T tile -w - 1 (see item_work: first on the least loaded units)
+    w = -w - 1;
+    r.is_t = 1;
+    r.seg = 0;
+    r.n0 = 0;
+    r.m0 = w * (BM * CG * MC) + pr * BM * CG;
+    r.kb0 = 0;
+    r.kb1 = nk;
+    r.lora = 0;
+    r.split = 0;
+    r.tile = w;
+    r.ks = 1;
+    return r;
+  }
+  r.is_t = 0;
+  // EPI_RESID split-K: tiles [0, n_full) run whole, the tail tiles in ksplit
+  // ordered parts (n_full = 0: every tile split); work = n_full + split * n_tail
+  // + tail tile, so part s of a tile is always scheduled after its part s - 1
+  int ks = EPI == EPI_RESID && p.ksplit > 1 ? p.ksplit : 1;
+  if (ks > 1 && w < p.n_full) {
+    ks = 1;
+    r.split = 0;
+    r.tile = w;
+  } else if (ks > 1) {
+    const int v = w - p.n_full, ntail = p.total_tiles - p.n_full;
+    r.split = v / ntail;
+    r.tile = p.n_full + (v - r.split * ntail);
+  } else {
+    r.split = 0;
+    r.tile = w;
+  }
+  r.ks = ks;
   decode_tile<EPI, BNT, CG, MC>(p, r.tile, r.seg, r.n0, r.m0);
   r.m0 += pr * BM * CG;
   const int kps = ks > 1 ? p.kblocks_per_split : nk;
@@ -242,6 +275,24 @@ __device__ __forceinline__ Work decode_work(const GemmParams& p, int w, int pr, 
   r.kb1 = min(nk, r.kb0 + kps);
   r.lora = (nlora > 0 && p.seg[r.seg].lora && r.split == ks - 1) ? nlora : 0;
   return r;
+}
+
+// The i-th work of `unit` (returns false past the end).  T tiles (in-GEMM LoRA
+// shrink) come first and go to the units that the round-robin leaves one work
+// short (the last units), T tile j to unit nunits - 1 - j (mod nunits); then
+// the unit's normal works unit, unit + nunits, ...  Every work a T tile's
+// consumers wait for is thus the first work(s) of some unit.  T tiles are
+// encoded as negative work ids (-j - 1) for decode_work.
+__device__ __forceinline__ bool item_work(const GemmParams& p, int unit, int nunits, int nnorm,
+                                          int i, int& w) {
+  const int t0 = nunits - 1 - unit;  // this unit's first T tile
+  const int nt = p.t_tiles > t0 ? (p.t_tiles - t0 + nunits - 1) / nunits : 0;
+  if (i < nt) {
+    w = -(t0 + i * nunits) - 1;
+    return true;
+  }
+  w = unit + (i - nt) * nunits;
+  return w < nnorm;
 }
 
 __device__ __forceinline__ void epi_bar() {  // the 4 epilogue warps of this CTA
@@ -280,12 +331,15 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
 
   const int nk = (p.K + BK - 1) / BK;
   const int nlora = p.lora_r > 0 ? (EPI == EPI_SILU ? 2 : 1) : 0;
-  const int nwork = EPI == EPI_RESID && p.ksplit > 1 ? p.total_tiles * p.ksplit : p.total_tiles;
+  const int nwork = EPI == EPI_RESID && p.ksplit > 1
+                        ? p.n_full + (p.total_tiles - p.n_full) * p.ksplit
+                        : p.total_tiles;  // normal works (T tiles come on top)
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&p.a);
     for (int i = 0; i < 3; ++i)
       if (i < p.nseg || (EPI == EPI_SILU && i < 2)) ptx::prefetch_tmap(&p.b[i]);
+    for (int i = 0; i < p.t_nt; ++i) ptx::prefetch_tmap(&p.la[i]);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full_bar(s), CG);  // leader expect_tx + peer arrive
       ptx::mbar_init(empty_bar(s), MC);  // one MMA commit per pair of the cluster
@@ -332,12 +386,56 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       };
       int stage = 0;
       uint32_t phase = 0;
-      for (int w = unit; w < nwork; w += nunits) {
+      uint64_t tseen[GEMM_MAX_TBLK / 64] = {};  // row blocks whose T this CTA saw ready
+      int w;
+      for (int it = 0; item_work(p, unit, nunits, nwork, it, w); ++it) {
         const Work wk = decode_work<EPI, BNT, CG, MC>(p, w, pr, nk, nlora);
         const int seg = wk.seg, n0 = wk.n0;
         const int ma = wk.m0 + rank * BM;  // this CTA's A rows
         const int nkb = wk.kb1 + wk.lora;
+        if (EPI != EPI_PARTIAL && wk.is_t) {
+          // T tile: this CTA stages its 128 rows of A and its t_rt_pad / CG rows of
+          // the stacked [lora_A_0; lora_A_1; ...] (8-row boxes; padding rows are
+          // never loaded — their accumulator columns are never read)
+          const int half = p.t_rt_pad / CG, rt = p.t_nt * p.t_r;
+          for (int kb = 0; kb < ((p.t_diag & 4) ? 0 : nk); ++kb) {
+            ptx::mbar_wait(empty_bar(stage), phase ^ 1);
+            const uint32_t sa = sbase + OFF_A + stage * A_BYTES;
+            const uint32_t sb = sbase + OFF_B + stage * BBYTES;
+            const uint32_t fb = full_bar(stage);
+            if (rank == 0)
+              ptx::mbar_expect_tx(fb, A_BYTES * CG + rt * ROW_BYTES);
+            else
+              ptx::mbar_arrive_leader(fb);
+            tma(&p.a, sa, fb, kb * BK, ma);
+            for (int c = 0; c < half; c += 8) {
+              const int srow = rank * half + c;
+              if (srow >= rt) break;
+              const int t = srow / p.t_r;
+              tma(&p.la[t], sb + c * ROW_BYTES, fb, kb * BK, srow - t * p.t_r);
+            }
+            if (++stage == STAGES) {
+              stage = 0;
+              phase ^= 1;
+            }
+          }
+          continue;
+        }
         for (int kb = wk.kb0; kb < nkb; ++kb) {
+          if (EPI != EPI_PARTIAL && p.t_tiles > 0 && kb == wk.kb1) {
+            // the LoRA K-extension reads T of this CTA's rows: wait for its T tile
+            // (once per 128-row block and CTA: later tiles of the block find it set)
+            const int blk = ma / BM;
+            const uint64_t bit = 1ull << (blk & 63);
+            if (!(tseen[blk >> 6] & bit) && !(p.t_diag & 2)) {
+              const int* f = p.t_flags + blk;
+              uint32_t n = 0;
+              while (ld_acquire(f) == 0)
+                if (++n == (1u << 30)) __trap();
+              if (!(p.t_diag & 1)) asm volatile("fence.proxy.async.global;" ::: "memory");
+              tseen[blk >> 6] |= bit;
+            }
+          }
           ptx::mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + OFF_A + stage * A_BYTES;
           const uint32_t sb = sbase + OFF_B + stage * BBYTES;
@@ -391,6 +489,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     if (rank == 0) {  // whole warp: uniform control flow, one elected lane issues
       constexpr uint32_t IDESC = ptx::idesc_bf16(BM * CG, BNX);
       constexpr uint32_t IDESC_HALF = ptx::idesc_bf16(BM * CG, 128);
+      const uint32_t IDESC_T = ptx::idesc_bf16(BM * CG, p.t_rt_pad > 0 ? p.t_rt_pad : 16);
       const int nmma_lora = (p.lora_r + 15) / 16;
       auto mma = [&](uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
         ptx::mma_bf16_ws<CG>(d, a, b, id, acc);
@@ -411,9 +510,10 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       uint32_t phase = 0;
       int acc = 0;
       uint32_t acc_phase = 0;
-      for (int w = unit; w < nwork; w += nunits) {
+      int w;
+      for (int it = 0; item_work(p, unit, nunits, nwork, it, w); ++it) {
         const Work wk = decode_work<EPI, BNT, CG, MC>(p, w, pr, nk, nlora);
-        const int kb0 = wk.kb0, nkb = wk.kb1 + wk.lora;
+        const int kb0 = wk.kb0, nkb = (wk.is_t && (p.t_diag & 4)) ? 0 : wk.kb1 + wk.lora;
         ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BNX;
@@ -422,7 +522,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           ptx::tc_fence_after();
           const uint64_t adesc = ptx::desc_sw128(sbase + OFF_A + stage * A_BYTES);
           const uint64_t bdesc = ptx::desc_sw128(sbase + OFF_B + stage * BBYTES);
-          if (EPI == EPI_PARTIAL || kb < wk.kb1) {
+          if (EPI != EPI_PARTIAL && wk.is_t) {
+#pragma unroll
+            for (int k = 0; k < BK / 16; ++k)
+              mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC_T, (kb | k) != 0);
+          } else if (EPI == EPI_PARTIAL || kb < wk.kb1) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
               mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC, ((kb - kb0) | k) != 0);
@@ -453,7 +557,8 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     uint8_t* stg = smem + OFF_STG + (warp - 2) * STG_WARP;
     int acc = 0;
     uint32_t acc_phase = 0;
-    for (int wi = unit; wi < nwork; wi += nunits) {
+    int wi;
+    for (int it = 0; item_work(p, unit, nunits, nwork, it, wi); ++it) {
       const Work wk = decode_work<EPI, BNT, CG, MC>(p, wi, pr, nk, nlora);
       const int tile = wk.tile, n0 = wk.n0, m0 = wk.m0;
       const GemmSeg sg = p.seg[wk.seg];
@@ -463,7 +568,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       const int row0 = m0 + rank * BM + q * 32;
       const int m = row0 + lane;
       float v[32], w[32];
-      if (EPI == EPI_PARTIAL) {
+      if (EPI != EPI_PARTIAL && wk.is_t) {
+        // T_t[m, j] = bf16(s * acc[m, t * r + j]): 8-column groups never straddle
+        // targets (r % 8 == 0); each thread writes its own row (rows contiguous)
+        const int rt = p.t_nt * p.t_r;
+#pragma unroll 1
+        for (int j = 0; j * 32 < rt; ++j) {
+          ld_chunk(tacc + j * 32, v);
+          if (m < p.M) {
+#pragma unroll
+            for (int g = 0; g < 4; ++g) {
+              const int c0 = j * 32 + g * 8;
+              if (c0 < rt) {
+                const int t = c0 / p.t_r;
+                uint4 o;
+                o.x = pack_bf16x2(p.t_scale * v[8 * g + 0], p.t_scale * v[8 * g + 1]);
+                o.y = pack_bf16x2(p.t_scale * v[8 * g + 2], p.t_scale * v[8 * g + 3]);
+                o.z = pack_bf16x2(p.t_scale * v[8 * g + 4], p.t_scale * v[8 * g + 5]);
+                o.w = pack_bf16x2(p.t_scale * v[8 * g + 6], p.t_scale * v[8 * g + 7]);
+                *reinterpret_cast<uint4*>(p.t_out[t] + (size_t)m * p.t_r + (c0 - t * p.t_r)) = o;
+              }
+            }
+          }
+        }
+        // publish: stores visible (generic and async proxy) before the flag
+        __threadfence();
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        epi_bar();
+        if (threadIdx.x == 64) st_release(p.t_flags + (m0 + rank * BM) / BM, 1);
+      } else if (EPI == EPI_PARTIAL) {
         const int ks = tile / p.m_tiles;
         const int ncols = p.nseg * p.src_rows;
         float* out = reinterpret_cast<float*>(p.out) + (size_t)ks * p.M * p.ldo;
@@ -489,7 +622,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
         }
       } else if (EPI == EPI_RESID) {
         const int ncols = min(BNT, sg.n - n0);
-        const int ks = p.ksplit > 1 ? p.ksplit : 1;
+        const int ks = wk.ks;
         int* flag = ks > 1 ? p.flags + (tile * MC + pr) * CG + rank : nullptr;
         if (ks > 1 && wk.split > 0) {
           // split s adds after split s-1 of this tile half has landed
@@ -618,7 +751,11 @@ cudaError_t launch_t(const GemmParams& p, int num_sms, cudaStream_t s) {
     attr_done = true;
   }
   const int units = gemm_units(CG, MC, num_sms);
-  const int grid = (p.total_tiles < units ? p.total_tiles : units) * CG * MC;
+  const int works = (EPI == EPI_RESID && p.ksplit > 1
+                         ? p.n_full + (p.total_tiles - p.n_full) * p.ksplit
+                         : p.total_tiles) +
+                    (EPI == EPI_PARTIAL ? 0 : p.t_tiles);
+  const int grid = (works < units ? works : units) * CG * MC;
   if (grid <= 0) return cudaSuccess;
   return launch_kt(EPI == EPI_PARTIAL ? "shrink" : "gemm", gemm_tc_kernel<EPI, BNT, CG, MC>, dim3(grid), dim3(NTHREADS),
                   Cfg<EPI, BNT, CG>::SMEM_BYTES, s, CG * MC, p);
@@ -720,29 +857,63 @@ static void gemm_plan_resid_single(int M, int N, int K, int num_sms, int* bn_out
   *bn_out = gemm_pick_bn(EPI_RESID, M, &N, 1, num_sms);
 }
 
-void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out, int* cg_out) {
+void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out, int* cg_out,
+                     bool allow_split, int* nfull_out) {
   if (cg_out) *cg_out = gemm_pick_cg(M);
+  if (nfull_out) *nfull_out = 0;
   const int cg = gemm_pick_cg(M), mc = gemm_pick_mc(M, num_sms);
   const long mt = gemm_m_tiles(M, cg, mc);
   const long units = gemm_units(cg, mc, num_sms);
   const int nk = (K + BK - 1) / BK;
+  static const int split_env = [] {
+    const char* e = getenv("TIDAL_RESID_SPLIT");  // 0: no split-K; 1: uniform parts only
+    return e ? e[0] - '0' : 2;
+  }();
+  const bool tail_ok = nfull_out != nullptr && split_env >= 2;
   static const int cands[] = {256, 192, 128};
+  // cost = rounds x (K-blocks per part + ~11 K-blocks of per-part epilogue and
+  // hand-off) x time per K-block.  A K-block of a 192-wide pair tile takes as
+  // long as a 256-wide one (tools/gemm_bench.py --resid-sweep, 13B S = 2048:
+  // O 256 x 3 parts 84 us, 192 x 1 part 97-127 us), so only 128-wide tiles
+  // are charged less (their A-operand traffic per MAC doubles: x 0.75).
   double best = 1e30;
-  int bb = 256, bk = 1;
+  int bb = 256, bk = 1, bf = 0;
   for (int bn : cands) {
     const long tiles = mt * ((N + bn - 1) / bn);
     if (tiles * mc * cg > GEMM_MAX_FLAGS) continue;
-    const double kb_bytes = A_BYTES + (double)(bn / cg) * ROW_BYTES;
+    const double kb_cost = bn == 128 ? 0.75 : 1.0;
+    // (a) every tile in ks ordered parts
     for (int ks = 1; ks <= 8 && ks <= nk; ++ks) {
       const int kps = (nk + ks - 1) / ks;
       const int ks_eff = (nk + kps - 1) / kps;  // every part non-empty
       if (ks_eff != ks) continue;
       const long rounds = (tiles * ks + units - 1) / units;
-      const double cost = (double)rounds * (kps + 11) * kb_bytes;
+      const double cost = (double)rounds * (kps + 11) * kb_cost;
       if (cost < best * 0.98) {  // prefer fewer parts unless clearly better
         best = cost;
         bb = bn;
         bk = ks;
+        bf = 0;
+      }
+    }
+    // (b) opt-in (TIDAL_RESID_SPLIT=3): whole tiles for the full waves, the
+    // last partial wave's tiles in ordered parts.  Measured slower than (a):
+    // the parts of one tile run concurrently, so their ordered epilogues
+    // serialise (O 256-wide: 92-116 us against 84 us uniform).
+    const long full = tiles / units, tail = tiles - full * units;
+    if (tail_ok && split_env == 3 && full >= 1 && tail > 0) {
+      int ks = (int)(units / tail);
+      ks = ks > 8 ? 8 : (ks > nk ? nk : ks);
+      if (ks >= 2) {
+        const int kps = (nk + ks - 1) / ks;
+        const int ks_eff = (nk + kps - 1) / kps;
+        const double cost = ((double)full * (nk + 11) + (kps + 11)) * kb_cost;
+        if (cost < best * 0.98) {
+          best = cost;
+          bb = bn;
+          bk = ks_eff;
+          bf = (int)(full * units);
+        }
       }
     }
   }
@@ -762,17 +933,14 @@ void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out,
       }
     }
   }
-  static const bool no_split = [] {
-    const char* e = getenv("TIDAL_RESID_SPLIT");
-    return e && e[0] == '0';
-  }();
-  if (no_split && bk > 1) {  // best single-part width instead
+  if ((split_env == 0 || !allow_split) && bk > 1) {  // best single-part width instead
     gemm_plan_resid_single(M, N, K, num_sms, bn_out);
     *ks_out = 1;
     return;
   }
   *bn_out = bb;
   *ks_out = bk;
+  if (nfull_out) *nfull_out = bf;
 }
 
 int gemm_b_box(int epi, int bn, int cg, int mc) { return (epi == EPI_SILU ? 128 : bn / cg) / mc; }

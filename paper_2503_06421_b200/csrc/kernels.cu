@@ -181,6 +181,37 @@ __global__ void __launch_bounds__(HEAD_THREADS) head_kernel(const float* __restr
   }
 }
 
+// ---------------- TP bf16 allreduce option ----------------
+// Pb = bf16(P) (the row-parallel partial sum), and after the allreduce X += Pb.
+__global__ void f32_to_bf16_kernel(const float4* __restrict__ P, uint2* __restrict__ Pb, size_t n4) {
+  ptx::pdl_begin();
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const float4 v = P[i];
+    __nv_bfloat162 a = __floats2bfloat162_rn(v.x, v.y), b = __floats2bfloat162_rn(v.z, v.w);
+    uint2 o;
+    o.x = *reinterpret_cast<uint32_t*>(&a);
+    o.y = *reinterpret_cast<uint32_t*>(&b);
+    Pb[i] = o;
+  }
+}
+
+__global__ void add_bf16_kernel(const uint2* __restrict__ Pb, float4* __restrict__ X, size_t n4) {
+  ptx::pdl_begin();
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n4;
+       i += (size_t)gridDim.x * blockDim.x) {
+    uint2 w = Pb[i];
+    const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&w);
+    const float2 a = __bfloat1622float2(h[0]), b = __bfloat1622float2(h[1]);
+    float4 x = X[i];
+    x.x += a.x;
+    x.y += a.y;
+    x.z += b.x;
+    x.w += b.y;
+    X[i] = x;
+  }
+}
+
 // ---------------- debug / invariants ----------------
 __global__ void poison_kernel(uint16_t* p, size_t n) {
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n;
@@ -251,6 +282,18 @@ cudaError_t head_launch(const float* X_last, size_t x_stride, int nseq, const bf
     if (e != cudaSuccess) return e;
   }
   return cudaSuccess;
+}
+
+cudaError_t tp_pack_bf16_launch(const float* P, bf16* Pb, size_t n, int num_sms, cudaStream_t s) {
+  if (n % 4) return cudaErrorInvalidValue;
+  return launch_k(f32_to_bf16_kernel, dim3(num_sms * 4), dim3(256), 0, s, 1,
+                  reinterpret_cast<const float4*>(P), reinterpret_cast<uint2*>(Pb), n / 4);
+}
+
+cudaError_t tp_add_bf16_launch(const bf16* Pb, float* X, size_t n, int num_sms, cudaStream_t s) {
+  if (n % 4) return cudaErrorInvalidValue;
+  return launch_k(add_bf16_kernel, dim3(num_sms * 4), dim3(256), 0, s, 1,
+                  reinterpret_cast<const uint2*>(Pb), reinterpret_cast<float4*>(X), n / 4);
 }
 
 cudaError_t poison_launch(void* p, size_t bytes, cudaStream_t s) {

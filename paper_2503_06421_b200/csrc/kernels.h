@@ -57,12 +57,28 @@ struct alignas(64) GemmParams {
   int bn;              // N tile: 256 | 192 | 128 (EPI_SILU: 128 output cols = 256 acc cols)
   bf16* vt;            // V^T [n_vt][vt_ld] for the tcgen05 attention (segments with vt=1)
   int vt_ld;
-  int ksplit, kblocks_per_split, src_rows;  // EPI_PARTIAL
+  int ksplit, kblocks_per_split, src_rows;  // EPI_PARTIAL / EPI_RESID split-K
+  int n_full;          // EPI_RESID with ksplit > 1: tiles [0, n_full) run whole, the rest
+                       // in ksplit ordered parts (0: every tile split)
   int cg;              // 1: single-CTA 128-row tiles; 2: CTA pair, 256-row tiles (cta_group::2)
   int mc;              // cg == 2: CTA pairs per cluster sharing W boxes (1 or 2; 0 = 1)
   int* flags;          // EPI_RESID with ksplit > 1: per (tile, CTA) split counters, all 0
                        // between launches (GEMM_MAX_FLAGS ints); parts add in split order
+  // In-GEMM LoRA shrink ("T tiles", t_tiles > 0): the first t_tiles works of the
+  // persistent grid compute T_t = bf16(t_scale * A x lora_A_t^T) for the t_nt
+  // targets sharing this GEMM's input A (stacked: t_nt * t_r columns, MMA N =
+  // t_rt_pad) into t_out[t] [M, t_r] and release t_flags[row / 128] = 1; the
+  // LoRA K-extension of every other tile waits for the flag of its rows.  The
+  // flags are zeroed once per forward.  Requires every CTA of the grid to be
+  // able to run (persistent grid <= SMs, no co-located grids).
+  CUtensorMap la[3];   // lora_A_t [t_r, K], box {64 cols, 8 rows}
+  bf16* t_out[3];
+  int t_tiles, t_nt, t_r, t_rt_pad;
+  float t_scale;
+  int* t_flags;
+  int t_diag;          // diagnostics (bit 0: no consumer-side proxy fence); 0 in production
 };
+constexpr int GEMM_MAX_TBLK = 256;  // 128-row blocks with T-ready flags (32768 rows)
 
 // CTA-group size for an M-row GEMM, and the TMA box rows of the W and lora_B
 // maps a CTA loads for (epi, bn, cg).
@@ -77,7 +93,12 @@ int gemm_b_box(int epi, int bn, int cg, int mc = 1);
 constexpr int GEMM_MAX_FLAGS = 16384;
 // cg_out (optional): also choose the CTA group — single-CTA tiles when they fit
 // one wave and pair tiles would not (short prompts); else the pair default.
-void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn, int* ks, int* cg_out = nullptr);
+// allow_split = false: one part only (no CTA waits on another CTA's flag —
+// required when several persistent grids may share the device).
+// nfull_out (optional): allow a tail split — tiles [0, *nfull_out) whole, the
+// rest in ks parts (GemmParams::n_full); without it every tile has ks parts.
+void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn, int* ks, int* cg_out = nullptr,
+                     bool allow_split = true, int* nfull_out = nullptr);
 int gemm_tb_box(int epi, int bn, int cg, int mc = 1);
 
 // LoRA shrink on tensor cores: T_t = bf16(scale * X A_t^T) for nt targets
@@ -214,6 +235,10 @@ cudaError_t dec_save_logits_launch(const DecodeState* st, const float* logits, f
                                    cudaStream_t s);
 cudaError_t dec_gemv_launch(const DecGemv& p, int mode, int num_sms, cudaStream_t s);
 cudaError_t dec_attn_launch(const DecAttn& a, int max_keys, cudaStream_t s);
+
+// TP bf16 allreduce option: Pb = bf16(P) before, X += Pb after the allreduce.
+cudaError_t tp_pack_bf16_launch(const float* P, bf16* Pb, size_t n, int num_sms, cudaStream_t s);
+cudaError_t tp_add_bf16_launch(const bf16* Pb, float* X, size_t n, int num_sms, cudaStream_t s);
 
 // Debug / invariants.
 cudaError_t poison_launch(void* p, size_t bytes, cudaStream_t s);           // bf16 NaN 0x7FC0

@@ -62,11 +62,23 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   dalloc(tok, S * 4);
   dalloc(shrink_ws, (size_t)SHRINK_MAX_SPLIT * S * 192 * 4);
   dalloc(gemm_flags, GEMM_MAX_FLAGS * sizeof(int));
+  dalloc(zero_b, (size_t)(m.d_ff / world) * 64 * 2);
+  cuda_check(cudaMemset(zero_b, 0, (size_t)(m.d_ff / world) * 64 * 2), "memset zero lora_B");
+  tflag_stride = (int)((S + 127) / 128 + 2);
+  dalloc(tflags, (size_t)m.n_layers * 4 * tflag_stride * sizeof(int));
+  {
+    const char* e = getenv("TIDAL_FUSED_SHRINK");
+    fuse_shrink = e && e[0] == '1';
+  }
   cuda_check(cudaMemset(gemm_flags, 0, GEMM_MAX_FLAGS * sizeof(int)), "memset flags");
   // V^T: batched prompts pad each sequence to 64 columns (<= 63 per prompt)
   vt_ld = (int)((S + 63) / 64 * 64 + 64 * (size_t)kMaxBatch);
   dalloc(Vt, nkv * (size_t)vt_ld * 2);
   cuda_check(cudaMemset(Vt, 0, nkv * (size_t)vt_ld * 2), "memset V^T");  // padding stays finite
+  if (world > 1) {  // bf16 allreduce option (allocated up front: the option may be set any time)
+    dalloc(P32, S * m.d_model * 4);
+    dalloc(Pb, S * m.d_model * 2);
+  }
   build_rope((int)S);
   cuda_check(cudaHostAlloc((void**)&h_tok, S * 4 + 16, cudaHostAllocDefault), "pinned tokens");
   cuda_check(cudaHostAlloc((void**)&h_logits, (size_t)kMaxBatch * m.vocab * 4 + 16,
@@ -133,7 +145,8 @@ void Exec::destroy() {
   cudaSetDevice(device);
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
-  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws, gemm_flags,
+  void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws, gemm_flags, P32, Pb, tflags,
+                  zero_b,
                   dec.kc, dec.vc, dec.q, dec.att, dec.h, dec.T, dec.part, dec.cnt, dec.shcnt, dec.st,
                   dec.toks,
                   dec.logits_all};
@@ -220,7 +233,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     GemmParams& o = ll.o;
     memset(&o, 0, sizeof o);
     int ks = 1;
-    gemm_plan_resid(S, d, nq, num_sms, &o.bn, &ks, &o.cg);
+    gemm_plan_resid(S, d, nq, num_sms, &o.bn, &ks, &o.cg, !colocated, &o.n_full);
     o.ksplit = ks;
     o.kblocks_per_split = ((nq + GEMM_BK - 1) / GEMM_BK + ks - 1) / ks;
     o.flags = gemm_flags;
@@ -256,13 +269,19 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     tmap(&g.b[0], W(tt.proj[l][T_GATE]), F, d, gemm_b_box(EPI_SILU, 128, g.cg, g.mc));
     tmap(&g.b[1], W(tt.proj[l][T_UP]), F, d, gemm_b_box(EPI_SILU, 128, g.cg, g.mc));
     g.seg[0].n = F;
-    g.seg[0].lora = tt.lora_a[l][T_GATE] >= 0;
-    if (g.seg[0].lora) {
-      g.lora_r = r;
-      tmap(&g.ta[0], T[T_GATE], S, r, 128);
-      tmap(&g.ta[1], T[T_UP], S, r, 128);
-      tmap(&g.tb[0], W(tt.lora_b[l][T_GATE]), F, r, gemm_tb_box(EPI_SILU, 128, g.cg, g.mc));
-      tmap(&g.tb[1], W(tt.lora_b[l][T_UP]), F, r, gemm_tb_box(EPI_SILU, 128, g.cg, g.mc));
+    {
+      // the paired gate/up tile has one LoRA K-extension per half; a target the
+      // adapter leaves out gets an all-zero lora_B box (its T is any finite T)
+      const bool lg = tt.lora_a[l][T_GATE] >= 0, lu = tt.lora_a[l][T_UP] >= 0;
+      g.seg[0].lora = lg || lu;
+      if (lg || lu) {
+        g.lora_r = r;
+        const int tbb = gemm_tb_box(EPI_SILU, 128, g.cg, g.mc);
+        tmap(&g.ta[0], T[lg ? T_GATE : T_UP], S, r, 128);
+        tmap(&g.ta[1], T[lu ? T_UP : T_GATE], S, r, 128);
+        tmap(&g.tb[0], lg ? W(tt.lora_b[l][T_GATE]) : zero_b, F, r, tbb);
+        tmap(&g.tb[1], lu ? W(tt.lora_b[l][T_UP]) : zero_b, F, r, tbb);
+      }
     }
     g.nseg = 1;
     g.bn = 128;
@@ -276,7 +295,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     // ---- down (+ residual) ----
     GemmParams& dn = ll.down;
     memset(&dn, 0, sizeof dn);
-    gemm_plan_resid(S, d, F, num_sms, &dn.bn, &ks, &dn.cg);
+    gemm_plan_resid(S, d, F, num_sms, &dn.bn, &ks, &dn.cg, !colocated, &dn.n_full);
     dn.ksplit = ks;
     dn.kblocks_per_split = ((F + GEMM_BK - 1) / GEMM_BK + ks - 1) / ks;
     dn.flags = gemm_flags;
@@ -304,6 +323,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
       const std::initializer_list<int> groups[4] = {{T_Q, T_K, T_V}, {T_O}, {T_GATE, T_UP}, {T_DOWN}};
       const bf16* inputs[4] = {Xn, O, Xn, Hb};
       const int kdim[4] = {d, nq, d, F};
+      GemmParams* gp[4] = {&ll.qkv, &ll.o, &ll.gu, &ll.down};
       for (int gi = 0; gi < 4; ++gi) {
         const bf16* A[3];
         bf16* Tt[3];
@@ -315,6 +335,27 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
             ++n;
           }
         if (!n) continue;
+        // in-GEMM T tiles when the stacked lora_A fits one accumulator buffer and
+        // no other grid can share the device (a T-tile wait needs its producer CTA)
+        GemmParams& g = *gp[gi];
+        const int rt_pad = (n * r + 15) / 16 * 16;
+        const int bnx = gi == 2 ? 256 : g.bn;
+        if (fuse_shrink && !colocated && g.mc <= 1 && rt_pad <= bnx &&
+            (S + 127) / 128 <= GEMM_MAX_TBLK) {
+          static const int diag = getenv("TIDAL_TDIAG") ? atoi(getenv("TIDAL_TDIAG")) : 0;
+          g.t_diag = diag;
+          for (int s2 = 0; s2 < n; ++s2) {
+            if (!make_tmap(&g.la[s2], A[s2], r, kdim[gi], (uint64_t)kdim[gi] * 2, 8, 64))
+              fail(3, "lora_A tensor maps");
+            g.t_out[s2] = Tt[s2];
+          }
+          g.t_nt = n;
+          g.t_r = r;
+          g.t_rt_pad = rt_pad;
+          g.t_tiles = g.m_tiles;
+          g.t_flags = tflags + (size_t)(4 * l + gi) * tflag_stride;
+          continue;
+        }
         if (!shrink_plan(&ll.sh[gi], inputs[gi], S, kdim[gi], A, Tt, n, r, shrink_ws, num_sms))
           fail(3, "shrink tensor maps");
         ll.has_sh[gi] = 1;
@@ -394,6 +435,7 @@ static int op_kind(const std::string& n) {
 
 // TP collectives (comm.cu); no-ops when world == 1.
 void tp_allreduce_f32(Exec& ex, Comm* comm, float* buf, size_t n);
+void tp_allreduce_bf16(Exec& ex, Comm* comm, bf16* buf, size_t n);
 void tp_argmax_reduce(Exec& ex, Comm* comm, unsigned long long* key, int nseq);
 void tp_allgather_logits(Exec& ex, Comm* comm, int nseq);
 
@@ -440,6 +482,36 @@ void run_forward(Exec& ex, const RunArgs& a) {
     return n;
   };
   const int nkv = m.n_kv_heads * hd / ex.world;
+  // row-parallel GEMMs under TP: rank 0 adds its partial sum to the residual,
+  // the others start from zero (the allreduce then sums residual + partials);
+  // with the bf16 allreduce every rank's partial goes to P32 instead
+  const bool bf16_ar = ex.world > 1 && ex.ar_bf16;
+  // GEMM launch; with in-GEMM T tiles the invocation's LoRA scale goes into a
+  // copy of the cached parameters
+  auto launch = [&](const GemmParams& g, int epi, float* out_override = nullptr) {
+    if (!g.t_tiles && !out_override) return gemm_launch(g, epi, ex.num_sms, st);
+    GemmParams p = g;
+    p.t_scale = a.lora_scale;
+    if (out_override) p.out = out_override;
+    return gemm_launch(p, epi, ex.num_sms, st);
+  };
+  auto resid_gemm = [&](const GemmParams& g) {
+    if (bf16_ar) {
+      cuda_check(cudaMemsetAsync(ex.P32, 0, (size_t)S * d * 4, st), "memset partial");
+      return launch(g, EPI_RESID, ex.P32);
+    }
+    if (ex.world > 1 && ex.rank != 0)
+      cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
+    return launch(g, EPI_RESID);
+  };
+  // the T-ready flags of the in-GEMM LoRA shrinks start at 0 in every forward
+  if (r) {
+    bool fused = false;
+    for (const LayerLaunch& ll : LP) fused |= ll.qkv.t_tiles || ll.o.t_tiles || ll.gu.t_tiles || ll.down.t_tiles;
+    if (fused)
+      cuda_check(cudaMemsetAsync(ex.tflags, 0, (size_t)m.n_layers * 4 * ex.tflag_stride * sizeof(int), st),
+                 "memset T flags");
+  }
   const std::vector<Op>& ops = *a.ops;
   for (size_t k = 0; k < ops.size(); ++k) {
     const Op& op = ops[k];
@@ -476,8 +548,19 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_MLP_AR:
         {
           const int e0 = P0();
-          tp_allreduce_f32(ex, a.comm, ex.X, (size_t)S * d);
-          if (e0 >= 0) ex.prof_end(KC_ALLREDUCE, e0, 0, Sd * d * 4);
+          const size_t n = (size_t)S * d;
+          if (bf16_ar && op_kind(op.name) != OP_EMBED_AR) {
+            // C1/C2 in bf16: the partial sum (P32, no residual) is rounded once,
+            // reduced in bf16 and added to the fp32 residual stream
+            cuda_check(tp_pack_bf16_launch(ex.P32, ex.Pb, n, ex.num_sms, st), "tp pack");
+            tp_allreduce_bf16(ex, a.comm, ex.Pb, n);
+            cuda_check(tp_add_bf16_launch(ex.Pb, ex.X, n, ex.num_sms, st), "tp add");
+            ex.launches += 2;
+            if (e0 >= 0) ex.prof_end(KC_ALLREDUCE, e0, 0, Sd * d * 2);
+          } else {
+            tp_allreduce_f32(ex, a.comm, ex.X, n);
+            if (e0 >= 0) ex.prof_end(KC_ALLREDUCE, e0, 0, Sd * d * 4);
+          }
         }
         break;
       case OP_ATTN_NORM:
@@ -493,7 +576,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
           const double n = nq + 2.0 * nkv;
           const int e0 = P0(KC_GEMM_QKV);
           K(KC_GEMM_QKV, e0, 2.0 * Sd * (n * d + r * lora_n(l, {T_Q, T_K, T_V})),
-            2.0 * (n * d + Sd * d + Sd * n), gemm_launch(LP[l].qkv, EPI_ROPE, ex.num_sms, st),
+            2.0 * (n * d + Sd * d + Sd * n), launch(LP[l].qkv, EPI_ROPE),
             "gemm_qkv");
         }
         break;
@@ -512,13 +595,11 @@ void run_forward(Exec& ex, const RunArgs& a) {
         break;
       case OP_O:
         shrink(ex.O, nq, nq, l, 1);
-        if (ex.world > 1 && ex.rank != 0)
-          cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
         {
           const int e0 = P0(KC_GEMM_O);
           K(KC_GEMM_O, e0, 2.0 * Sd * d * ((double)nq + r * lora_n(l, {T_O}) / d),
             2.0 * ((double)d * nq + Sd * nq) + 8.0 * Sd * d,
-            gemm_launch(LP[l].o, EPI_RESID, ex.num_sms, st), "gemm_o");
+            resid_gemm(LP[l].o), "gemm_o");
         }
         break;
       case OP_MLP_NORM:
@@ -533,7 +614,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         {
           const int e0 = P0(KC_GEMM_GU);
           K(KC_GEMM_GU, e0, 2.0 * Sd * (2.0 * F * d + r * lora_n(l, {T_GATE, T_UP})),
-            2.0 * (2.0 * F * d + Sd * d + Sd * F), gemm_launch(LP[l].gu, EPI_SILU, ex.num_sms, st),
+            2.0 * (2.0 * F * d + Sd * d + Sd * F), launch(LP[l].gu, EPI_SILU),
             "gemm_gate_up");
         }
         break;
@@ -541,13 +622,11 @@ void run_forward(Exec& ex, const RunArgs& a) {
         break;
       case OP_DOWN:
         shrink(ex.Hb, F, F, l, 3);
-        if (ex.world > 1 && ex.rank != 0)
-          cuda_check(cudaMemsetAsync(ex.X, 0, (size_t)S * d * 4, st), "memset partial");
         {
           const int e0 = P0(KC_GEMM_DOWN);
           K(KC_GEMM_DOWN, e0, 2.0 * Sd * ((double)d * F + r * lora_n(l, {T_DOWN})),
             2.0 * ((double)d * F + Sd * F) + 8.0 * Sd * d,
-            gemm_launch(LP[l].down, EPI_RESID, ex.num_sms, st), "gemm_down");
+            resid_gemm(LP[l].down), "gemm_down");
         }
         break;
       case OP_FNORM:  // fused into the head kernel (fp32 last-row norm)

@@ -52,7 +52,19 @@ struct Exec {
   float2* rope = nullptr;
   float* shrink_ws = nullptr;  // split-K partials of the LoRA shrink
   int* gemm_flags = nullptr;   // ordered split-K counters of the residual GEMMs (all 0 at rest)
+  // in-GEMM LoRA shrink: per (layer, GEMM) a row-block array of T-ready flags,
+  // zeroed at the start of every forward; tflag_stride ints per GEMM
+  int* tflags = nullptr;
+  int tflag_stride = 0;
+  bool fuse_shrink = true;
+  bf16* zero_b = nullptr;      // [F / world][64] zeros: lora_B of an untargeted gate or up half     // T tiles inside the GEMMs (else split-K shrink + reduce launches)
   bf16* Vt = nullptr;  // V^T [KV*hd][vt_ld] (tcgen05 attention, hd = 128)
+  // TP: row-parallel partial sums for the bf16 allreduce option (C1/C2 in
+  // bf16): the GEMM adds into P32 (zeroed), P32 -> Pb, allreduce(Pb), X += Pb
+  bool ar_bf16 = false;
+  bool colocated = false;  // TP ranks share this GPU (Comm::colocated)
+  float* P32 = nullptr;
+  bf16* Pb = nullptr;
   int vt_ld = 0;
   std::map<std::pair<int, int>, AttnParams> attn_cache;  // per (rows, prompts)
   // decode continuation (decode.cu): KV cache filled by the prefill's QKV
@@ -70,6 +82,7 @@ struct Exec {
     float* logits_all = nullptr;      // [max_new][V]
     int prompt_len = 0;               // rows of the cache valid (last single-prompt prefill)
     const void* prompt_akey = nullptr;
+    uint64_t prompt_adapter = 0;      // serial of the prefill's adapter (0: none)
     uint64_t prompt_gen = 0;
     cudaGraphExec_t gexec = nullptr;
     int launches_per_step = 0;
@@ -136,8 +149,13 @@ struct Recorder {  // lax tracing: first-read order of weights as ops execute
 // floats, this rank's slice filled in place.
 struct Comm {
   int world = 1, rank = 0, device = 0;
+  // ranks may share a GPU (LocalComm): kernels whose CTAs wait on other CTAs
+  // of the same grid (ordered split-K, in-GEMM LoRA T tiles) are not used,
+  // since two ranks' persistent grids may each be only partly resident
+  bool colocated = false;
   virtual ~Comm() {}
   virtual void allreduce_f32(float* buf, size_t n, cudaStream_t s) = 0;
+  virtual void allreduce_bf16(bf16* buf, size_t n, cudaStream_t s) = 0;
   virtual void max_u64(unsigned long long* key, size_t n, cudaStream_t s) = 0;
   virtual void allgather_f32(float* buf, size_t n, cudaStream_t s) = 0;
 };

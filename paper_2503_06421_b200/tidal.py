@@ -22,7 +22,9 @@ ERR_NAMES = {0: "OK", 1: "INVALID", 2: "OOM", 3: "CUDA", 4: "NCCL", 5: "STRUCTUR
 GROUPS_PER_LAYER, GROUPS_MAX_TRANSFERS, GROUPS_PER_TENSOR = 0, 1, 2
 DEBUG_POISON, DEBUG_SKIP_BARRIER, DEBUG_SCRUB_L2, DEBUG_SERIAL, DEBUG_PROFILE = 1, 2, 4, 8, 16
 DEBUG_PROFILE_GEMM = 32
+DEBUG_NO_GRAPH = 64
 ORDER_TRACED, ORDER_REVERSE, ORDER_REGISTRATION = 0, 1, 2
+DTYPE_F32, DTYPE_BF16 = 0, 1
 U64_MAX = (1 << 64) - 1
 
 
@@ -122,7 +124,9 @@ SIGNATURES = [
     ("tidal_comm_create", C.c_int, [C.c_int, C.c_int, VP, C.c_int, C.POINTER(VP)]),
     ("tidal_comm_create_local", C.c_int, [C.c_int, C.c_int, C.c_char_p, C.c_int, C.POINTER(VP)]),
     ("tidal_comm_destroy", None, [VP]),
+    ("tidal_comm_selftest", C.c_int, [VP, C.c_uint64]),
     ("tidal_set_debug", C.c_int, [VP, C.c_int, C.c_int]),
+    ("tidal_set_allreduce_dtype", C.c_int, [VP, C.c_int]),
     ("tidal_template_checksum", C.c_int, [VP, C.POINTER(C.c_uint64)]),
     ("tidal_profile_read", C.c_int, [VP, C.POINTER(KernelTime), C.c_int, C.POINTER(C.c_int),
                                      C.c_int]),
@@ -346,6 +350,10 @@ class Template:
     def set_debug(self, flags: int, arg: int = -1) -> None:
         _check(lib().tidal_set_debug(self.h, flags, arg))
 
+    def set_allreduce_dtype(self, dtype: int) -> None:
+        """DTYPE_F32 (default) or DTYPE_BF16 for the row-parallel allreduces."""
+        _check(lib().tidal_set_allreduce_dtype(self.h, dtype))
+
     def profile(self, reset: bool = True) -> dict:
         n = C.c_int(0)
         arr = (KernelTime * 32)()
@@ -417,6 +425,10 @@ class Comm:
             idb = C.create_string_buffer(unique_id, 128)
             _check(lib().tidal_comm_create(world, rank, idb, device, C.byref(h)))
         self.h = h
+
+    def selftest(self, n: int = 4096) -> None:
+        """Run every collective on exact small-integer buffers (all ranks at once)."""
+        _check(lib().tidal_comm_selftest(self.h, n))
 
     @staticmethod
     def unique_id() -> bytes:

@@ -120,3 +120,22 @@ def test_decode_error_paths(T):
     tpl.invoke(prompt)
     toks, _, _ = tpl.decode(4, want_logits=False)
     assert toks.shape == (4,)
+
+
+def test_decode_refuses_another_adapter(T):
+    """decode must continue with the adapter of the preceding prefill,
+    even when another adapter has the same rank and targets (same arena layout)."""
+    cfg = synth.config("tiny")
+    model, tpl, ad = _setup(T, cfg, 16, 8, 1.0, 4)
+    slots, total = tpl.adapter_layout(8, 0x7F)
+    buf = T.PinnedBuffer(total)
+    synth.adapter_fill(cfg, 8, 9, slots, buf.view(), 0x7F)
+    other = T.Adapter(tpl, 8, 0.5, 0x7F, buf, total, "adapter:9")
+    prompt = synth.prompt(cfg, 16, 3)
+    tpl.invoke(prompt, ad)
+    with pytest.raises(T.TidalError):
+        tpl.decode(2, other)
+    with pytest.raises(T.TidalError):
+        tpl.decode(2)            # nor without the adapter
+    toks, _, _ = tpl.decode(2, ad, want_logits=False)
+    assert toks.shape == (2,)

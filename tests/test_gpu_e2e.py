@@ -120,7 +120,9 @@ def test_residency_and_policies_poisoned(T, budget, policy):
 def test_partial_targets_and_scale(T, tiny):
     cfg = tiny.cfg
     tok = synth.prompt(cfg, 33, 5)
-    for mask in (0x07, 0x08, 0x30, 0x40, 0x31):
+    # 0x10 / 0x20 / 0x50 / 0x21: gate or up alone (the paired gate/up tile gets
+    # a zero lora_B box for the untargeted half)
+    for mask in (0x07, 0x08, 0x30, 0x40, 0x31, 0x10, 0x20, 0x50, 0x21):
         a = tiny.adapter(8, 6, mask=mask, scale=2.0)
         ref = F.forward(cfg, tiny.w, tok, F.synth_adapter(cfg, 8, 6, mask), mask, 2.0)
         check(tiny.tpl.invoke(tok, a), ref)
@@ -253,3 +255,27 @@ def test_batch_prompts_match_oracle(T, cfg, B, Ls, rho, rank):
     t1, l1, _ = rig.tpl.invoke(toks[1], a)
     o1, lb, _ = rig.tpl.invoke_batch(toks[1:2], a)
     assert int(o1[0]) == t1 and np.array_equal(lb[0], l1)
+
+
+def test_graph_replay_equals_eager(T, tiny):
+    """The captured invocation (CUDA graph, event waits as edges) returns the
+    same bits as the eager enqueue, across replays, adapter hot-swaps with the
+    same buffer shape, scale changes (a new capture) and a template resize."""
+    cfg = tiny.cfg
+    tok = synth.prompt(cfg, 40, 77)
+    a1 = tiny.adapter(16, 21, scale=0.5)
+    outs = {}
+    for dbg in (T.DEBUG_NO_GRAPH, 0, 0, T.DEBUG_NO_GRAPH):
+        tiny.tpl.set_debug(dbg)
+        tk, lg, st = tiny.tpl.invoke(tok, a1)
+        outs.setdefault(dbg, []).append((tk, lg))
+    tiny.tpl.set_debug(0)
+    ref = outs[T.DEBUG_NO_GRAPH][0]
+    for tk, lg in outs[0] + outs[T.DEBUG_NO_GRAPH][1:]:
+        assert tk == ref[0] and np.array_equal(lg, ref[1])
+    check(tiny.tpl.invoke(tok, a1), F.forward(cfg, tiny.w, tok, F.synth_adapter(cfg, 16, 21),
+                                              0x7F, 0.5))
+    a2 = tiny.adapter(16, 22, scale=1.5)   # another buffer and scale: a new capture
+    check(tiny.tpl.invoke(tok, a2), F.forward(cfg, tiny.w, tok, F.synth_adapter(cfg, 16, 22),
+                                              0x7F, 1.5))
+    check(tiny.tpl.invoke(tok), F.forward(cfg, tiny.w, tok))

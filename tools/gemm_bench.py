@@ -35,8 +35,8 @@ def rnd(*shape, scale=1.0):
     return (torch.randn(*shape, device="cuda") * scale).to(torch.bfloat16)
 
 
-def bench(name, epi, bn, cg, mc, N_list, K, flops, ks=0):
-    code = epi | (bn << 8) | (cg << 20) | (mc << 22) | (ks << 24)
+def bench(name, epi, bn, cg, mc, N_list, K, flops, ks=0, tail=0):
+    code = epi | (bn << 8) | (cg << 20) | (mc << 22) | (ks << 24) | (tail << 28)
     A = rnd(M, K)
     srcs = N_list * 2 if epi == 2 else N_list  # EPI_SILU: gate and up
     Ws = [rnd(n, K, scale=1 / math.sqrt(K)) for n in srcs]
@@ -65,8 +65,8 @@ def bench(name, epi, bn, cg, mc, N_list, K, flops, ks=0):
         torch.cuda.synchronize()
         best = min(best, e0.elapsed_time(e1) / args.reps)
     os.environ["TIDAL_K_REPEAT"] = "1"
-    print(f"{name:8s} bn={bn:3d} cg={cg} mc={mc} ks={ks}  {best * 1e3:8.1f} us  {flops / best / 1e9:7.0f} TF/s",
-          flush=True)
+    print(f"{name:8s} bn={bn:3d} cg={cg} mc={mc} ks={ks} tail={tail}  {best * 1e3:8.1f} us  "
+          f"{flops / best / 1e9:7.0f} TF/s", flush=True)
 
 
 if args.mc_sweep:  # CTA-pair clusters sharing the A tile (TMA multicast), residual GEMMs
@@ -92,14 +92,20 @@ if args.resid_sweep:
     for _ in range(3):
         for name, N, K in (("o", d, d), ("down", d, F)):
             for bn in (192, 256):
-                for ks in (1, 2, 3, 4):
+                for ks, tail in ((1, 0), (2, 0), (3, 0), (4, 0), (2, 1), (4, 1), (6, 1), (8, 1)):
                     import io, contextlib
                     buf = io.StringIO()
                     with contextlib.redirect_stdout(buf):
-                        bench(name, 3, bn, 2, 1, [N], K, 2.0 * M * N * K, ks)
+                        bench(name, 3, bn, 2, 1, [N], K, 2.0 * M * N * K, ks, tail)
                     us = float(buf.getvalue().split("us")[0].split()[-1])
-                    res.setdefault((name, bn, ks), []).append(us)
-    for k, v in sorted(res.items()):
+                    res.setdefault((name, bn, ks, tail), []).append(us)
+            import io, contextlib
+            buf = io.StringIO()
+            with contextlib.redirect_stdout(buf):
+                bench(name, 3, 0, 0, 0, [N], K, 2.0 * M * N * K)   # the planner's choice
+            us = float(buf.getvalue().split("us")[0].split()[-1])
+            res.setdefault((name, "auto"), []).append(us)
+    for k, v in sorted(res.items(), key=str):
         print(k, "median us", round(statistics.median(v), 1), [round(x, 1) for x in v])
     sys.exit(0)
 
