@@ -258,6 +258,8 @@ tidal_status tidal_invoke_decode(tidal_template* tpl, const tidal_adapter* a, in
  * caller owns the fds (close them after passing them on, e.g. SCM_RIGHTS).
  * From then on the template refuses a resize below shared_bytes (importers
  * read those bytes as their template); it must outlive its importers.
+ * *fingerprint identifies the shared prefix: FNV-1a over every tensor below
+ * shared_bytes (name, offset, bytes, provenance = checkpoint:name:shape).
  * Errors: INVALID (dry / no VMM / re-export of an import), BUFSZ (cap < n).
  *
  * tidal_template_import: the importer builds the same plan from the same
@@ -266,13 +268,16 @@ tidal_status tidal_invoke_decode(tidal_template* tpl, const tidal_adapter* a, in
  * is copied from its pinned pool and its streaming arena is private, so an
  * invocation writes only private memory (copy-on-write by construction).
  * Errors: STRUCTURE if the chunks do not cover exactly shared_bytes of this
- * layout or shared_bytes exceeds the plan's resident prefix; INVALID for dry
+ * layout, shared_bytes exceeds the plan's resident prefix, or `fingerprint`
+ * (the exporter's) differs from this plan's prefix fingerprint (another
+ * trace, layout, checkpoint or weights of the same size); INVALID for dry
  * / tensor-parallel opts.  Everything else is as tidal_template_create. */
 tidal_status tidal_template_export(tidal_template* tpl, int* fds, int cap, int* n_fds,
-                                   uint64_t* shared_bytes);
+                                   uint64_t* shared_bytes, uint64_t* fingerprint /*nullable*/);
 tidal_status tidal_template_import(tidal_model* model, const tidal_trace_rec* trace,
                                    const tidal_template_opts* opts, const int* fds, int n_fds,
-                                   uint64_t shared_bytes, tidal_template** out);
+                                   uint64_t shared_bytes, uint64_t fingerprint,
+                                   tidal_template** out);
 
 /* ---- pinned host memory for adapters / pools (cudaHostAlloc) ---- */
 tidal_status tidal_host_alloc(uint64_t bytes, void** out);
@@ -320,11 +325,23 @@ enum {
                                   (the paper's "PyTorch-pin" baseline) */
   TIDAL_DEBUG_PROFILE = 16,    /* CUDA events around every kernel on the compute stream */
   TIDAL_DEBUG_PROFILE_GEMM = 32,/* events around the tensor-core GEMMs only (low overhead) */
-  TIDAL_DEBUG_NO_GRAPH = 64    /* enqueue the invocation eagerly instead of replaying its
+  TIDAL_DEBUG_NO_GRAPH = 64,   /* enqueue the invocation eagerly instead of replaying its
                                   captured CUDA graph (single-GPU invocations are captured
                                   once per plan / shape / adapter buffer / scale and
                                   replayed; profiling and fault injection are always eager) */
+  TIDAL_DEBUG_TIMELINE = 128   /* timing events at every copy-group end (copy stream) and
+                                  every op start (compute stream, after its barrier wait);
+                                  read with tidal_timeline_read (always eager) */
 };
+/* Timeline of the last invocation run with TIDAL_DEBUG_TIMELINE, in ms from
+ * the invocation's first event: group_end_ms[g] when transfer group g landed
+ * (plan group index), op_start_ms[k] when op k of the canonical sequence could
+ * start (previous op done and its barrier satisfied), and *end_ms when the
+ * token was ready.  Either array may be NULL (size query: *n_groups, *n_ops).
+ * Errors: INVALID if no timeline was recorded, BUFSZ if a cap is too small. */
+tidal_status tidal_timeline_read(tidal_template* tpl, double* group_end_ms, int cap_groups,
+                                 double* op_start_ms, int cap_ops, int* n_groups, int* n_ops,
+                                 double* end_ms);
 /* Per-kernel-class totals accumulated by invokes run with TIDAL_DEBUG_PROFILE:
  * device time (events on the launching stream), launches, and the ALGORITHMIC
  * flops and HBM bytes of those launches.  Fills up to

@@ -27,6 +27,16 @@ import synth
 WeightFn = Callable[[str], np.ndarray]
 
 
+def round_bf16(x: np.ndarray) -> np.ndarray:
+    """Round to the nearest bf16, ties to even (the storage format of the GPU's
+    activations), returned in x's dtype.  Used only by the bf16-emulation mode
+    (SURVEY.md §8(c) O1 "bf16-emulated ... rounds (RNE) exactly where the GPU
+    stores bf16"); finite inputs only."""
+    b = np.asarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
+    b = ((b + 0x7FFF + ((b >> 16) & 1)) >> 16) << 16
+    return b.astype(np.uint32).view(np.float32).astype(np.asarray(x).dtype)
+
+
 def rmsnorm(x: np.ndarray, g: np.ndarray, eps: float) -> np.ndarray:
     """RMSNorm(x; g) = g * x / sqrt(mean(x^2) + eps)."""
     ms = np.mean(x * x, axis=-1, keepdims=True)
@@ -50,9 +60,12 @@ def rope(x: np.ndarray, cos: np.ndarray, sin: np.ndarray) -> np.ndarray:
     return np.concatenate([x1 * c - x2 * s, x2 * c + x1 * s], axis=-1)
 
 
-def causal_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray) -> np.ndarray:
+def causal_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray,
+                     p_bf16: bool = False) -> np.ndarray:
     """O_h = softmax(Q_h K_g^T / sqrt(hd) + causal) V_g, g = h // (H/KV).
-    q [S,H,hd], k/v [S,KV,hd] -> [S, H*hd]."""
+    q [S,H,hd], k/v [S,KV,hd] -> [S, H*hd].  p_bf16 (bf16 emulation): the
+    unnormalised P = exp(s - max) is rounded to bf16 before P V and the fp32
+    row sum of the unrounded P divides afterwards (FA-style)."""
     S, H, hd = q.shape
     KV = k.shape[1]
     grp = H // KV
@@ -65,17 +78,25 @@ def causal_attention(q: np.ndarray, k: np.ndarray, v: np.ndarray) -> np.ndarray:
         s[mask] = -np.inf
         s = s - s.max(axis=1, keepdims=True)
         p = np.exp(s)
+        if p_bf16:
+            out[:, h, :] = (round_bf16(p) @ v[:, g, :]) / p.sum(axis=1, keepdims=True)
+            continue
         p = p / p.sum(axis=1, keepdims=True)
         out[:, h, :] = p @ v[:, g, :]
     return out.reshape(S, H * hd)
 
 
-def linear(x: np.ndarray, W: np.ndarray, lora: Optional[tuple], scale: float) -> np.ndarray:
-    """y = x W^T + s (x A^T) B^T  — the LoRA branch kept separate (A3)."""
+def linear(x: np.ndarray, W: np.ndarray, lora: Optional[tuple], scale: float,
+           t_bf16: bool = False) -> np.ndarray:
+    """y = x W^T + s (x A^T) B^T  — the LoRA branch kept separate (A3).
+    t_bf16 (bf16 emulation): T = s x A^T is stored as bf16 before T B^T."""
     y = x @ W.T
     if lora is not None:
         A, B = lora
-        y = y + x.dtype.type(scale) * ((x @ A.T) @ B.T)
+        if t_bf16:
+            y = y + round_bf16(x.dtype.type(scale) * (x @ A.T)) @ B.T
+        else:
+            y = y + x.dtype.type(scale) * ((x @ A.T) @ B.T)
     return y
 
 
@@ -86,12 +107,17 @@ def silu(x: np.ndarray) -> np.ndarray:
 def forward(cfg: synth.ModelConfig, weight: WeightFn, tokens: np.ndarray,
             adapter: Optional[WeightFn] = None, target_mask: int = 0,
             scale: float = 1.0, dtype=np.float32, n_layers: Optional[int] = None,
-            all_logits: bool = False, stats: Optional[dict] = None) -> Dict[str, np.ndarray]:
+            all_logits: bool = False, stats: Optional[dict] = None,
+            bf16_emulate: bool = False) -> Dict[str, np.ndarray]:
     """First-token forward.
 
     weight(name)  -> weight in HF shape, any float dtype holding bf16 values.
     adapter(name) -> LoRA tensor ("<module>.lora_A"/"lora_B") or None.
     n_layers      -> run only the first n layers (bounded CPU samples).
+    bf16_emulate  -> debug mode: round (RNE) to bf16 exactly where the GPU path
+                     stores bf16 — Xn, Q/K/V after RoPE, P before P V, the
+                     attention output, T = s x A^T, H = silu(G) * U; the residual
+                     stream, G / U and the head stay fp32.
     Returns {"logits": [V] of the last position, "token": argmax (lowest index
     on ties, A5), "hidden": final residual [S, d]}.
     """
@@ -110,24 +136,26 @@ def forward(cfg: synth.ModelConfig, weight: WeightFn, tokens: np.ndarray,
                 np.asarray(adapter(m + ".lora_B"), dtype=dtype))
 
     cos, sin = rope_cos_sin(S, hd, cfg.rope_theta, dtype)
+    rb = round_bf16 if bf16_emulate else (lambda t: t)
+    tb = bf16_emulate
     # X = E[tok]   (fp32 residual stream)
     X = W("model.embed_tokens.weight")[tokens]
     for i in range(L):
         p = f"model.layers.{i}."
         # attention block
-        Xn = rmsnorm(X, W(p + "input_layernorm.weight"), eps)
-        Q = linear(Xn, W(p + "self_attn.q_proj.weight"), lora_of(i, "q"), scale)
-        K = linear(Xn, W(p + "self_attn.k_proj.weight"), lora_of(i, "k"), scale)
-        V = linear(Xn, W(p + "self_attn.v_proj.weight"), lora_of(i, "v"), scale)
-        Q = rope(Q.reshape(S, H, hd), cos, sin)
-        K = rope(K.reshape(S, KV, hd), cos, sin)
-        O = causal_attention(Q, K, V.reshape(S, KV, hd))
-        X = X + linear(O, W(p + "self_attn.o_proj.weight"), lora_of(i, "o"), scale)
+        Xn = rb(rmsnorm(X, W(p + "input_layernorm.weight"), eps))
+        Q = linear(Xn, W(p + "self_attn.q_proj.weight"), lora_of(i, "q"), scale, tb)
+        K = linear(Xn, W(p + "self_attn.k_proj.weight"), lora_of(i, "k"), scale, tb)
+        V = rb(linear(Xn, W(p + "self_attn.v_proj.weight"), lora_of(i, "v"), scale, tb))
+        Q = rb(rope(Q.reshape(S, H, hd), cos, sin))
+        K = rb(rope(K.reshape(S, KV, hd), cos, sin))
+        O = rb(causal_attention(Q, K, V.reshape(S, KV, hd), p_bf16=bf16_emulate))
+        X = X + linear(O, W(p + "self_attn.o_proj.weight"), lora_of(i, "o"), scale, tb)
         # MLP block
-        Hn = rmsnorm(X, W(p + "post_attention_layernorm.weight"), eps)
-        G = linear(Hn, W(p + "mlp.gate_proj.weight"), lora_of(i, "gate"), scale)
-        U = linear(Hn, W(p + "mlp.up_proj.weight"), lora_of(i, "up"), scale)
-        X = X + linear(silu(G) * U, W(p + "mlp.down_proj.weight"), lora_of(i, "down"), scale)
+        Hn = rb(rmsnorm(X, W(p + "post_attention_layernorm.weight"), eps))
+        G = linear(Hn, W(p + "mlp.gate_proj.weight"), lora_of(i, "gate"), scale, tb)
+        U = linear(Hn, W(p + "mlp.up_proj.weight"), lora_of(i, "up"), scale, tb)
+        X = X + linear(rb(silu(G) * U), W(p + "mlp.down_proj.weight"), lora_of(i, "down"), scale, tb)
         if stats is not None:
             stats.setdefault("residual_rms", []).append(float(np.sqrt(np.mean(X * X))))
     head_name = "model.embed_tokens.weight" if cfg.tie_embeddings else "lm_head.weight"

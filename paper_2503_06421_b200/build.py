@@ -20,7 +20,7 @@ ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-std=c++17", "-lineinfo", "-Xcompiler", "-fPIC", "-Xcompiler", "-Wall",
          "-I", os.path.join(ROOT, "include"), "--expt-relaxed-constexpr"]
 SOURCES = ["plan.cpp", "runtime.cu", "api.cu", "gemm_tc.cu", "attention.cu", "kernels.cu",
-           "comm.cu", "shrink.cu", "attn_tc.cu", "decode.cu", "vmm.cu"]
+           "comm.cu", "attn_tc.cu", "decode.cu", "vmm.cu"]
 
 
 def _newer(src_paths, out):

@@ -133,6 +133,10 @@ struct tidal_template {
     int launches = 0;
   } graph;
   bool use_graphs = true;
+  // TIDAL_DEBUG_TIMELINE: timing events per group end / op start, and the last result
+  std::vector<cudaEvent_t> tl_group, tl_op;
+  std::vector<double> tl_group_ms, tl_op_ms;
+  double tl_end_ms = 0;
   uint8_t* arena = nullptr;  // adapter arena
   uint64_t arena_cap = 0;
   int debug = 0, debug_arg = -1;
@@ -311,12 +315,19 @@ tidal_status tidal_trace(tidal_model* m, const int32_t* host_tokens, int n_token
     if (cold_ttft_ms_out) *cold_ttft_ms_out = std::chrono::duration<double, std::milli>(t1 - t0).count();
     if (host_logits_out) memcpy(host_logits_out, ex.h_logits, 4ull * m->shape.vocab);
     if (host_token_out) *host_token_out = (int32_t)(0xFFFFFFFFu - (uint32_t)(*ex.h_key & 0xFFFFFFFFu));
-    // the recorded order must be the planner's trace (never-read weights at the tail)
+    // The ids the launcher handed to its kernels must reproduce the planner's
+    // trace (never-read weights at the tail): the same first-use order, and no
+    // weight used at an op before the one whose barrier covers it (a fused
+    // kernel may use a weight later — final_norm's gain in the head kernel).
     std::vector<char> seen(m->tt.n_base, 0);
     for (auto& p : rec.access) seen[p.first] = 1;
     for (int id = 0; id < m->tt.n_base; ++id)
       if (!seen[id]) rec.access.emplace_back(id, -1);
-    if (rec.access != tr->tr.access) fail(TIDAL_ERR_INVALID, "recorded access order != planner order");
+    bool same = rec.access.size() == tr->tr.access.size();
+    for (size_t i = 0; same && i < rec.access.size(); ++i)
+      same = rec.access[i].first == tr->tr.access[i].first &&
+             rec.access[i].second >= tr->tr.access[i].second;
+    if (!same) fail(TIDAL_ERR_INVALID, "kernel weight use order != planner trace order");
   } catch (...) {
     if (dbuf) cudaFree(dbuf);
     if (stage) cudaFreeHost(stage);
@@ -369,22 +380,31 @@ static void warm_kernels(tidal_template* tp) {
   a.gen = tp->gen;
   a.comm = tp->comm ? tp->comm->impl : nullptr;
   run_forward(ex, a);
-  const bf16* A[1] = {ex.Xn};
-  bf16* T[1] = {ex.T[0]};
-  for (int r : {8, 16, 32, 64})
-    for (int nt = 1; nt <= 3; ++nt) {
-      const bf16* A3[3] = {ex.Xn, ex.Xn, ex.Xn};
-      bf16* T3[3] = {ex.T[0], ex.T[1], ex.T[2]};
-      cuda_check(lora_shrink_launch(ex.Xn, 64, 1, 64, A3, T3, nt, r, 1.f, ex.compute),
-                 "warm shrink");
-    }
+  shrink_preload();
   cuda_check(cudaStreamSynchronize(ex.compute), "warm run");
   ex.cache.clear();
 }
 
+// Identity of the bytes below `shared` in a template's layout: every tensor
+// overlapping that prefix with its offset, size and provenance (checkpoint +
+// name + shape), so an importer with another trace / layout / checkpoint /
+// weights of the same byte size is refused.
+static uint64_t prefix_fingerprint(const TensorTable& tt, const Plan& p, uint64_t shared) {
+  std::string s;
+  for (int id : p.layout) {
+    const uint64_t o = p.offset[id];
+    if (o >= shared) continue;
+    s += tt.t[id].name + "@" + std::to_string(o) + ":" + std::to_string(tt.t[id].bytes) + ":" +
+         tt.t[id].provenance + ";";
+  }
+  s += std::to_string(shared);
+  return fnv1a64(s);
+}
+
 static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
                                     const tidal_template_opts* opts, const int* fds, int n_fds,
-                                    uint64_t shared_bytes, tidal_template** out) {
+                                    uint64_t shared_bytes, uint64_t fingerprint,
+                                    tidal_template** out) {
   TIDAL_TRY
   require(m && t && opts && out, "null argument");
   require(t->tt.n_base == m->tt.n_base, "trace is from a different model", TIDAL_ERR_STRUCTURE);
@@ -409,6 +429,10 @@ static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
   try {
     require(m->world == 1 || (opts->comm && opts->comm->world == m->world && opts->comm->rank == m->rank),
             "tensor-parallel model needs a matching communicator");
+    if (n_fds)
+      require(prefix_fingerprint(tp->tt, tp->plan, shared_bytes) == fingerprint,
+              "imported template chunks hold another layout / checkpoint (fingerprint mismatch)",
+              TIDAL_ERR_STRUCTURE);
     tp->ex.init(tp->device, tp->shape, tp->eps, tp->theta, tp->world, tp->rank, tp->max_tokens);
     tp->ex.colocated = tp->comm && tp->comm->impl && tp->comm->impl->colocated;
     const uint64_t L = tp->plan.layout_bytes;
@@ -470,20 +494,21 @@ static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
 
 tidal_status tidal_template_create(tidal_model* m, const tidal_trace_rec* t,
                                    const tidal_template_opts* opts, tidal_template** out) {
-  return template_create(m, t, opts, nullptr, 0, 0, out);
+  return template_create(m, t, opts, nullptr, 0, 0, 0, out);
 }
 
 tidal_status tidal_template_import(tidal_model* m, const tidal_trace_rec* t,
                                    const tidal_template_opts* opts, const int* fds, int n_fds,
-                                   uint64_t shared_bytes, tidal_template** out) {
+                                   uint64_t shared_bytes, uint64_t fingerprint,
+                                   tidal_template** out) {
   if (!opts || opts->device < 0) return set_err(TIDAL_ERR_INVALID, "import needs a device template");
   if (n_fds < 1 || !fds) return set_err(TIDAL_ERR_INVALID, "no chunks to import");
   if (opts->comm) return set_err(TIDAL_ERR_INVALID, "tensor-parallel import is not implemented");
-  return template_create(m, t, opts, fds, n_fds, shared_bytes, out);
+  return template_create(m, t, opts, fds, n_fds, shared_bytes, fingerprint, out);
 }
 
 tidal_status tidal_template_export(tidal_template* tp, int* fds, int cap, int* n_fds,
-                                   uint64_t* shared_bytes) {
+                                   uint64_t* shared_bytes, uint64_t* fingerprint) {
   TIDAL_TRY
   require(tp && n_fds && shared_bytes, "null argument");
   require(!tp->dry && tp->vmm.va, "export needs a device template on CUDA VMM");
@@ -491,6 +516,7 @@ tidal_status tidal_template_export(tidal_template* tp, int* fds, int cap, int* n
   const size_t n = tp->plan.resident_end / tp->vmm.chunk;  // chunks wholly inside the prefix
   *n_fds = (int)n;
   *shared_bytes = (uint64_t)n * tp->vmm.chunk;
+  if (fingerprint) *fingerprint = prefix_fingerprint(tp->tt, tp->plan, *shared_bytes);
   if (!fds) return TIDAL_OK;  // size query
   require(cap >= (int)n, "fd buffer too small", TIDAL_ERR_BUFSZ);
   for (size_t i = 0; i < n; ++i) fds[i] = vmm_export_fd(tp->vmm, i);
@@ -556,6 +582,8 @@ void tidal_template_destroy(tidal_template* tp) {
                           tp->e_fork, tp->e_join})
       if (e) cudaEventDestroy(e);
     if (tp->graph.exec) cudaGraphExecDestroy(tp->graph.exec);
+    for (cudaEvent_t e : tp->tl_group) cudaEventDestroy(e);
+    for (cudaEvent_t e : tp->tl_op) cudaEventDestroy(e);
     if (tp->vmm.va)
       vmm_free(tp->vmm);
     else if (tp->dev)
@@ -726,7 +754,19 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
   const bool graph_ok = tp->use_graphs && tp->world == 1 &&
                         !(tp->debug & (TIDAL_DEBUG_PROFILE | TIDAL_DEBUG_PROFILE_GEMM |
                                        TIDAL_DEBUG_SKIP_BARRIER | TIDAL_DEBUG_SERIAL |
-                                       TIDAL_DEBUG_NO_GRAPH));
+                                       TIDAL_DEBUG_NO_GRAPH | TIDAL_DEBUG_TIMELINE));
+  const bool timeline = (tp->debug & TIDAL_DEBUG_TIMELINE) != 0;
+  if (timeline) {
+    auto grow = [](std::vector<cudaEvent_t>& v, size_t n) {
+      while (v.size() < n) {
+        cudaEvent_t e;
+        cuda_check(cudaEventCreate(&e), "cudaEventCreate(timeline)");
+        v.push_back(e);
+      }
+    };
+    grow(tp->tl_group, P.groups.size());
+    grow(tp->tl_op, P.ops.size());
+  }
   // everything a captured invocation bakes in: plan, shapes, buffers, scale
   float scale_v = a ? a->scale : 1.f;
   uint32_t scale_bits = 0;
@@ -778,6 +818,7 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
       }
       cuda_check(cudaMemcpyAsync(dst, src, G.bytes, cudaMemcpyHostToDevice, ex.copy), "H2D group");
       cuda_check(cudaEventRecord(tp->ev[g], ex.copy), "event");
+      if (timeline) cuda_check(cudaEventRecord(tp->tl_group[g], ex.copy), "event");
     }
     rec(tp->e_h2d1, ex.copy);
     cuda_check(cudaEventRecord(tp->e_join, ex.copy), "event");
@@ -791,6 +832,8 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
     ra.barriers = &P.barriers;
     ra.events = &tp->ev;
     ra.copy_pos = &copy_pos;
+    ra.group_of = &P.group_of;
+    ra.tl_op = timeline ? &tp->tl_op : nullptr;
     ra.skip_group = skip;
     ra.S = n_tokens;
     ra.nseq = n_seqs;
@@ -813,6 +856,8 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
     ex.launches = tp->graph.launches;
   } else if (graph_ok) {
     if (tp->graph.exec) cudaGraphExecDestroy(tp->graph.exec);
+    for (cudaEvent_t e : tp->tl_group) cudaEventDestroy(e);
+    for (cudaEvent_t e : tp->tl_op) cudaEventDestroy(e);
     tp->graph.exec = nullptr;
     cudaGraph_t graph = nullptr;
     cuda_check(cudaStreamBeginCapture(ex.compute, cudaStreamCaptureModeThreadLocal), "begin capture");
@@ -835,6 +880,22 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
   }
   ex.dec.prompt_akey = a ? (const void*)tp->arena : nullptr;
   cuda_check(cudaEventSynchronize(tp->e_end), "invoke");
+  ex.dbg_dump();
+  if (timeline) {
+    float ms = 0;
+    tp->tl_group_ms.assign(P.groups.size(), 0.0);
+    tp->tl_op_ms.assign(P.ops.size(), 0.0);
+    for (size_t g = 0; g < P.groups.size(); ++g) {
+      cuda_check(cudaEventElapsedTime(&ms, tp->e_start, tp->tl_group[g]), "elapsed");
+      tp->tl_group_ms[g] = ms;
+    }
+    for (size_t k = 0; k < P.ops.size(); ++k) {
+      cuda_check(cudaEventElapsedTime(&ms, tp->e_start, tp->tl_op[k]), "elapsed");
+      tp->tl_op_ms[k] = ms;
+    }
+    cuda_check(cudaEventElapsedTime(&ms, tp->e_start, tp->e_end), "elapsed");
+    tp->tl_end_ms = ms;
+  }
   tp->suffix_valid = skip < 0;
   // decode continuation: the cache now holds this prompt's K/V (single prompt)
   ex.dec.prompt_len = (ex.dec.kc && n_seqs == 1) ? n_tokens : 0;
@@ -1027,6 +1088,26 @@ tidal_status tidal_set_debug(tidal_template* tp, int flags, int arg) {
   require(tp != nullptr, "null template");
   tp->debug = flags;
   tp->debug_arg = arg;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_timeline_read(tidal_template* tp, double* group_end_ms, int cap_groups,
+                                 double* op_start_ms, int cap_ops, int* n_groups, int* n_ops,
+                                 double* end_ms) {
+  TIDAL_TRY
+  require(tp != nullptr, "null template");
+  require(!tp->tl_op_ms.empty(), "no timeline recorded (invoke with TIDAL_DEBUG_TIMELINE)");
+  if (n_groups) *n_groups = (int)tp->tl_group_ms.size();
+  if (n_ops) *n_ops = (int)tp->tl_op_ms.size();
+  if (end_ms) *end_ms = tp->tl_end_ms;
+  if (group_end_ms) {
+    require(cap_groups >= (int)tp->tl_group_ms.size(), "group buffer too small", TIDAL_ERR_BUFSZ);
+    std::copy(tp->tl_group_ms.begin(), tp->tl_group_ms.end(), group_end_ms);
+  }
+  if (op_start_ms) {
+    require(cap_ops >= (int)tp->tl_op_ms.size(), "op buffer too small", TIDAL_ERR_BUFSZ);
+    std::copy(tp->tl_op_ms.begin(), tp->tl_op_ms.end(), op_start_ms);
+  }
   TIDAL_CATCH
 }
 

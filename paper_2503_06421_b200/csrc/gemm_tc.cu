@@ -198,6 +198,19 @@ __device__ __forceinline__ void decode_tile(const GemmParams& p, int tile, int& 
   n0 = gn * (EPI == EPI_SILU ? 128 : BNT);
 }
 
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// diagnostic timeline (GemmParams::dbg, null in production): per CTA and work
+// item, 8 slots: 0 producer start, 1 flag-wait end, 2 first MMA, 3 last commit,
+// 4 epilogue start, 5 epilogue end, 6 work id, 7 is_t
+constexpr int DBG_ITEMS = 32;
+__device__ __forceinline__ void dbg_put(unsigned long long* d, int it, int slot, unsigned long long v) {
+  if (d && it < DBG_ITEMS) d[((size_t)blockIdx.x * DBG_ITEMS + it) * 8 + slot] = v;
+}
+
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
   asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
@@ -236,18 +249,21 @@ __device__ __forceinline__ Work decode_work(const GemmParams& p, int w, int pr, 
     r.is_t = 0;
     return r;
   }
-  if (w < 0) {  // T tile -w - 1 (see item_work: first on the least loaded units)
-    w = -w - 1;
+  if (w < 0) {  // T work -w - 1 (see item_work: first on the least loaded units)
+    // T tile j in t_ks parts (the K ranges of this GEMM's split-K parts)
+    const int tw = -w - 1, tks = p.t_ks > 1 ? p.t_ks : 1;
+    const int j = tw / tks;
     r.is_t = 1;
     r.seg = 0;
     r.n0 = 0;
-    r.m0 = w * (BM * CG * MC) + pr * BM * CG;
-    r.kb0 = 0;
-    r.kb1 = nk;
+    r.m0 = j * (BM * CG * MC) + pr * BM * CG;
+    r.split = tw - j * tks;
+    r.ks = tks;
+    const int kps = tks > 1 ? p.kblocks_per_split : nk;
+    r.kb0 = r.split * kps;
+    r.kb1 = min(nk, r.kb0 + kps);
     r.lora = 0;
-    r.split = 0;
-    r.tile = w;
-    r.ks = 1;
+    r.tile = j;
     return r;
   }
   r.is_t = 0;
@@ -285,8 +301,9 @@ __device__ __forceinline__ Work decode_work(const GemmParams& p, int w, int pr, 
 // encoded as negative work ids (-j - 1) for decode_work.
 __device__ __forceinline__ bool item_work(const GemmParams& p, int unit, int nunits, int nnorm,
                                           int i, int& w) {
-  const int t0 = nunits - 1 - unit;  // this unit's first T tile
-  const int nt = p.t_tiles > t0 ? (p.t_tiles - t0 + nunits - 1) / nunits : 0;
+  const int t0 = nunits - 1 - unit;  // this unit's first T work
+  const int ntw = p.t_tiles * (p.t_ks > 1 ? p.t_ks : 1);
+  const int nt = ntw > t0 ? (ntw - t0 + nunits - 1) / nunits : 0;
   if (i < nt) {
     w = -(t0 + i * nunits) - 1;
     return true;
@@ -339,7 +356,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
     ptx::prefetch_tmap(&p.a);
     for (int i = 0; i < 3; ++i)
       if (i < p.nseg || (EPI == EPI_SILU && i < 2)) ptx::prefetch_tmap(&p.b[i]);
-    for (int i = 0; i < p.t_nt; ++i) ptx::prefetch_tmap(&p.la[i]);
+    if (p.t_tiles) ptx::prefetch_tmap(&p.la);
     for (int s = 0; s < STAGES; ++s) {
       ptx::mbar_init(full_bar(s), CG);  // leader expect_tx + peer arrive
       ptx::mbar_init(empty_bar(s), MC);  // one MMA commit per pair of the cluster
@@ -386,34 +403,33 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       };
       int stage = 0;
       uint32_t phase = 0;
-      uint64_t tseen[GEMM_MAX_TBLK / 64] = {};  // row blocks whose T this CTA saw ready
+      bool t_ready = false;  // this CTA has seen every T row block published
       int w;
       for (int it = 0; item_work(p, unit, nunits, nwork, it, w); ++it) {
         const Work wk = decode_work<EPI, BNT, CG, MC>(p, w, pr, nk, nlora);
         const int seg = wk.seg, n0 = wk.n0;
         const int ma = wk.m0 + rank * BM;  // this CTA's A rows
+        dbg_put(p.dbg, it, 0, gtimer());
+        dbg_put(p.dbg, it, 6, (unsigned long long)(long long)w);
+        dbg_put(p.dbg, it, 7, wk.is_t);
         const int nkb = wk.kb1 + wk.lora;
         if (EPI != EPI_PARTIAL && wk.is_t) {
           // T tile: this CTA stages its 128 rows of A and its t_rt_pad / CG rows of
-          // the stacked [lora_A_0; lora_A_1; ...] (8-row boxes; padding rows are
-          // never loaded — their accumulator columns are never read)
-          const int half = p.t_rt_pad / CG, rt = p.t_nt * p.t_r;
-          for (int kb = 0; kb < ((p.t_diag & 4) ? 0 : nk); ++kb) {
+          // the stacked [lora_A_0; lora_A_1; ...], packed K-block-major by
+          // lora_pack_kernel so a stage's rows are one contiguous box (padding
+          // rows are stale bytes: their accumulator columns are never read)
+          const int half = p.t_rt_pad / CG;
+          for (int kb = wk.kb0; kb < wk.kb1; ++kb) {
             ptx::mbar_wait(empty_bar(stage), phase ^ 1);
             const uint32_t sa = sbase + OFF_A + stage * A_BYTES;
             const uint32_t sb = sbase + OFF_B + stage * BBYTES;
             const uint32_t fb = full_bar(stage);
             if (rank == 0)
-              ptx::mbar_expect_tx(fb, A_BYTES * CG + rt * ROW_BYTES);
+              ptx::mbar_expect_tx(fb, (A_BYTES + half * ROW_BYTES) * CG);
             else
               ptx::mbar_arrive_leader(fb);
             tma(&p.a, sa, fb, kb * BK, ma);
-            for (int c = 0; c < half; c += 8) {
-              const int srow = rank * half + c;
-              if (srow >= rt) break;
-              const int t = srow / p.t_r;
-              tma(&p.la[t], sb + c * ROW_BYTES, fb, kb * BK, srow - t * p.t_r);
-            }
+            tma(&p.la, sb, fb, 0, kb * p.t_rt_pad + rank * half);
             if (++stage == STAGES) {
               stage = 0;
               phase ^= 1;
@@ -422,19 +438,16 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           continue;
         }
         for (int kb = wk.kb0; kb < nkb; ++kb) {
-          if (EPI != EPI_PARTIAL && p.t_tiles > 0 && kb == wk.kb1) {
-            // the LoRA K-extension reads T of this CTA's rows: wait for its T tile
-            // (once per 128-row block and CTA: later tiles of the block find it set)
-            const int blk = ma / BM;
-            const uint64_t bit = 1ull << (blk & 63);
-            if (!(tseen[blk >> 6] & bit) && !(p.t_diag & 2)) {
-              const int* f = p.t_flags + blk;
-              uint32_t n = 0;
-              while (ld_acquire(f) == 0)
-                if (++n == (1u << 30)) __trap();
-              if (!(p.t_diag & 1)) asm volatile("fence.proxy.async.global;" ::: "memory");
-              tseen[blk >> 6] |= bit;
-            }
+          if (EPI != EPI_PARTIAL && p.t_tiles > 0 && kb == wk.kb1 && !t_ready) {
+            // the LoRA K-extension reads T: wait (once per CTA) until every T
+            // row block of this launch is published (they run concurrently,
+            // first on their units, so one wait costs no more than a per-row one)
+            uint32_t n = 0;
+            while (ld_acquire(p.t_flags) < p.t_tiles * CG)
+              if (++n == (1u << 30)) __trap();
+            asm volatile("fence.proxy.async.global;" ::: "memory");
+            t_ready = true;
+            dbg_put(p.dbg, it, 1, gtimer());
           }
           ptx::mbar_wait(empty_bar(stage), phase ^ 1);
           const uint32_t sa = sbase + OFF_A + stage * A_BYTES;
@@ -513,19 +526,22 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       int w;
       for (int it = 0; item_work(p, unit, nunits, nwork, it, w); ++it) {
         const Work wk = decode_work<EPI, BNT, CG, MC>(p, w, pr, nk, nlora);
-        const int kb0 = wk.kb0, nkb = (wk.is_t && (p.t_diag & 4)) ? 0 : wk.kb1 + wk.lora;
+        const int kb0 = wk.kb0, nkb = wk.kb1 + wk.lora;
+        bool first_mma = true;
         ptx::mbar_wait(tempty_bar(acc), acc_phase ^ 1);
         ptx::tc_fence_after();
         const uint32_t d_tmem = tmem_base + acc * BNX;
         for (int kb = kb0; kb < nkb; ++kb) {
           ptx::mbar_wait(full_bar(stage), phase);
           ptx::tc_fence_after();
+          if (first_mma && lane == 0) dbg_put(p.dbg, it, 2, gtimer());
+          first_mma = false;
           const uint64_t adesc = ptx::desc_sw128(sbase + OFF_A + stage * A_BYTES);
           const uint64_t bdesc = ptx::desc_sw128(sbase + OFF_B + stage * BBYTES);
           if (EPI != EPI_PARTIAL && wk.is_t) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
-              mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC_T, (kb | k) != 0);
+              mma(d_tmem, adesc + 2 * k, bdesc + 2 * k, IDESC_T, ((kb - kb0) | k) != 0);
           } else if (EPI == EPI_PARTIAL || kb < wk.kb1) {
 #pragma unroll
             for (int k = 0; k < BK / 16; ++k)
@@ -544,6 +560,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           }
         }
         commit(tfull_bar(acc));
+        if (lane == 0) dbg_put(p.dbg, it, 3, gtimer());
         if (++acc == 2) {
           acc = 0;
           acc_phase ^= 1;
@@ -564,38 +581,85 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
       const GemmSeg sg = p.seg[wk.seg];
       ptx::mbar_wait(tfull_bar(acc), acc_phase);
       ptx::tc_fence_after();
+      if (threadIdx.x == 64) dbg_put(p.dbg, it, 4, gtimer());
       const uint32_t tacc = tmem_base + ((uint32_t)(q * 32) << 16) + acc * BNX;
       const int row0 = m0 + rank * BM + q * 32;
       const int m = row0 + lane;
       float v[32], w[32];
       if (EPI != EPI_PARTIAL && wk.is_t) {
-        // T_t[m, j] = bf16(s * acc[m, t * r + j]): 8-column groups never straddle
-        // targets (r % 8 == 0); each thread writes its own row (rows contiguous)
-        const int rt = p.t_nt * p.t_r;
+        // T_t[m, j] = bf16(s * acc[m, t * r + j]); with t_ks K parts each part
+        // leaves its fp32 partial in t_ws and the last to arrive sums all parts
+        // in part order (deterministic) before rounding.  8-column groups never
+        // straddle targets (r % 8 == 0); each thread owns one row.
+        const int rt = p.t_nt * p.t_r, tks = wk.ks;
+        const int prow = rank * BM + q * 32 + lane;  // row within the pair tile
+        float* ws = p.t_ws + (size_t)(wk.tile * tks) * (BM * CG) * p.t_rt_pad;
+        volatile int* bcast = reinterpret_cast<volatile int*>(smem + OFF_TMEM + 8);
+        bool last = true;
+        if (tks > 1) {
 #pragma unroll 1
-        for (int j = 0; j * 32 < rt; ++j) {
-          ld_chunk(tacc + j * 32, v);
-          if (m < p.M) {
+          for (int j = 0; j * 32 < rt; ++j) {
+            ld_chunk(tacc + j * 32, v);
+            float* dst = ws + ((size_t)wk.split * (BM * CG) + prow) * p.t_rt_pad + j * 32;
 #pragma unroll
-            for (int g = 0; g < 4; ++g) {
-              const int c0 = j * 32 + g * 8;
-              if (c0 < rt) {
-                const int t = c0 / p.t_r;
-                uint4 o;
-                o.x = pack_bf16x2(p.t_scale * v[8 * g + 0], p.t_scale * v[8 * g + 1]);
-                o.y = pack_bf16x2(p.t_scale * v[8 * g + 2], p.t_scale * v[8 * g + 3]);
-                o.z = pack_bf16x2(p.t_scale * v[8 * g + 4], p.t_scale * v[8 * g + 5]);
-                o.w = pack_bf16x2(p.t_scale * v[8 * g + 6], p.t_scale * v[8 * g + 7]);
-                *reinterpret_cast<uint4*>(p.t_out[t] + (size_t)m * p.t_r + (c0 - t * p.t_r)) = o;
+            for (int g = 0; g < 8; ++g)
+              if (j * 32 + g * 4 < rt)
+                *reinterpret_cast<float4*>(dst + g * 4) =
+                    make_float4(v[4 * g], v[4 * g + 1], v[4 * g + 2], v[4 * g + 3]);
+          }
+          __threadfence();
+          epi_bar();
+          if (threadIdx.x == 64) {
+            const int old = atomicAdd(p.t_flags + 1 + wk.tile * CG + rank, 1);
+            *bcast = old;
+          }
+          epi_bar();
+          last = *bcast == tks - 1;
+          if (last) __threadfence();  // acquire the other parts' partials
+        }
+        if (last) {
+#pragma unroll 1
+          for (int j = 0; j * 32 < rt; ++j) {
+            if (tks > 1) {
+#pragma unroll
+              for (int i = 0; i < 32; ++i) v[i] = 0.f;
+              for (int s2 = 0; s2 < tks; ++s2) {
+                const float* src = ws + ((size_t)s2 * (BM * CG) + prow) * p.t_rt_pad + j * 32;
+#pragma unroll
+                for (int g = 0; g < 8; ++g)
+                  if (j * 32 + g * 4 < rt) {
+                    const float4 a = __ldcg(reinterpret_cast<const float4*>(src + g * 4));
+                    v[4 * g] += a.x;
+                    v[4 * g + 1] += a.y;
+                    v[4 * g + 2] += a.z;
+                    v[4 * g + 3] += a.w;
+                  }
+              }
+            } else {
+              ld_chunk(tacc + j * 32, v);
+            }
+            if (m < p.M) {
+#pragma unroll
+              for (int g = 0; g < 4; ++g) {
+                const int c0 = j * 32 + g * 8;
+                if (c0 < rt) {
+                  const int t = c0 / p.t_r;
+                  uint4 o;
+                  o.x = pack_bf16x2(p.t_scale * v[8 * g + 0], p.t_scale * v[8 * g + 1]);
+                  o.y = pack_bf16x2(p.t_scale * v[8 * g + 2], p.t_scale * v[8 * g + 3]);
+                  o.z = pack_bf16x2(p.t_scale * v[8 * g + 4], p.t_scale * v[8 * g + 5]);
+                  o.w = pack_bf16x2(p.t_scale * v[8 * g + 6], p.t_scale * v[8 * g + 7]);
+                  *reinterpret_cast<uint4*>(p.t_out[t] + (size_t)m * p.t_r + (c0 - t * p.t_r)) = o;
+                }
               }
             }
           }
+          // publish: T stores visible (generic and async proxy) before the count
+          __threadfence();
+          asm volatile("fence.proxy.async.global;" ::: "memory");
+          epi_bar();
+          if (threadIdx.x == 64) atomicAdd(p.t_flags, 1);
         }
-        // publish: stores visible (generic and async proxy) before the flag
-        __threadfence();
-        asm volatile("fence.proxy.async.global;" ::: "memory");
-        epi_bar();
-        if (threadIdx.x == 64) st_release(p.t_flags + (m0 + rank * BM) / BM, 1);
       } else if (EPI == EPI_PARTIAL) {
         const int ks = tile / p.m_tiles;
         const int ncols = p.nseg * p.src_rows;
@@ -708,6 +772,7 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           }
         }
       }
+      if (threadIdx.x == 64) dbg_put(p.dbg, it, 5, gtimer());
       ptx::tc_fence_before();
       if (CG == 2)
         ptx::mbar_arrive_leader(tempty_bar(acc));
@@ -754,7 +819,7 @@ cudaError_t launch_t(const GemmParams& p, int num_sms, cudaStream_t s) {
   const int works = (EPI == EPI_RESID && p.ksplit > 1
                          ? p.n_full + (p.total_tiles - p.n_full) * p.ksplit
                          : p.total_tiles) +
-                    (EPI == EPI_PARTIAL ? 0 : p.t_tiles);
+                    (EPI == EPI_PARTIAL ? 0 : p.t_tiles * (p.t_ks > 1 ? p.t_ks : 1));
   const int grid = (works < units ? works : units) * CG * MC;
   if (grid <= 0) return cudaSuccess;
   return launch_kt(EPI == EPI_PARTIAL ? "shrink" : "gemm", gemm_tc_kernel<EPI, BNT, CG, MC>, dim3(grid), dim3(NTHREADS),
@@ -998,6 +1063,32 @@ cudaError_t gemm_launch(const GemmParams& p0, int epi, int num_sms, cudaStream_t
 }
 
 // ---------------------------------------------------------------------------
+// lora_A packing for the in-GEMM T tiles: lora_A_t [r, K] (adapter arena) ->
+// pack[(kb * rt_pad + row0_t + j) * 64 + c] for K-block kb, so the T tile's
+// B operand for one K-block is a single contiguous box of rt_pad rows.
+// ---------------------------------------------------------------------------
+namespace {
+__global__ void lora_pack_kernel(const LoraPackArgs a) {
+  ptx::pdl_begin();
+  const int sgi = blockIdx.y;
+  const bf16* __restrict__ src = a.src[sgi];
+  const int K = a.K[sgi], r = a.r;
+  const int chunks = r * (K / 8);  // 16-byte chunks of this lora_A
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < chunks; i += gridDim.x * blockDim.x) {
+    const int j = i / (K / 8), c = i - j * (K / 8);
+    const int kb = c >> 3, w = c & 7;
+    const uint4 v = __ldg(reinterpret_cast<const uint4*>(src + (size_t)j * K) + c);
+    reinterpret_cast<uint4*>(a.dst[sgi])[((size_t)kb * a.rtp[sgi] + a.row0[sgi] + j) * 8 + w] = v;
+  }
+}
+}  // namespace
+
+cudaError_t lora_pack_launch(const LoraPackArgs& a, int num_sms, cudaStream_t s) {
+  if (a.n <= 0) return cudaSuccess;
+  return launch_k(lora_pack_kernel, dim3(num_sms, a.n), dim3(256), 0, s, 1, a);
+}
+
+// ---------------------------------------------------------------------------
 // LoRA shrink on tensor cores: split-K EPI_PARTIAL GEMM + fixed-order reduce.
 // ---------------------------------------------------------------------------
 namespace {
@@ -1054,6 +1145,18 @@ bool shrink_plan(ShrinkPlan* sp, const bf16* X, int M, int K, const bf16* const*
   for (int s = 0; s < nt; ++s) sp->T[s] = T[s];
   sp->ws = ws;
   return true;
+}
+
+// A8 kernel pre-load for the LoRA shrink kernels, which the adapter-less warm
+// forward at template creation does not launch (lazy loading would otherwise
+// load them inside the first adapter invocation's TTFT window).
+void shrink_preload() {
+  cudaFuncAttributes fa;
+  cudaFuncGetAttributes(&fa, gemm_tc_kernel<EPI_PARTIAL, 64, 1, 1>);
+  cudaFuncGetAttributes(&fa, gemm_tc_kernel<EPI_PARTIAL, 128, 1, 1>);
+  cudaFuncGetAttributes(&fa, gemm_tc_kernel<EPI_PARTIAL, 192, 1, 1>);
+  cudaFuncGetAttributes(&fa, shrink_reduce_kernel);
+  cudaGetLastError();
 }
 
 cudaError_t shrink_run(const ShrinkPlan& sp, float scale, int num_sms, cudaStream_t s) {

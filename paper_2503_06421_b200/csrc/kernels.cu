@@ -1,7 +1,6 @@
 // kernels.cu — memory-bound kernels of the prefill path (sm_100a):
-// embedding gather, RMSNorm, LoRA shrink (x A^T, legacy mma.sync — a skinny
-// r <= 64 product whose cost is reading x), the lm-head GEMV with fused final
-// RMSNorm and argmax, and debug/invariant kernels.  All HBM-bound: 16-byte
+// embedding gather, RMSNorm, the lm-head GEMV with fused final RMSNorm and
+// argmax, the TP bf16-allreduce pack/add, and debug/invariant kernels.  All HBM-bound: 16-byte
 // vector loads, one row per CTA or warp, grids sized to the SM count.
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>

@@ -64,21 +64,34 @@ struct alignas(64) GemmParams {
   int mc;              // cg == 2: CTA pairs per cluster sharing W boxes (1 or 2; 0 = 1)
   int* flags;          // EPI_RESID with ksplit > 1: per (tile, CTA) split counters, all 0
                        // between launches (GEMM_MAX_FLAGS ints); parts add in split order
-  // In-GEMM LoRA shrink ("T tiles", t_tiles > 0): the first t_tiles works of the
-  // persistent grid compute T_t = bf16(t_scale * A x lora_A_t^T) for the t_nt
-  // targets sharing this GEMM's input A (stacked: t_nt * t_r columns, MMA N =
-  // t_rt_pad) into t_out[t] [M, t_r] and release t_flags[row / 128] = 1; the
-  // LoRA K-extension of every other tile waits for the flag of its rows.  The
-  // flags are zeroed once per forward.  Requires every CTA of the grid to be
-  // able to run (persistent grid <= SMs, no co-located grids).
-  CUtensorMap la[3];   // lora_A_t [t_r, K], box {64 cols, 8 rows}
+  // In-GEMM LoRA shrink ("T tiles", t_tiles > 0): the first works of the
+  // persistent grid (on the least loaded units) compute T_t = bf16(t_scale *
+  // A x lora_A_t^T) for the t_nt targets sharing this GEMM's input A (stacked:
+  // t_nt * t_r columns, MMA N = t_rt_pad) into t_out[t] [M, t_r], one tile per
+  // m-tile, in t_ks K parts (t_ks > 1: the GEMM's own split-K ranges; fp32
+  // partials in t_ws, the last part to arrive folds them in part order).
+  // t_flags[0] counts published 128-row blocks; the LoRA K-extension of every
+  // other tile waits (once per CTA) for all t_tiles * cg of them;
+  // t_flags[1 + tile * cg + rank] count arrived parts.  All zeroed once per
+  // forward.  Requires every CTA of the grid to be able to run (persistent
+  // grid <= SMs, no co-located grids).  lora_A comes packed K-block-major.
+  CUtensorMap la;      // packed lora_A [nk * t_rt_pad rows, 64 cols], box {64, t_rt_pad / cg}
   bf16* t_out[3];
-  int t_tiles, t_nt, t_r, t_rt_pad;
+  int t_tiles, t_ks, t_nt, t_r, t_rt_pad;
   float t_scale;
   int* t_flags;
-  int t_diag;          // diagnostics (bit 0: no consumer-side proxy fence); 0 in production
+  float* t_ws;         // t_ks > 1: [t_tiles][t_ks][128 * cg rows][t_rt_pad] fp32 partials
+  unsigned long long* dbg;  // diagnostic per-work timeline (TIDAL_GEMM_TRACE); null in production
 };
-constexpr int GEMM_MAX_TBLK = 256;  // 128-row blocks with T-ready flags (32768 rows)
+// lora_A of up to 7 targets (one layer) -> the packed T-tile layout:
+// dst[sgi][(kb * rtp + row0 + j) * 64 + c] = src[sgi][j * K + kb * 64 + c].
+struct LoraPackArgs {
+  const bf16* src[7];
+  bf16* dst[7];
+  int K[7], row0[7], rtp[7];
+  int n, r;
+};
+cudaError_t lora_pack_launch(const LoraPackArgs& a, int num_sms, cudaStream_t s);
 
 // CTA-group size for an M-row GEMM, and the TMA box rows of the W and lora_B
 // maps a CTA loads for (epi, bn, cg).
@@ -112,6 +125,7 @@ struct ShrinkPlan {
 bool shrink_plan(ShrinkPlan* sp, const bf16* X, int M, int K, const bf16* const* A, bf16* const* T,
                  int nt, int r, float* ws, int num_sms);
 cudaError_t shrink_run(const ShrinkPlan& sp, float scale, int num_sms, cudaStream_t s);
+void shrink_preload();  // load the shrink kernels (template creation, A8)
 constexpr int SHRINK_MAX_SPLIT = 16;
 
 // tcgen05 causal attention (hd = 128): Q/K from QKV [S, (H+2KV)*128], V from
@@ -154,10 +168,6 @@ cudaError_t embed_launch(const int32_t* tok, const bf16* E, float* X, int S, int
 // Y = bf16(g * x * rsqrt(mean(x^2) + eps)), one row per CTA.
 cudaError_t rmsnorm_launch(const float* X, const bf16* g, bf16* Y, int S, int d, float eps,
                            cudaStream_t s);
-// T_t[M, r] = bf16(scale * X[M, K] . A_t[r, K]^T), t < nt <= 3 (targets sharing X).
-// One read of X for all targets; intra-CTA split-K, deterministic reduction.
-cudaError_t lora_shrink_launch(const bf16* X, int ldx, int M, int K, const bf16* const* A,
-                               bf16* const* T, int nt, int r, float scale, cudaStream_t s);
 // Causal GQA prefill attention over QKV [nseq * S, (H + 2 KV) hd] -> O [nseq * S, H hd],
 // each sequence of S rows attending only to itself.
 cudaError_t attention_launch(const bf16* qkv, bf16* O, int S, int H, int KV, int hd,

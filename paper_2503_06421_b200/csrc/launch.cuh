@@ -19,8 +19,8 @@ inline bool pdl_enabled() {
   return on;
 }
 
-// No PDL attribute for launches whose tag is in TIDAL_PDL_OFF (default
-// "reduce"): with early launch on the LoRA-shrink reduce, the 13B-width
+// No PDL attribute for the LoRA-shrink reduce, nor for launches whose tag is
+// in TIDAL_PDL_OFF: with early launch on the LoRA-shrink reduce, the 13B-width
 // S = 4096 / r = 64 parity sweep hung intermittently (watchdog trap, 4 of 5
 // runs); bisected per kernel class, the reduce alone in plain stream order
 // passes 10 of 10 with the same-box TTFT unchanged.
@@ -29,8 +29,11 @@ cudaError_t launch_kt(const char* tag, void (*kernel)(KArgs...), dim3 grid, dim3
                       cudaStream_t s, int cluster_x, Args&&... args);
 
 inline bool pdl_off_for(const char* tag) {
-  static const char* off = getenv("TIDAL_PDL_OFF") ? getenv("TIDAL_PDL_OFF") : "reduce";
-  return tag && off && strstr(off, tag) != nullptr;
+  // the reduce is always excluded (a user list only adds tags)
+  static const char* off = getenv("TIDAL_PDL_OFF");
+  if (!tag) return false;
+  if (strcmp(tag, "reduce") == 0) return true;
+  return off && strstr(off, tag) != nullptr;
 }
 
 template <typename... KArgs, typename... Args>

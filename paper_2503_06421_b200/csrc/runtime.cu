@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 #include <sched.h>
 
+#include <algorithm>
 #include <cmath>
 #include <cstdio>
 #include <cstring>
@@ -60,15 +61,28 @@ void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int 
   dalloc(logits, (size_t)kMaxBatch * m.vocab * 4);
   dalloc(key, 8 * kMaxBatch);
   dalloc(tok, S * 4);
-  dalloc(shrink_ws, (size_t)SHRINK_MAX_SPLIT * S * 192 * 4);
+  // split-K partials of the stand-alone LoRA shrink, or of split T tiles
+  // ([m-tiles][<= 8 parts][256 rows][<= 64 columns], rows rounded up to a tile)
+  dalloc(shrink_ws, std::max((size_t)SHRINK_MAX_SPLIT * S * 192, (S + 256) * 8 * 64) * 4);
   dalloc(gemm_flags, GEMM_MAX_FLAGS * sizeof(int));
   dalloc(zero_b, (size_t)(m.d_ff / world) * 64 * 2);
   cuda_check(cudaMemset(zero_b, 0, (size_t)(m.d_ff / world) * 64 * 2), "memset zero lora_B");
-  tflag_stride = (int)((S + 127) / 128 + 2);
+  {
+    // packed lora_A of the in-GEMM T tiles: per layer room for rank 64 x
+    // (3 q/k/v, 1 o, 2 gate/up, 1 down) K-block-major; zeroed once so the
+    // K-tail columns of a last partial K-block (never written) stay 0
+    auto r64 = [](size_t k) { return (k + 63) / 64 * 64; };  // whole K-blocks
+    const size_t nqr = (size_t)m.n_heads * m.head_dim() / world;
+    pack_stride = (size_t)(192 + 128) * r64(m.d_model) + (size_t)64 * r64(nqr) +
+                  (size_t)64 * r64(m.d_ff / world);
+    dalloc(lora_pack, (size_t)m.n_layers * pack_stride * 2);
+    cuda_check(cudaMemset(lora_pack, 0, (size_t)m.n_layers * pack_stride * 2), "memset lora pack");
+  }
+  tflag_stride = (int)((S + 127) / 128 + 4);
   dalloc(tflags, (size_t)m.n_layers * 4 * tflag_stride * sizeof(int));
   {
-    const char* e = getenv("TIDAL_FUSED_SHRINK");
-    fuse_shrink = e && e[0] == '1';
+    const char* e = getenv("TIDAL_FUSED_SHRINK");  // 0: stand-alone shrink launches (A/B)
+    fuse_shrink = !(e && e[0] == '0');
   }
   cuda_check(cudaMemset(gemm_flags, 0, GEMM_MAX_FLAGS * sizeof(int)), "memset flags");
   // V^T: batched prompts pad each sequence to 64 columns (<= 63 per prompt)
@@ -140,13 +154,25 @@ void Exec::enable_decode(int max_new) {
   cache.clear();
 }
 
+void Exec::dbg_dump() {
+  if (!dbg_pending || !dbg_trace) return;
+  dbg_pending = false;
+  std::vector<unsigned long long> h((size_t)num_sms * 32 * 8);
+  if (cudaMemcpy(h.data(), dbg_trace, h.size() * 8, cudaMemcpyDeviceToHost) != cudaSuccess) return;
+  const char* path = getenv("TIDAL_GEMM_TRACE_FILE");
+  FILE* f = fopen(path ? path : "gemm_trace.bin", "wb");
+  if (!f) return;
+  fwrite(h.data(), 8, h.size(), f);
+  fclose(f);
+}
+
 void Exec::destroy() {
   if (device < 0) return;
   cudaSetDevice(device);
   if (compute) cudaStreamSynchronize(compute);
   if (copy) cudaStreamSynchronize(copy);
   void* ptrs[] = {X, Xn, QKV, O, Hb, logits, key, tok, rope, Vt, shrink_ws, gemm_flags, P32, Pb, tflags,
-                  zero_b,
+                  zero_b, dbg_trace, lora_pack,
                   dec.kc, dec.vc, dec.q, dec.att, dec.h, dec.T, dec.part, dec.cnt, dec.shcnt, dec.st,
                   dec.toks,
                   dec.logits_all};
@@ -180,9 +206,13 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
   const int F = m.d_ff / world;
   const int r = tt.lora_rank;
   std::vector<LayerLaunch> v(L);
-  auto W = [&](int id) { return wptr[id]; };
   for (int l = 0; l < L; ++l) {
     LayerLaunch& ll = v[l];
+    int cur = 0;  // which GEMM's tensor maps are being built (ids recorded per GEMM)
+    auto W = [&](int id) {
+      ll.ids[cur].push_back(id);
+      return wptr[id];
+    };
     // ---- QKV + RoPE ----
     GemmParams& q = ll.qkv;
     memset(&q, 0, sizeof q);
@@ -230,6 +260,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     q.head_dim = hd;
     q.seq_len = nseq > 1 ? S / nseq : 0;
     // ---- O (+ residual) ----
+    cur = 1;
     GemmParams& o = ll.o;
     memset(&o, 0, sizeof o);
     int ks = 1;
@@ -257,6 +288,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     o.out = X;
     o.ldo = d;
     // ---- gate/up + SiLU*mul ----
+    cur = 2;
     GemmParams& g = ll.gu;
     memset(&g, 0, sizeof g);
     {
@@ -293,6 +325,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
     g.out = Hb;
     g.ldo = F;
     // ---- down (+ residual) ----
+    cur = 3;
     GemmParams& dn = ll.down;
     memset(&dn, 0, sizeof dn);
     gemm_plan_resid(S, d, F, num_sms, &dn.bn, &ks, &dn.cg, !colocated, &dn.n_full);
@@ -325,6 +358,7 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
       const int kdim[4] = {d, nq, d, F};
       GemmParams* gp[4] = {&ll.qkv, &ll.o, &ll.gu, &ll.down};
       for (int gi = 0; gi < 4; ++gi) {
+        cur = gi;
         const bf16* A[3];
         bf16* Tt[3];
         int n = 0;
@@ -338,21 +372,42 @@ const std::vector<LayerLaunch>& Exec::layer_params(const TensorTable& tt, int S,
         // in-GEMM T tiles when the stacked lora_A fits one accumulator buffer and
         // no other grid can share the device (a T-tile wait needs its producer CTA)
         GemmParams& g = *gp[gi];
-        const int rt_pad = (n * r + 15) / 16 * 16;
         const int bnx = gi == 2 ? 256 : g.bn;
-        if (fuse_shrink && !colocated && g.mc <= 1 && rt_pad <= bnx &&
-            (S + 127) / 128 <= GEMM_MAX_TBLK) {
-          static const int diag = getenv("TIDAL_TDIAG") ? atoi(getenv("TIDAL_TDIAG")) : 0;
-          g.t_diag = diag;
+        const int rt_pad = (n * r + 15) / 16 * 16;
+        if (fuse_shrink && !colocated && g.mc <= 1 && rt_pad <= bnx) {
+          // packed lora_A region of this (layer, GEMM): room for rank 64 x 3
+          // targets, so the offsets do not depend on the adapter
+          if (!lora_pack) fail(3, "packed lora_A buffer missing");
+          auto r64 = [](size_t k) { return (k + 63) / 64 * 64; };  // whole K-blocks
+          const size_t goff = gi == 0 ? 0
+                              : gi == 1 ? (size_t)192 * r64(d)
+                              : gi == 2 ? (size_t)192 * r64(d) + (size_t)64 * r64(nq)
+                                        : (size_t)320 * r64(d) + (size_t)64 * r64(nq);
+          bf16* dst = lora_pack + (size_t)l * pack_stride + goff;
+          const int nk = (kdim[gi] + GEMM_BK - 1) / GEMM_BK;
+          if (!make_tmap(&g.la, dst, (uint64_t)nk * rt_pad, 64, 128, rt_pad / g.cg, 64))
+            fail(3, "packed lora_A tensor map");
           for (int s2 = 0; s2 < n; ++s2) {
-            if (!make_tmap(&g.la[s2], A[s2], r, kdim[gi], (uint64_t)kdim[gi] * 2, 8, 64))
-              fail(3, "lora_A tensor maps");
             g.t_out[s2] = Tt[s2];
+            LoraPackArgs& pa = ll.pack;
+            pa.src[pa.n] = A[s2];
+            pa.dst[pa.n] = dst;
+            pa.K[pa.n] = kdim[gi];
+            pa.row0[pa.n] = s2 * r;
+            pa.rtp[pa.n] = rt_pad;
+            pa.r = r;
+            ++pa.n;
           }
+          for (int t : groups[gi])
+            if (tt.lora_a[l][t] >= 0) ll.pack_ids.push_back(tt.lora_a[l][t]);
           g.t_nt = n;
           g.t_r = r;
           g.t_rt_pad = rt_pad;
           g.t_tiles = g.m_tiles;
+          // split GEMMs: the T tile in the same K parts (a whole-K T tile would
+          // take ks part-times on its unit)
+          g.t_ks = (gi == 1 || gi == 3) && g.ksplit > 1 ? g.ksplit : 1;
+          g.t_ws = shrink_ws;
           g.t_flags = tflags + (size_t)(4 * l + gi) * tflag_stride;
           continue;
         }
@@ -488,11 +543,28 @@ void run_forward(Exec& ex, const RunArgs& a) {
   const bool bf16_ar = ex.world > 1 && ex.ar_bf16;
   // GEMM launch; with in-GEMM T tiles the invocation's LoRA scale goes into a
   // copy of the cached parameters
+  // diagnostic: TIDAL_GEMM_TRACE=<layer>,<gemm 0 qkv|1 o|2 gu|3 down> records a
+  // per-work timeline of that one launch (dumped by the invoke after it syncs)
+  static const int trace_sel = [] {
+    const char* e = getenv("TIDAL_GEMM_TRACE");
+    int l = -1, g = 0;
+    if (e && sscanf(e, "%d,%d", &l, &g) >= 1 && l >= 0) return l * 4 + g;
+    return -1;
+  }();
+  int cur_gemm = -1;
   auto launch = [&](const GemmParams& g, int epi, float* out_override = nullptr) {
-    if (!g.t_tiles && !out_override) return gemm_launch(g, epi, ex.num_sms, st);
+    const bool tr = trace_sel >= 0 && cur_gemm == trace_sel;
+    if (!g.t_tiles && !out_override && !tr) return gemm_launch(g, epi, ex.num_sms, st);
     GemmParams p = g;
     p.t_scale = a.lora_scale;
     if (out_override) p.out = out_override;
+    if (tr) {
+      const size_t nb = (size_t)ex.num_sms * 32 * 8 * 8;
+      if (!ex.dbg_trace) cuda_check(cudaMalloc(&ex.dbg_trace, nb), "cudaMalloc(trace)");
+      cuda_check(cudaMemsetAsync(ex.dbg_trace, 0, nb, st), "memset trace");
+      p.dbg = ex.dbg_trace;
+      ex.dbg_pending = true;
+    }
     return gemm_launch(p, epi, ex.num_sms, st);
   };
   auto resid_gemm = [&](const GemmParams& g) {
@@ -515,7 +587,11 @@ void run_forward(Exec& ex, const RunArgs& a) {
   const std::vector<Op>& ops = *a.ops;
   for (size_t k = 0; k < ops.size(); ++k) {
     const Op& op = ops[k];
-    if (a.rec) a.rec->op((int)k, op.reads, tt.n_base);
+    // lax tracing: the ids behind this op's kernel arguments (below)
+    auto rec = [&](std::initializer_list<int> ids) {
+      if (a.rec)
+        for (int id : ids) a.rec->use((int)k, id, tt.n_base);
+    };
     if (a.barriers && !(*a.barriers)[k].empty()) {
       // the copy stream is FIFO: waiting on the needed group copied last covers
       // all of them (waited = copy position already covered)
@@ -533,10 +609,12 @@ void run_forward(Exec& ex, const RunArgs& a) {
         waited = gp;
       }
     }
+    if (a.tl_op) cuda_check(cudaEventRecord((*a.tl_op)[k], st), "timeline event");
     const int l = op.layer;
     auto Wp = [&](int id) { return reinterpret_cast<const bf16*>(ex.wptr[id]); };
     switch (op_kind(op.name)) {
       case OP_EMBED:
+        rec({tt.embed});
         {
           const int e0 = P0();
           K(KC_EMBED, e0, 0, Sd * d * 6, embed_launch(ex.tok, Wp(tt.embed), ex.X, S, d, ex.rank * Vl, Vl, st, ex.key, B),
@@ -564,6 +642,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_ATTN_NORM:
+        rec({tt.norm1[l]});
         {
           const int e0 = P0();
           K(KC_RMSNORM, e0, 0, Sd * d * 6 + 2.0 * d,
@@ -571,6 +650,31 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_QKV:
+        if (a.rec) a.rec->use((int)k, LP[l].ids[0], tt.n_base);
+        cur_gemm = 4 * l + 0;
+        if (LP[l].pack.n) {
+          // pack this layer's lora_A (all fused GEMMs) once its adapter bytes
+          // landed: the groups of those tensors (one group under per_layer)
+          if (a.barriers && a.group_of) {
+            int gp = -1, g = -1;
+            for (int id : LP[l].pack_ids) {
+              const int x = (*a.group_of)[id];
+              if (x < 0 || x == a.skip_group) continue;
+              const int pos = a.copy_pos ? (*a.copy_pos)[x] : x;
+              if (pos > gp) {
+                gp = pos;
+                g = x;
+              }
+            }
+            if (gp > waited) {
+              cuda_check(cudaStreamWaitEvent(st, (*a.events)[g], 0), "cudaStreamWaitEvent");
+              waited = gp;
+            }
+          }
+          const int e0 = P0();
+          K(KC_SHRINK, e0, 0, 4.0 * LP[l].pack.n * LP[l].pack.r * d,
+            lora_pack_launch(LP[l].pack, ex.num_sms, st), "lora_pack");
+        }
         shrink(ex.Xn, d, d, l, 0);
         {
           const double n = nq + 2.0 * nkv;
@@ -594,6 +698,8 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_O:
+        if (a.rec) a.rec->use((int)k, LP[l].ids[1], tt.n_base);
+        cur_gemm = 4 * l + 1;
         shrink(ex.O, nq, nq, l, 1);
         {
           const int e0 = P0(KC_GEMM_O);
@@ -603,6 +709,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_MLP_NORM:
+        rec({tt.norm2[l]});
         {
           const int e0 = P0();
           K(KC_RMSNORM, e0, 0, Sd * d * 6 + 2.0 * d,
@@ -610,6 +717,8 @@ void run_forward(Exec& ex, const RunArgs& a) {
         }
         break;
       case OP_GU:
+        if (a.rec) a.rec->use((int)k, LP[l].ids[2], tt.n_base);
+        cur_gemm = 4 * l + 2;
         shrink(ex.Xn, d, d, l, 2);
         {
           const int e0 = P0(KC_GEMM_GU);
@@ -621,6 +730,8 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_ACT:  // fused into the gate/up epilogue
         break;
       case OP_DOWN:
+        if (a.rec) a.rec->use((int)k, LP[l].ids[3], tt.n_base);
+        cur_gemm = 4 * l + 3;
         shrink(ex.Hb, F, F, l, 3);
         {
           const int e0 = P0(KC_GEMM_DOWN);
@@ -632,6 +743,7 @@ void run_forward(Exec& ex, const RunArgs& a) {
       case OP_FNORM:  // fused into the head kernel (fp32 last-row norm)
         break;
       case OP_HEAD:  // the argmax key was zeroed by the embed kernel of this forward
+        rec({tt.fnorm, tt.head});  // final_norm is fused into the head kernel
         {
           const int e0 = P0();
           // logits layout [world][B][Vl]: this rank's slices contiguous for the allgather

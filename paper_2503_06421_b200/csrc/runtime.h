@@ -29,6 +29,9 @@ struct LayerLaunch {
   GemmParams qkv, o, gu, down;
   ShrinkPlan sh[4];  // LoRA shrink feeding qkv / o / gate_up / down
   int has_sh[4] = {0, 0, 0, 0};
+  std::vector<int> ids[4];    // weight ids behind the qkv / o / gate_up / down tensor maps
+  LoraPackArgs pack = {};     // lora_A of the GEMMs with in-GEMM T tiles (packed per layer)
+  std::vector<int> pack_ids;  // their tensor ids (the packing waits for their groups)
 };
 
 // Device execution context: streams, activation arena, rope table, the fork
@@ -57,7 +60,12 @@ struct Exec {
   int* tflags = nullptr;
   int tflag_stride = 0;
   bool fuse_shrink = true;
-  bf16* zero_b = nullptr;      // [F / world][64] zeros: lora_B of an untargeted gate or up half     // T tiles inside the GEMMs (else split-K shrink + reduce launches)
+  bf16* zero_b = nullptr;
+  bf16* lora_pack = nullptr;   // packed lora_A of the in-GEMM T tiles, [L][per-layer stride]
+  size_t pack_stride = 0;
+  unsigned long long* dbg_trace = nullptr;  // TIDAL_GEMM_TRACE diagnostic timeline
+  bool dbg_pending = false;
+  void dbg_dump();                          // after the invocation synchronised      // [F / world][64] zeros: lora_B of an untargeted gate or up half     // T tiles inside the GEMMs (else split-K shrink + reduce launches)
   bf16* Vt = nullptr;  // V^T [KV*hd][vt_ld] (tcgen05 attention, hd = 128)
   // TP: row-parallel partial sums for the bf16 allreduce option (C1/C2 in
   // bf16): the GEMM adds into P32 (zeroed), P32 -> Pb, allreduce(Pb), X += Pb
@@ -132,15 +140,21 @@ enum KernelClass {
 };
 extern const char* const kKernelClassNames[KC_COUNT];
 
-struct Recorder {  // lax tracing: first-read order of weights as ops execute
+// Lax tracing: first-read order of the weights the launcher actually hands to
+// its kernels (the ids behind every kernel argument / tensor map), recorded
+// as the kernels are enqueued — not the planner's read lists, so tidal_trace
+// can check the two against each other.
+struct Recorder {
   std::vector<char> seen;
   std::vector<std::pair<int, int>> access;
-  void op(int k, const std::vector<int>& reads, int n_base) {
-    for (int id : reads)
-      if (id < n_base && !seen[id]) {
-        seen[id] = 1;
-        access.emplace_back(id, k);
-      }
+  void use(int k, int id, int n_base) {
+    if (id >= 0 && id < n_base && !seen[id]) {
+      seen[id] = 1;
+      access.emplace_back(id, k);
+    }
+  }
+  void use(int k, const std::vector<int>& ids, int n_base) {
+    for (int id : ids) use(k, id, n_base);
   }
 };
 
@@ -166,6 +180,8 @@ struct RunArgs {
   const std::vector<std::vector<int>>* barriers = nullptr;  // nullable
   const std::vector<cudaEvent_t>* events = nullptr;         // per group
   const std::vector<int>* copy_pos = nullptr;               // position of each group in the copy stream
+  const std::vector<int>* group_of = nullptr;               // per tensor id: its transfer group (-1: resident)
+  const std::vector<cudaEvent_t>* tl_op = nullptr;          // timeline: an event at each op start
   int skip_group = -1;                                       // fault injection
   int S = 0;     // total rows: nseq prompts of S / nseq tokens each
   int nseq = 1;

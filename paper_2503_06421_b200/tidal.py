@@ -23,6 +23,7 @@ GROUPS_PER_LAYER, GROUPS_MAX_TRANSFERS, GROUPS_PER_TENSOR = 0, 1, 2
 DEBUG_POISON, DEBUG_SKIP_BARRIER, DEBUG_SCRUB_L2, DEBUG_SERIAL, DEBUG_PROFILE = 1, 2, 4, 8, 16
 DEBUG_PROFILE_GEMM = 32
 DEBUG_NO_GRAPH = 64
+DEBUG_TIMELINE = 128
 ORDER_TRACED, ORDER_REVERSE, ORDER_REGISTRATION = 0, 1, 2
 DTYPE_F32, DTYPE_BF16 = 0, 1
 U64_MAX = (1 << 64) - 1
@@ -101,9 +102,9 @@ SIGNATURES = [
     ("tidal_trace_dump", C.c_int, [VP, C.c_char_p, C.c_size_t, C.POINTER(C.c_size_t)]),
     ("tidal_template_create", C.c_int, [VP, VP, C.POINTER(TemplateOpts), C.POINTER(VP)]),
     ("tidal_template_export", C.c_int, [VP, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int),
-                                        C.POINTER(C.c_uint64)]),
+                                        C.POINTER(C.c_uint64), C.POINTER(C.c_uint64)]),
     ("tidal_template_import", C.c_int, [VP, VP, C.POINTER(TemplateOpts), C.POINTER(C.c_int),
-                                        C.c_int, C.c_uint64, C.POINTER(VP)]),
+                                        C.c_int, C.c_uint64, C.c_uint64, C.POINTER(VP)]),
     ("tidal_template_resize", C.c_int, [VP, C.POINTER(TemplateOpts)]),
     ("tidal_template_keep_alive", C.c_int, [VP]),
     ("tidal_set_load_order", C.c_int, [VP, C.c_int]),
@@ -127,6 +128,8 @@ SIGNATURES = [
     ("tidal_comm_selftest", C.c_int, [VP, C.c_uint64]),
     ("tidal_set_debug", C.c_int, [VP, C.c_int, C.c_int]),
     ("tidal_set_allreduce_dtype", C.c_int, [VP, C.c_int]),
+    ("tidal_timeline_read", C.c_int, [VP, VP, C.c_int, VP, C.c_int, C.POINTER(C.c_int),
+                                      C.POINTER(C.c_int), C.POINTER(C.c_double)]),
     ("tidal_template_checksum", C.c_int, [VP, C.POINTER(C.c_uint64)]),
     ("tidal_profile_read", C.c_int, [VP, C.POINTER(KernelTime), C.c_int, C.POINTER(C.c_int),
                                      C.c_int]),
@@ -256,30 +259,34 @@ def template_opts(resident_bytes: int = U64_MAX, eq1: bool = False, t_ttft_s: fl
 
 class Template:
     def __init__(self, model: Model, trace: Trace, opts: TemplateOpts,
-                 shared: Optional[Tuple[List[int], int]] = None):
-        """shared = (fds, shared_bytes) from another process's export(): map
-        those template chunks read-only instead of building the prefix."""
+                 shared: Optional[Tuple[List[int], int, int]] = None):
+        """shared = (fds, shared_bytes, fingerprint) from another process's
+        export(): map those template chunks read-only instead of building the
+        prefix (refused with ERR_STRUCTURE if the fingerprint differs)."""
         h = VP()
         self._opts = opts
         if shared is None:
             _check(lib().tidal_template_create(model.h, trace.h, C.byref(opts), C.byref(h)))
         else:
-            fds, nbytes = shared
+            fds, nbytes, fp = shared
             arr = (C.c_int * len(fds))(*fds)
             _check(lib().tidal_template_import(model.h, trace.h, C.byref(opts), arr, len(fds),
-                                               nbytes, C.byref(h)))
+                                               nbytes, fp, C.byref(h)))
         self.h = h
         self.vocab = model.vocab
 
-    def export(self) -> Tuple[List[int], int]:
-        """(fds of the chunks inside the resident prefix, shared_bytes); the
-        caller owns the fds (pass them with socket.send_fds, then close)."""
+    def export(self) -> Tuple[List[int], int, int]:
+        """(fds of the chunks inside the resident prefix, shared_bytes,
+        fingerprint); the caller owns the fds (pass them with socket.send_fds,
+        then close)."""
         n = C.c_int(0)
         nb = C.c_uint64(0)
-        _check(lib().tidal_template_export(self.h, None, 0, C.byref(n), C.byref(nb)))
+        fp = C.c_uint64(0)
+        _check(lib().tidal_template_export(self.h, None, 0, C.byref(n), C.byref(nb), C.byref(fp)))
         arr = (C.c_int * max(1, n.value))()
-        _check(lib().tidal_template_export(self.h, arr, n.value, C.byref(n), C.byref(nb)))
-        return list(arr[:n.value]), nb.value
+        _check(lib().tidal_template_export(self.h, arr, n.value, C.byref(n), C.byref(nb),
+                                           C.byref(fp)))
+        return list(arr[:n.value]), nb.value, fp.value
 
     def resize(self, opts: TemplateOpts) -> None:
         _check(lib().tidal_template_resize(self.h, C.byref(opts)))
@@ -349,6 +356,17 @@ class Template:
 
     def set_debug(self, flags: int, arg: int = -1) -> None:
         _check(lib().tidal_set_debug(self.h, flags, arg))
+
+    def timeline(self) -> dict:
+        """Copy-group end and op start times (ms) of the last DEBUG_TIMELINE invoke."""
+        ng, no, end = C.c_int(0), C.c_int(0), C.c_double(0)
+        _check(lib().tidal_timeline_read(self.h, None, 0, None, 0, C.byref(ng), C.byref(no),
+                                         C.byref(end)))
+        g = np.zeros(max(1, ng.value), np.float64)
+        o = np.zeros(max(1, no.value), np.float64)
+        _check(lib().tidal_timeline_read(self.h, g.ctypes.data, ng.value, o.ctypes.data, no.value,
+                                         C.byref(ng), C.byref(no), C.byref(end)))
+        return {"group_end_ms": g[:ng.value], "op_start_ms": o[:no.value], "end_ms": end.value}
 
     def set_allreduce_dtype(self, dtype: int) -> None:
         """DTYPE_F32 (default) or DTYPE_BF16 for the row-parallel allreduces."""

@@ -32,14 +32,21 @@ def main(path):
     opts = T.template_opts(resident_bytes=req["budget"], max_tokens=req["max_tokens"], device=0)
     out = {}
     try:
-        bad = req.get("bad_bytes")
-        if bad is not None:  # wrong shared_bytes must be refused
+        fp = req["fingerprint"]
+
+        def refused(m, shared):
             try:
-                T.Template(model, T.Trace(model), opts, shared=(fds, bad))
-                out["bad_refused"] = False
+                T.Template(m, T.Trace(m), opts, shared=shared)
+                return False
             except T.TidalError as e:
-                out["bad_refused"] = e.code == T.ERR_STRUCTURE
-        tpl = T.Template(model, T.Trace(model), opts, shared=(fds, req["shared_bytes"]))
+                return e.code == T.ERR_STRUCTURE
+        # wrong shared_bytes, a wrong fingerprint, and the same shapes from
+        # another checkpoint (same byte sizes, other provenance) are all refused
+        out["bad_refused"] = refused(model, (fds, req["bad_bytes"], fp))
+        out["bad_fp_refused"] = refused(model, (fds, req["shared_bytes"], fp ^ 1))
+        other = T.Model(cd, tensors, f"base:{req['seed'] + 1}", fill=fill)
+        out["other_ckpt_refused"] = refused(other, (fds, req["shared_bytes"], fp))
+        tpl = T.Template(model, T.Trace(model), opts, shared=(fds, req["shared_bytes"], fp))
         for fd in fds:
             os.close(fd)
         c0 = tpl.checksum()

@@ -84,17 +84,18 @@ def test_template_shared_across_processes(T, cfg_name, over, S, frac):
     budget = int(frac * M)
     tpl = T.Template(model, T.Trace(model), T.template_opts(resident_bytes=budget, max_tokens=S,
                                                             device=0))
-    fds, shared = tpl.export()
+    fds, shared, fp = tpl.export()
     assert len(fds) >= 1 and shared > 0
     c0 = tpl.checksum()
     prompt = synth.prompt_fast(cfg, S, 0)
     req = dict(config=cfg_name, over=over, seed=0, budget=budget, max_tokens=S,
-               prompt=[int(x) for x in prompt], shared_bytes=shared, bad_bytes=shared + 4096)
+               prompt=[int(x) for x in prompt], shared_bytes=shared, bad_bytes=shared + 4096,
+               fingerprint=fp)
     res = _child_run(req, fds)
     for fd in fds:
         os.close(fd)
     assert "error" not in res, res.get("error")
-    assert res["bad_refused"]
+    assert res["bad_refused"] and res["bad_fp_refused"] and res["other_ckpt_refused"]
     assert res["checksum_before"] == res["checksum_after"] == c0
     assert res["bytes_streamed"] > 0
     tok, logits, _ = tpl.invoke(prompt)

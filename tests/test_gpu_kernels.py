@@ -50,6 +50,19 @@ def _close_bf16(out, ref):
     assert err <= tol, (err, tol)
 
 
+def _close_rows_bf16(out, ref):
+    """Attention: the same bound per output row (query, all heads), so rows
+    that average many keys (small |O|) are held to their own scale, not to the
+    first rows' max|v|: bf16 P (2^-9 rel.) and the bf16 output rounding give
+    <= ~2^-8 of the row's max; 2^-7 leaves 2x headroom (VERDICT r1 weak #2a)."""
+    out = out.reshape(out.shape[0], -1)
+    ref = ref.reshape(ref.shape[0], -1)
+    tol = 2.0 ** -7 * np.abs(ref).max(axis=1) + 1e-3
+    err = np.abs(out - ref).max(axis=1)
+    bad = np.nonzero(err > tol)[0]
+    assert bad.size == 0, (bad[:8], err[bad[:8]], tol[bad[:8]])
+
+
 @pytest.mark.parametrize("M,N,K", [(128, 256, 64), (300, 384, 320), (77, 256, 688), (512, 768, 1024)])
 def test_gemm_store(T, M, N, K):
     rng = np.random.default_rng(M + N + K)
@@ -233,8 +246,7 @@ def test_attention_causal_gqa(T, S, H, KV, hd):
     k = qkv[:, H * hd:(H + KV) * hd].reshape(S, KV, hd)
     v = qkv[:, (H + KV) * hd:].reshape(S, KV, hd)
     ref = F.causal_attention(q, k, v)
-    err = np.abs(_host(O) - ref).max()
-    assert err <= 2e-2, err
+    _close_rows_bf16(_host(O), ref)
 
 
 @pytest.mark.parametrize("S,H,KV", [(1, 2, 1), (128, 2, 2), (300, 4, 2), (1000, 3, 1), (2048, 2, 2)])
@@ -253,8 +265,7 @@ def test_attention_tcgen05(T, S, H, KV):
     O = torch.zeros(S, H * hd, dtype=torch.bfloat16, device="cuda")
     T.k_attention_tc(_dev(qkv), _dev(vt), vt_ld, O, S, H, KV)
     ref = F.causal_attention(q, k, v)
-    err = np.abs(_host(O) - ref).max()
-    assert err <= 2e-2, err
+    _close_rows_bf16(_host(O), ref)
 
 
 def test_attention_tcgen05_large_logits(T):
@@ -270,7 +281,7 @@ def test_attention_tcgen05_large_logits(T):
     O = torch.zeros(S, hd, dtype=torch.bfloat16, device="cuda")
     T.k_attention_tc(_dev(qkv), _dev(vt), S, O, S, H, KV)
     ref = F.causal_attention(q.astype(np.float64), k.astype(np.float64), v.astype(np.float64))
-    assert np.abs(_host(O) - ref).max() <= 2e-2
+    _close_rows_bf16(_host(O), ref)
 
 
 @pytest.mark.parametrize("S,d", [(1, 256), (37, 5120), (16, 4096)])
@@ -302,9 +313,9 @@ def test_embed_and_vocab_shard(T):
                                    (1, 64, 32), (4096, 5120, 64), (20000, 256, 32),
                                    (19000, 128, 16)])
 def test_lora_shrink(T, M, K, r):
-    """Split-K parts of a 128-row block reduced over DSMEM in part order
-    (cluster of <= 8 CTAs); past 148 row blocks one CTA takes the whole K and
-    walks several blocks (no reduction), for r a multiple of 32 or not."""
+    """The stand-alone LoRA shrink T = s X A^T: a split-K tcgen05 GEMM
+    (EPI_PARTIAL, fp32 partials per K range) plus a fixed-order reduce to bf16
+    (gemm_tc.cu shrink_plan / shrink_run), for r a multiple of 32 or not."""
     rng = np.random.default_rng(K)
     X, A = _bf(rng, (M, K)), _bf(rng, (r, K), 1 / math.sqrt(K))
     out = torch.zeros(M, r, dtype=torch.bfloat16, device="cuda")
@@ -341,3 +352,92 @@ def test_head_argmax_ties_lowest_index(T):
     T.k_head(torch.from_numpy(x).cuda(), _dev(g), _dev(W), V, d, 1e-5, logits, key)
     k = int(key.cpu().numpy()[0]) & 0xFFFFFFFFFFFFFFFF
     assert 0xFFFFFFFF - (k & 0xFFFFFFFF) == 7
+
+
+# ---- per-op bf16 ulp checks against the bf16-emulation oracle (SURVEY §8(c) O1:
+# "feed the oracle the GPU's own inputs for a single op, and the outputs must
+# agree to <= 1 bf16 ulp per element for GEMMs, <= 2 ulp where the GPU uses
+# approximate ex2 / rsqrt").  The reference is computed in float64 and rounded
+# once to bf16 (F.round_bf16); the GPU accumulates in fp32 in another order, so
+# a value within ~2^-16 of a rounding boundary may land one ulp away.
+def _ulps(out, ref64, acc_err=None):
+    """bf16 ulp distance between the GPU's bf16 values and round_bf16(ref),
+    after subtracting `acc_err`: the fp32 accumulation bound of a dot product,
+    K * 2^-24 * sum|a_i b_i| (matters only where terms cancel and the result is
+    tiny against its terms; elsewhere it is far below one bf16 ulp)."""
+    r = F.round_bf16(ref64.astype(np.float32)).astype(np.float64)
+    o = out.astype(np.float64)
+    d = np.abs(o - r)
+    if acc_err is not None:
+        d = np.maximum(0.0, d - acc_err)
+    mag = np.maximum(np.abs(o), np.abs(r))
+    ulp = np.exp2(np.floor(np.log2(np.maximum(mag, 2.0 ** -120))) - 7)
+    return d / ulp
+
+
+def _acc_err(A, W, K):
+    return K * 2.0 ** -24 * (np.abs(A.astype(np.float64)) @ np.abs(W.astype(np.float64)).T)
+
+
+@pytest.mark.parametrize("M,N,K", [(300, 384, 320), (512, 768, 1024), (128, 256, 5120)])
+def test_gemm_store_ulp(T, M, N, K):
+    rng = np.random.default_rng(7 * M + K)
+    A, W = _bf(rng, (M, K)), _bf(rng, (N, K), 1 / math.sqrt(K))
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    T.k_gemm(0, _dev(A), [_dev(W)], [N], out, N, M, K)
+    u = _ulps(_host(out), F.linear(A.astype(np.float64), W.astype(np.float64), None, 1.0),
+              _acc_err(A, W, K))
+    assert u.max() <= 1.0, (u.max(), (u > 0.5).mean())
+
+
+@pytest.mark.parametrize("M", [256, 333])
+def test_gemm_lora_kext_ulp(T, M):
+    """LoRA as a K-extension: x W^T + T B^T with T the bf16 shrink output
+    (F.linear's t_bf16 storage point), one rounding of the fp32 sum."""
+    rng = np.random.default_rng(M)
+    K, N, r = 512, 256, 16
+    A, W = _bf(rng, (M, K)), _bf(rng, (N, K), 1 / math.sqrt(K))
+    Tt, B = _bf(rng, (M, r)), _bf(rng, (N, r), 0.2)
+    out = torch.zeros(M, N, dtype=torch.bfloat16, device="cuda")
+    T.k_gemm(0, _dev(A), [_dev(W)], [N], out, N, M, K, [_dev(Tt)], [_dev(B)], r)
+    ref = A.astype(np.float64) @ W.T.astype(np.float64) + Tt.astype(np.float64) @ B.T.astype(np.float64)
+    err = _acc_err(np.concatenate([A, Tt], 1), np.concatenate([W, B], 1), K + r)
+    assert _ulps(_host(out), ref, err).max() <= 1.0
+
+
+def test_lora_shrink_ulp(T):
+    """T = bf16(s x A^T): split-K fp32 partials summed in a fixed order."""
+    rng = np.random.default_rng(5)
+    M, K, r = 300, 5120, 16
+    X, A = _bf(rng, (M, K)), _bf(rng, (r, K), 1 / math.sqrt(K))
+    out = torch.zeros(M, r, dtype=torch.bfloat16, device="cuda")
+    T.k_lora_shrink(_dev(X), M, K, _dev(A), out, r, 0.5)
+    ref = 0.5 * (X.astype(np.float64) @ A.T.astype(np.float64))
+    assert _ulps(_host(out), ref, 0.5 * _acc_err(X, A, K)).max() <= 1.0
+
+
+@pytest.mark.parametrize("S,d", [(37, 5120), (16, 4096)])
+def test_rmsnorm_ulp(T, S, d):
+    """rsqrt.approx on the GPU: <= 2 ulp of bf16 against the float64 definition."""
+    rng = np.random.default_rng(d + 1)
+    X = rng.standard_normal((S, d)).astype(np.float32)
+    g = synth.bf16_bits_to_f32(synth.f32_to_bf16_bits(_bf(rng, (d,), 0.1) + 1.0))
+    Y = torch.zeros(S, d, dtype=torch.bfloat16, device="cuda")
+    T.k_rmsnorm(torch.from_numpy(X).cuda(), _dev(g), Y, S, d, 1e-5)
+    ref = F.rmsnorm(X.astype(np.float64), g.astype(np.float64), 1e-5)
+    assert _ulps(_host(Y), ref).max() <= 2.0
+
+
+def test_gemm_silu_ulp(T):
+    """silu(g) * u with ex2.approx / rcp.approx: <= 2 ulp (G, U fp32, H bf16)."""
+    rng = np.random.default_rng(9)
+    M, K, Fd = 256, 512, 384
+    A = _bf(rng, (M, K))
+    Wg, Wu = _bf(rng, (Fd, K), 1 / math.sqrt(K)), _bf(rng, (Fd, K), 1 / math.sqrt(K))
+    out = torch.zeros(M, Fd, dtype=torch.bfloat16, device="cuda")
+    T.k_gemm(2, _dev(A), [_dev(Wg), _dev(Wu)], [Fd], out, Fd, M, K)
+    A64 = A.astype(np.float64)
+    g, u = A64 @ Wg.T.astype(np.float64), A64 @ Wu.T.astype(np.float64)
+    # accumulation error of g and u propagated through silu(g) * u (|d/dg| <= 1.1 |u|)
+    err = 1.1 * np.abs(u) * _acc_err(A, Wg, K) + np.abs(F.silu(g)) * _acc_err(A, Wu, K)
+    assert _ulps(_host(out), F.silu(g) * u, err).max() <= 2.0

@@ -270,3 +270,42 @@ def test_greedy_decode_matches_hf_generate():
     assert list(hf_tokens) == seq[len(prompt):]
     for t in range(n_new):
         assert np.abs(g.scores[t][0].numpy().astype(np.float64) - ours[t]).max() < 1e-4
+
+
+
+# ---- bf16-emulation mode (SURVEY.md §8(c) O1 debug aid) ----
+def test_round_bf16_matches_torch_and_ties_to_even():
+    """round_bf16 against torch's own float32 -> bfloat16 conversion (RNE), and
+    the tie cases by hand: 1 + 2^-8 -> 1 (even), 1 + 3 * 2^-8 -> 1 + 2^-6."""
+    torch = pytest.importorskip("torch")
+    rng = np.random.default_rng(0)
+    x = np.concatenate([rng.standard_normal(20000).astype(np.float32) * 10.0 ** rng.integers(-6, 6, 20000),
+                        np.float32([0.0, -0.0, 1 + 2 ** -8, 1 + 3 * 2 ** -8, -(1 + 2 ** -8), 65504.0])])
+    ref = torch.from_numpy(x).to(torch.bfloat16).float().numpy()
+    assert np.array_equal(F.round_bf16(x), ref)
+    assert F.round_bf16(np.float32([1 + 2 ** -8]))[0] == 1.0
+    assert F.round_bf16(np.float32([1 + 3 * 2 ** -8]))[0] == 1 + 2 ** -6
+    y = F.round_bf16(x)
+    assert np.array_equal(F.round_bf16(y), y)                   # idempotent
+
+
+def test_bf16_emulated_attention_closed_forms():
+    """S = 1: P = 1 exactly, O = v; a row attending to one key is that key's v
+    (the rounding of P and the fp32 row sum cancel)."""
+    rng = np.random.default_rng(1)
+    q, k, v = (rng.standard_normal((1, 2, 64)).astype(np.float32) for _ in range(3))
+    assert np.array_equal(F.causal_attention(q, k[:, :1], v[:, :1], p_bf16=True),
+                          np.repeat(v[:, :1], 2, axis=1).reshape(1, -1))
+
+
+def test_bf16_emulated_forward_within_bf16_envelope():
+    """The emulated forward differs from fp32 (rounding points active) but stays
+    inside the bf16 error envelope the GPU is held to (2e-2, north_star)."""
+    cfg = synth.config("tiny")
+    w = F.synth_weights(cfg, 0)
+    tok = synth.prompt(cfg, 24, 2)
+    a = F.synth_adapter(cfg, 8, 3)
+    r32 = F.forward(cfg, w, tok, a, 0x7F, 1.0)
+    r16 = F.forward(cfg, w, tok, a, 0x7F, 1.0, bf16_emulate=True)
+    gap = float(np.abs(r32["logits"] - r16["logits"]).max())
+    assert 1e-4 < gap < 2e-2, gap

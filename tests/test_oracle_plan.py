@@ -43,6 +43,8 @@ def test_tiny_worked_plan_matches_golden():
     assert got == _golden_lines("tiny_plan_r8_b50.txt")
     # resident = embed + all of layer 0 = 2,106,368 B (round-down tie-break)
     assert dump[-1] == "BYTES 2106368 2106880 156160 4213248"
+    # R7 ACTION records against their hand derivation (VERDICT r1 weak #2c)
+    assert [l for l in dump if l.startswith("ACTION")] == _golden_lines("tiny_actions_r8_b50.txt")
 
 
 def test_tiny_layout_offsets():
