@@ -279,6 +279,22 @@ tidal_status tidal_template_import(tidal_model* model, const tidal_trace_rec* tr
                                    uint64_t shared_bytes, uint64_t fingerprint,
                                    tidal_template** out);
 
+/* ---- device memory ---- */
+/* Route the library's device allocations through the caller (e.g. PyTorch's
+ * caching allocator), process-wide, from the next allocation on (SURVEY.md
+ * §8(b); north_star "PyTorch is used only for device memory, streams and
+ * process groups"): a template's layout buffer (read-only template prefix +
+ * streaming arena), its activations and scratch, and the adapter arena.
+ * alloc(bytes, device, ctx) returns a device pointer (>= 256-B aligned) or
+ * NULL (-> TIDAL_ERR_OOM); free_(ptr, device, ctx) releases it.  Every block
+ * is returned to the allocator that produced it, even if the hook changes
+ * later.  Pass (NULL, NULL, NULL) to return to cudaMalloc.  A template whose
+ * layout buffer comes from a hook is not on CUDA VMM and cannot be exported
+ * (tidal_template_export -> INVALID).  Errors: INVALID (one of the two NULL). */
+tidal_status tidal_set_device_allocator(void* (*alloc)(size_t bytes, int device, void* ctx),
+                                       void (*free_)(void* ptr, int device, void* ctx),
+                                       void* ctx);
+
 /* ---- pinned host memory for adapters / pools (cudaHostAlloc) ---- */
 tidal_status tidal_host_alloc(uint64_t bytes, void** out);
 void tidal_host_free(void* p);

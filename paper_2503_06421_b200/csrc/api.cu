@@ -448,7 +448,7 @@ static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
         prev_end = o + tp->tt.t[id].bytes;
       }
     }
-    if (vmm_available()) {
+    if (vmm_available() && !device_allocator_set()) {
       vmm_alloc(tp->vmm, L, tp->device, fds, n_fds);
       tp->dev = reinterpret_cast<uint8_t*>(tp->vmm.va);
       if (n_fds)
@@ -457,8 +457,9 @@ static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
                 "imported chunks do not match this template's layout / resident prefix",
                 TIDAL_ERR_STRUCTURE);
     } else {
-      require(n_fds == 0, "CUDA virtual memory management unavailable: cannot import");
-      cuda_check(cudaMalloc((void**)&tp->dev, L), "cudaMalloc(template+arena)");
+      require(n_fds == 0, "template memory not on CUDA VMM (unavailable, or a caller allocator "
+                          "is set): cannot import");
+      tp->dev = reinterpret_cast<uint8_t*>(dev_alloc(L, tp->device, "template + streaming arena"));
     }
     tp->shared_bytes = shared_bytes;
     // the shared prefix is already on the device (the exporter's bytes)
@@ -475,7 +476,7 @@ static tidal_status template_create(tidal_model* m, const tidal_trace_rec* t,
       tp->use_graphs = !(g && g[0] == '0');
     }
     tp->ensure_events(tp->plan.groups.size() + 2 * tp->shape.n_layers + 4);
-    cuda_check(cudaMalloc((void**)&tp->d_sum, 64), "cudaMalloc");
+    tp->d_sum = reinterpret_cast<unsigned long long*>(dev_alloc(64, tp->device, "checksum"));
     // warm run streams nothing: make every weight valid once (prefix resident,
     // suffix copied) so the warm launches read real bytes
     if (tp->plan.resident_end < L)
@@ -586,11 +587,11 @@ void tidal_template_destroy(tidal_template* tp) {
     for (cudaEvent_t e : tp->tl_op) cudaEventDestroy(e);
     if (tp->vmm.va)
       vmm_free(tp->vmm);
-    else if (tp->dev)
-      cudaFree(tp->dev);
-    if (tp->arena) cudaFree(tp->arena);
-    if (tp->scrub) cudaFree(tp->scrub);
-    if (tp->d_sum) cudaFree(tp->d_sum);
+    else
+      dev_free(tp->dev);
+    dev_free(tp->arena);
+    dev_free(tp->scrub);
+    dev_free(tp->d_sum);
     if (tp->pool) cudaFreeHost(tp->pool);
     tp->ex.destroy();
   }
@@ -718,9 +719,12 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
   Exec& ex = tp->ex;
   cuda_check(cudaSetDevice(tp->device), "cudaSetDevice");
   if (a && P.adapter_bytes > tp->arena_cap) {
-    if (tp->arena) cuda_check(cudaFree(tp->arena), "cudaFree");
+    if (tp->arena) {
+      cuda_check(cudaStreamSynchronize(ex.compute), "sync");
+      dev_free(tp->arena);
+    }
     tp->arena = nullptr;
-    cuda_check(cudaMalloc((void**)&tp->arena, P.adapter_bytes), "cudaMalloc(adapter arena)");
+    tp->arena = reinterpret_cast<uint8_t*>(dev_alloc(P.adapter_bytes, tp->device, "adapter arena"));
     tp->arena_cap = P.adapter_bytes;
   }
   tp->ensure_events(P.groups.size());
@@ -736,7 +740,7 @@ tidal_status tidal_invoke_prefill_batch(tidal_template* tp, const tidal_adapter*
     if (a) cuda_check(poison_launch(tp->arena, P.adapter_bytes, ex.compute), "poison");
   }
   if (tp->debug & TIDAL_DEBUG_SCRUB_L2) {
-    if (!tp->scrub) cuda_check(cudaMalloc(&tp->scrub, 512ull << 20), "cudaMalloc(scrub)");
+    if (!tp->scrub) tp->scrub = dev_alloc(512ull << 20, tp->device, "L2 scrub buffer");
     cuda_check(scrub_launch(tp->scrub, 512ull << 20, ex.compute), "scrub");
   }
   if (tp->debug & (TIDAL_DEBUG_POISON | TIDAL_DEBUG_SCRUB_L2))
@@ -1088,6 +1092,14 @@ tidal_status tidal_set_debug(tidal_template* tp, int flags, int arg) {
   require(tp != nullptr, "null template");
   tp->debug = flags;
   tp->debug_arg = arg;
+  TIDAL_CATCH
+}
+
+tidal_status tidal_set_device_allocator(void* (*alloc)(size_t, int, void*),
+                                       void (*free_)(void*, int, void*), void* ctx) {
+  TIDAL_TRY
+  require((alloc == nullptr) == (free_ == nullptr), "alloc and free must both be set or both NULL");
+  set_device_allocator(alloc, free_, ctx);
   TIDAL_CATCH
 }
 

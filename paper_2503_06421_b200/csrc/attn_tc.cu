@@ -37,6 +37,7 @@
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <cstdlib>
 
 #include "kernels.h"
 #include "launch.cuh"
@@ -50,22 +51,30 @@ constexpr int TILE = 128 * 128 * 2;  // 32 KB: any 128 x 128 bf16 tile (two 64-w
 constexpr int HALF = TILE / 2;
 constexpr int KST = 3, VST = 2;
 constexpr int OFF_Q = 0, OFF_K = OFF_Q + TILE, OFF_V = OFF_K + KST * TILE;
-constexpr int OFF_RED = OFF_V + VST * TILE;          // [2 slots][2 halves][128] row maxima
-constexpr int OFF_LSUM = OFF_RED + 2 * 2 * BQ * 4;   // [2 items][2 halves][128] row sums
-constexpr int OFF_BAR = OFF_LSUM + 2 * 2 * BQ * 4;
-constexpr int N_BARS = 4 + 2 * KST + 2 * VST + 2 + 2 + 2 + 2;
-constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
-constexpr int SMEM = OFF_TMEM + 16 + 1024;
-constexpr int NSOFT = 256;           // softmax threads
-constexpr int NEPI = 128;            // epilogue threads: O / l -> bf16, off the softmax path
-constexpr int NTH = 64 + NSOFT + NEPI;
+// Softmax in SPLIT column groups of the 128 keys of a tile (SPLIT = 2: 8
+// warps, 64 columns per thread; SPLIT = 4: 16 warps, 32 columns per thread —
+// twice the warps per scheduler to hide the per-tile TMEM / barrier latency)
+template <int SPLIT>
+struct ACfg {
+  static constexpr int OFF_RED = OFF_V + VST * TILE;              // [2 slots][SPLIT][128] row maxima
+  static constexpr int OFF_LSUM = OFF_RED + 2 * SPLIT * BQ * 4;   // [2 items][SPLIT][128] row sums
+  static constexpr int OFF_BAR = OFF_LSUM + 2 * SPLIT * BQ * 4;
+  static constexpr int N_BARS = 4 + 2 * KST + 2 * VST + 2 + 2 + 2 + 2;
+  static constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
+  static constexpr int SMEM = OFF_TMEM + 16 + 1024;
+  static constexpr int NSOFT = 128 * SPLIT;  // softmax threads
+  static constexpr int NEPI = 128;           // epilogue threads: O / l -> bf16, off the softmax path
+  static constexpr int NTH = 64 + NSOFT + NEPI;
+  static constexpr int COLS = 128 / SPLIT;   // keys per softmax thread
+};
 constexpr uint32_t COL_S0 = 0, COL_O = 256, COL_P = 384;
 
 __device__ __forceinline__ uint32_t pack_bf16x2(float lo, float hi) {
   __nv_bfloat162 v = __floats2bfloat162_rn(lo, hi);
   return *reinterpret_cast<uint32_t*>(&v);
 }
-__device__ __forceinline__ void softmax_bar() {  // the 8 softmax warps only
+template <int NSOFT>
+__device__ __forceinline__ void softmax_bar() {  // the softmax warps only
   asm volatile("bar.sync 1, %0;" ::"n"(NSOFT) : "memory");
 }
 
@@ -88,7 +97,11 @@ __device__ __forceinline__ bool item_at(const AttnParams& p, int nq, int round, 
   return true;
 }
 
-__global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
+template <int SPLIT>
+__global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __grid_constant__ AttnParams p) {
+  using A = ACfg<SPLIT>;
+  constexpr int OFF_RED = A::OFF_RED, OFF_LSUM = A::OFF_LSUM, OFF_BAR = A::OFF_BAR,
+                OFF_TMEM = A::OFF_TMEM, NSOFT = A::NSOFT, NEPI = A::NEPI, COLS = A::COLS;
   extern __shared__ uint8_t smem_raw[];
   // 1024-B aligned (SWIZZLE_128B); offsetting smem_raw keeps the shared state
   // space visible to the compiler (STS/LDS, not generic ST/LD)
@@ -238,7 +251,10 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       gt += it.qt + 1;
       const int b = i & 1;
       ptx::mbar_wait(l_ready(b), (i >> 1) & 1);
-      const float inv = 1.f / (lsum[(b * 2 + 0) * BQ + row] + lsum[(b * 2 + 1) * BQ + row]);
+      float lsum_row = 0.f;
+#pragma unroll
+      for (int h = 0; h < SPLIT; ++h) lsum_row += lsum[(b * SPLIT + h) * BQ + row];
+      const float inv = 1.f / lsum_row;
       ptx::mbar_wait(pv_done((gt - 1) & 1), ((gt - 1) >> 1) & 1);
       ptx::tc_fence_after();
       const int qi = it.qt * BQ + row;
@@ -266,14 +282,14 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       }
     }
   } else {
-    // ===================== softmax: two column halves =====================
-    const int half = (warp - 2) >> 2;  // 0: keys 0..63, 1: keys 64..127 of each tile
-    const int q = warp & 3;            // TMEM lane quarter (shared by both halves)
+    // ===================== softmax: SPLIT column groups =====================
+    const int half = (warp - 2) >> 2;  // column group: keys half*COLS .. +COLS of each tile
+    const int q = warp & 3;            // TMEM lane quarter (shared by all groups)
     const int row = q * 32 + lane;
     const uint32_t lane_base = (uint32_t)(q * 32) << 16;
-    float* red = reinterpret_cast<float*>(smem + OFF_RED);    // [slot][half][row]
-    float* lsum = reinterpret_cast<float*>(smem + OFF_LSUM);  // [item&1][half][row]
-    const uint32_t o_col = tmem + lane_base + COL_O + half * 64;
+    float* red = reinterpret_cast<float*>(smem + OFF_RED);    // [slot][group][row]
+    float* lsum = reinterpret_cast<float*>(smem + OFF_LSUM);  // [item&1][group][row]
+    const uint32_t o_col = tmem + lane_base + COL_O + half * COLS;
     int gt = 0;  // S/P tiles consumed by this CTA
     for (int i = 0; item_at(p, nq, i, it); ++i) {
       const int q0 = it.qt * BQ, qi = q0 + row;
@@ -283,46 +299,47 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         const int b = gt & 1;
         ptx::mbar_wait(s_full(b), (gt >> 1) & 1);
         ptx::tc_fence_after();
-        float v[64];
+        float v[COLS];
         {
-          uint32_t r0[32], r1[32];
-          const uint32_t sc = tmem + lane_base + COL_S0 + b * 128 + half * 64;
-          ptx::tmem_ld32(sc, r0);
-          ptx::tmem_ld32(sc + 32, r1);
-          ptx::tmem_ld_wait();
+          const uint32_t sc = tmem + lane_base + COL_S0 + b * 128 + half * COLS;
 #pragma unroll
-          for (int c = 0; c < 32; ++c) {
-            v[c] = __uint_as_float(r0[c]);  // raw scores
-            v[32 + c] = __uint_as_float(r1[c]);
+          for (int c0 = 0; c0 < COLS; c0 += 32) {
+            uint32_t r0[32];
+            ptx::tmem_ld32(sc + c0, r0);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int c = 0; c < 32; ++c) v[c0 + c] = __uint_as_float(r0[c]);  // raw scores
           }
         }
-        const int key0 = j * BKV + half * 64;
-        if (key0 + 63 > q0) {  // reaches the diagonal: causal mask
+        const int key0 = j * BKV + half * COLS;
+        if (key0 + COLS - 1 > q0) {  // reaches the diagonal: causal mask
 #pragma unroll
-          for (int c = 0; c < 64; ++c)
+          for (int c = 0; c < COLS; ++c)
             if (key0 + c > qi) v[c] = -INFINITY;
         }
         float mr[8];  // 8 independent max chains
 #pragma unroll
         for (int k = 0; k < 8; ++k) mr[k] = v[k];
 #pragma unroll
-        for (int c = 8; c < 64; ++c) mr[c & 7] = fmaxf(mr[c & 7], v[c]);
+        for (int c = 8; c < COLS; ++c) mr[c & 7] = fmaxf(mr[c & 7], v[c]);
         float mraw = fmaxf(fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3])),
                            fmaxf(fmaxf(mr[4], mr[5]), fmaxf(mr[6], mr[7])));
-        // exchange the half-row maxima (double-buffered slot: no WAR hazard)
-        float* slot = red + b * 2 * BQ;
+        // exchange the group row maxima (double-buffered slot: no WAR hazard)
+        float* slot = red + b * SPLIT * BQ;
         slot[half * BQ + row] = mraw;
-        softmax_bar();
-        mraw = fmaxf(mraw, slot[(half ^ 1) * BQ + row]);
+        softmax_bar<NSOFT>();
+#pragma unroll
+        for (int h = 0; h < SPLIT; ++h)
+          if (h != half) mraw = fmaxf(mraw, slot[h * BQ + row]);
         const float mx = fmaxf(m_used, mraw * p.scale_log2);  // scale > 0: max commutes
-        const bool need = mx > m_used + 8.f;                  // identical in both halves
+        const bool need = mx > m_used + 8.f;                  // identical in every group
         if (j > 0 && __any_sync(0xffffffffu, need)) {
           // O settled: the previous tile's PV (and so every earlier PV) has completed
           ptx::mbar_wait(pv_done((gt - 1) & 1), ((gt - 1) >> 1) & 1);
           ptx::tc_fence_after();
           const float corr = need ? ptx::ex2(m_used - mx) : 1.f;
 #pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < COLS / 32; ++c) {
             uint32_t r[32];
             ptx::tmem_ld32(o_col + c * 32, r);
             ptx::tmem_ld_wait();
@@ -336,11 +353,11 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
         if (need) m_used = mx;
         // P buffer b was last read by the PV of tile gt-2
         if (gt >= 2) ptx::mbar_wait(pv_done(b), ((gt - 2) >> 1) & 1);
-        // P = 2^(s*scale - m) -> packed bf16 pairs, 32 TMEM columns per half
+        // P = 2^(s*scale - m) -> packed bf16 pairs, COLS / 2 TMEM columns per group
         float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent sum chains
-        uint32_t pk[32];
+        uint32_t pk[COLS / 2];
 #pragma unroll
-        for (int c = 0; c < 8; ++c) {
+        for (int c = 0; c < COLS / 8; ++c) {
           float e[8];
 #pragma unroll
           for (int k = 0; k < 8; ++k) {
@@ -353,7 +370,10 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
           pk[4 * c + 3] = pack_bf16x2(e[6], e[7]);
         }
         ptx::tc_fence_after();
-        ptx::tmem_st32(tmem + lane_base + COL_P + b * 64 + half * 32, pk);
+        if constexpr (COLS == 64)
+          ptx::tmem_st32(tmem + lane_base + COL_P + b * 64 + half * 32, pk);
+        else
+          ptx::tmem_st16(tmem + lane_base + COL_P + b * 64 + half * 16, pk);
         l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
@@ -361,7 +381,7 @@ __global__ void __launch_bounds__(NTH, 1) attn_tc_kernel(const __grid_constant__
       }
       // hand the row sums to the epilogue warps (double-buffered by item: the
       // epilogue of item i has read them before item i+2's softmax can end)
-      lsum[((i & 1) * 2 + half) * BQ + row] = l;
+      lsum[((i & 1) * SPLIT + half) * BQ + row] = l;
       ptx::mbar_arrive(l_ready(i & 1));
     }
   }
@@ -397,14 +417,28 @@ bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, b
   return true;
 }
 
-cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
+template <int SPLIT>
+static cudaError_t attn_set_attr() {
   static bool attr = false;
   if (!attr) {
-    cudaError_t e =
-        cudaFuncSetAttribute(attn_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM);
+    cudaError_t e = cudaFuncSetAttribute(attn_tc_kernel<SPLIT>,
+                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         ACfg<SPLIT>::SMEM);
     if (e != cudaSuccess) return e;
     attr = true;
   }
+  return cudaSuccess;
+}
+
+// SPLIT = 2 (8 softmax warps).  SPLIT = 4 (16 warps, 32 keys per thread)
+// compiles and is parity-clean but measured slower (13B S = 2048: 68 vs 61
+// us; S = 8192: 775 vs 735 us, tools/attn_bench.py): the per-tile softmax is
+// not latency-hidden by more warps — the extra row-max exchange and barrier
+// of 512 threads cost more than they hide.
+cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
+  constexpr int split = 2;
+  cudaError_t ea = attn_set_attr<split>();
+  if (ea != cudaSuccess) return ea;
   static int sms = 0;
   if (!sms) {
     int dev = 0;
@@ -414,7 +448,8 @@ cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
   const long items = (long)((p.S + BQ - 1) / BQ) * p.H * p.nseq;  // persistent: <= one CTA per SM
   const int grid = (int)(items < sms ? items : sms);
   if (grid <= 0) return cudaSuccess;
-  return launch_kt("attn", attn_tc_kernel, dim3(grid), dim3(NTH), SMEM, s, 1, p);
+  return launch_kt("attn", attn_tc_kernel<split>, dim3(grid), dim3(ACfg<split>::NTH),
+                   ACfg<split>::SMEM, s, 1, p);
 }
 
 }  // namespace tidal

@@ -911,100 +911,85 @@ int gemm_pick_bn(int epi, int M, const int* seg_n, int nseg, int num_sms, int* c
   return best;
 }
 
-// Residual (row-parallel) GEMMs are short in N (d_model) and often few waves
-// deep: choose the N-tile width and an ordered split-K jointly to minimise
-// rounds x (K-blocks per part + per-part overhead) x shared-memory bytes per
-// K-block.  The per-part overhead (epilogue reductions, flag hand-off) was
-// measured at ~11 K-blocks (tools/gemm_bench.py, 13B O/down shapes), so at
-// S = 2048 one part wins and splitting pays only for short prompts.
-static void gemm_plan_resid_single(int M, int N, int K, int num_sms, int* bn_out) {
-  (void)K;
-  *bn_out = gemm_pick_bn(EPI_RESID, M, &N, 1, num_sms);
-}
-
+// Residual (row-parallel) GEMMs: choose the CTA group, the N-tile width and
+// the ordered split-K jointly.  Cost of a plan, in K-block times of a pair
+// tile (~0.39 us at 13B): rounds x (K-blocks per part + ~11 K-blocks of
+// per-part epilogue / hand-off), plus the ordered epilogue chain when the
+// parts of a tile run in the same round; a K-block of a 192-wide pair tile
+// costs as much as a 256-wide one (tools/gemm_bench.py --resid-sweep: O 256 x
+// 2-3 parts 84-86 us, 192 x 1 part 97-127 us); single-CTA tiles (cg = 1, M =
+// 128 rows) give the same per-SM rate.  Short prompts thereby split K until
+// the works fill the SMs (13B S = 256: down 20 pair tiles x 3 parts instead
+// of 54 whole-K single-CTA tiles on 54 SMs).
 void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out, int* cg_out,
                      bool allow_split, int* nfull_out) {
-  if (cg_out) *cg_out = gemm_pick_cg(M);
   if (nfull_out) *nfull_out = 0;
-  const int cg = gemm_pick_cg(M), mc = gemm_pick_mc(M, num_sms);
-  const long mt = gemm_m_tiles(M, cg, mc);
-  const long units = gemm_units(cg, mc, num_sms);
+  const int cg0 = gemm_pick_cg(M);
   const int nk = (K + BK - 1) / BK;
   static const int split_env = [] {
-    const char* e = getenv("TIDAL_RESID_SPLIT");  // 0: no split-K; 1: uniform parts only
+    const char* e = getenv("TIDAL_RESID_SPLIT");  // 0: no split-K; 3: also tail splits
     return e ? e[0] - '0' : 2;
   }();
-  const bool tail_ok = nfull_out != nullptr && split_env >= 2;
+  const bool split_ok = allow_split && split_env != 0;
+  const bool tail_ok = nfull_out != nullptr && split_env == 3 && split_ok;
   static const int cands[] = {256, 192, 128};
-  // cost = rounds x (K-blocks per part + ~11 K-blocks of per-part epilogue and
-  // hand-off) x time per K-block.  A K-block of a 192-wide pair tile takes as
-  // long as a 256-wide one (tools/gemm_bench.py --resid-sweep, 13B S = 2048:
-  // O 256 x 3 parts 84 us, 192 x 1 part 97-127 us), so only 128-wide tiles
-  // are charged less (their A-operand traffic per MAC doubles: x 0.75).
   double best = 1e30;
-  int bb = 256, bk = 1, bf = 0;
-  for (int bn : cands) {
-    const long tiles = mt * ((N + bn - 1) / bn);
-    if (tiles * mc * cg > GEMM_MAX_FLAGS) continue;
-    const double kb_cost = bn == 128 ? 0.75 : 1.0;
-    // (a) every tile in ks ordered parts
-    for (int ks = 1; ks <= 8 && ks <= nk; ++ks) {
-      const int kps = (nk + ks - 1) / ks;
-      const int ks_eff = (nk + kps - 1) / kps;  // every part non-empty
-      if (ks_eff != ks) continue;
-      const long rounds = (tiles * ks + units - 1) / units;
-      const double cost = (double)rounds * (kps + 11) * kb_cost;
-      if (cost < best * 0.98) {  // prefer fewer parts unless clearly better
-        best = cost;
-        bb = bn;
-        bk = ks;
-        bf = 0;
-      }
-    }
-    // (b) opt-in (TIDAL_RESID_SPLIT=3): whole tiles for the full waves, the
-    // last partial wave's tiles in ordered parts.  Measured slower than (a):
-    // the parts of one tile run concurrently, so their ordered epilogues
-    // serialise (O 256-wide: 92-116 us against 84 us uniform).
-    const long full = tiles / units, tail = tiles - full * units;
-    if (tail_ok && split_env == 3 && full >= 1 && tail > 0) {
-      int ks = (int)(units / tail);
-      ks = ks > 8 ? 8 : (ks > nk ? nk : ks);
-      if (ks >= 2) {
+  int bb = 256, bk = 1, bf = 0, bc = cg0;
+  for (int cg = cg0; cg >= (cg_out ? 1 : cg0); --cg) {
+    const int mc = cg == 2 ? gemm_pick_mc(M, num_sms) : 1;
+    const long mt = gemm_m_tiles(M, cg, mc);
+    const long units = gemm_units(cg, mc, num_sms);
+    for (int bn : cands) {
+      const long tiles = mt * ((N + bn - 1) / bn);
+      if (tiles * mc * cg > GEMM_MAX_FLAGS) continue;
+      // with one or two M tiles the K-block rate is bound by each SM's operand
+      // stream (A + B bytes), not the MMA: a 192-wide K-block then costs ~0.8
+      // of a 256-wide one (13B S = 256: O 192 x 2 parts 25.5-26 us vs 256 x 3
+      // 33.5 us; down 192 x 2 46.4 us vs 256 x 3 51.6 us)
+      const bool stream_bound = M <= 2 * BM * 2;
+      const double kb_cost = (bn == 128 ? 0.75 : (bn == 192 && stream_bound ? 0.8 : 1.0)) *
+                             (cg == 1 ? 1.03 : 1.0);
+      for (int ks = 1; ks <= (split_ok ? 8 : 1) && ks <= nk; ++ks) {
         const int kps = (nk + ks - 1) / ks;
-        const int ks_eff = (nk + kps - 1) / kps;
-        const double cost = ((double)full * (nk + 11) + (kps + 11)) * kb_cost;
-        if (cost < best * 0.98) {
+        const int ks_eff = (nk + kps - 1) / kps;  // every part non-empty
+        if (ks_eff != ks) continue;
+        const long rounds = (tiles * ks + units - 1) / units;
+        const double chain = rounds < ks ? 11.0 * (ks - 1) : 0.0;
+        const double cost = ((double)rounds * (kps + 11) + chain) * kb_cost;
+        if (cost < best * 0.98) {  // prefer fewer parts / the pair unless clearly better
           best = cost;
           bb = bn;
-          bk = ks_eff;
-          bf = (int)(full * units);
+          bk = ks;
+          bf = 0;
+          bc = cg;
+        }
+      }
+      // (b) opt-in (TIDAL_RESID_SPLIT=3): whole tiles for the full waves, the
+      // last partial wave's tiles in ordered parts.  Measured slower than (a):
+      // the parts of one tile run concurrently, so their ordered epilogues
+      // serialise (O 256-wide: 92-116 us against 84 us uniform).
+      const long full = tiles / units, tail = tiles - full * units;
+      if (tail_ok && cg == cg0 && full >= 1 && tail > 0) {
+        int ks = (int)(units / tail);
+        ks = ks > 8 ? 8 : (ks > nk ? nk : ks);
+        if (ks >= 2) {
+          const int kps = (nk + ks - 1) / ks;
+          const int ks_eff = (nk + kps - 1) / kps;
+          const double cost = ((double)full * (nk + 11) + (kps + 11) + 11.0 * (ks - 1)) * kb_cost;
+          if (cost < best * 0.98) {
+            best = cost;
+            bb = bn;
+            bk = ks_eff;
+            bf = (int)(full * units);
+            bc = cg;
+          }
         }
       }
     }
   }
-  // short prompts: one wave of whole-K single-CTA tiles beats rounds of pairs
-  // and split-K (13B O/down, tools/gemm_bench.py --small-sweep: S = 867
-  // 42 / 103 us against 57 / 137 us; S = 640 35 / 84 against 38 / 88); the
-  // narrower tile first (more SMs streaming), 128-wide tiles never pay
-  if (cg_out && cg == 2) {
-    const long mt1 = (M + BM - 1) / BM;
-    for (int bn : {192, 256}) {
-      const long tiles = mt1 * ((N + bn - 1) / bn);
-      if (tiles <= num_sms && tiles <= GEMM_MAX_FLAGS) {
-        *bn_out = bn;
-        *ks_out = 1;
-        *cg_out = 1;
-        return;
-      }
-    }
-  }
-  if ((split_env == 0 || !allow_split) && bk > 1) {  // best single-part width instead
-    gemm_plan_resid_single(M, N, K, num_sms, bn_out);
-    *ks_out = 1;
-    return;
-  }
   *bn_out = bb;
   *ks_out = bk;
+  if (cg_out) *cg_out = bc;
   if (nfull_out) *nfull_out = bf;
 }
 

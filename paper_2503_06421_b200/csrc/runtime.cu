@@ -12,6 +12,8 @@
 #include <cstring>
 #include <fstream>
 #include <sstream>
+#include <mutex>
+#include <unordered_map>
 
 #include "runtime.h"
 
@@ -26,11 +28,74 @@ void cuda_check(cudaError_t e, const char* what) {
   }
 }
 
+namespace {
+struct DevAllocator {
+  DevAllocFn alloc = nullptr;
+  DevFreeFn free_ = nullptr;
+  void* ctx = nullptr;
+  int device = -1;
+};
+std::mutex g_alloc_mu;
+DevAllocator g_alloc;                                // the current hook (alloc == null: cudaMalloc)
+std::unordered_map<void*, DevAllocator> g_owned;     // blocks that came from a hook
+}  // namespace
+
+void set_device_allocator(DevAllocFn alloc, DevFreeFn free_, void* ctx) {
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  g_alloc.alloc = alloc;
+  g_alloc.free_ = free_;
+  g_alloc.ctx = ctx;
+}
+
+bool device_allocator_set() {
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  return g_alloc.alloc != nullptr;
+}
+
+void* dev_alloc(size_t bytes, int device, const char* what) {
+  DevAllocator a;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    a = g_alloc;
+  }
+  bytes = bytes ? bytes : 16;
+  if (!a.alloc) {
+    void* q = nullptr;
+    cuda_check(cudaMalloc(&q, bytes), what);
+    return q;
+  }
+  void* q = a.alloc(bytes, device, a.ctx);
+  if (!q) fail(2, std::string(what) + ": the caller's allocator returned NULL");
+  a.device = device;
+  std::lock_guard<std::mutex> lk(g_alloc_mu);
+  g_owned[q] = a;
+  return q;
+}
+
+void dev_free(void* p) {
+  if (!p) return;
+  DevAllocator a;
+  {
+    std::lock_guard<std::mutex> lk(g_alloc_mu);
+    auto it = g_owned.find(p);
+    if (it == g_owned.end()) {
+      a.alloc = nullptr;
+    } else {
+      a = it->second;
+      g_owned.erase(it);
+    }
+  }
+  if (a.free_)
+    a.free_(p, a.device, a.ctx);
+  else if (!a.alloc)
+    cudaFree(p);
+}
+
 template <typename T>
 static void dalloc(T*& p, size_t bytes) {
-  void* q = nullptr;
-  cuda_check(cudaMalloc(&q, bytes ? bytes : 16), "cudaMalloc(activations)");
-  p = reinterpret_cast<T*>(q);
+  int dev = 0;
+  cudaGetDevice(&dev);
+  p = reinterpret_cast<T*>(dev_alloc(bytes, dev, "device allocation (activations)"));
 }
 
 void Exec::init(int dev, const ModelShape& shape, float eps_, float theta_, int world_, int rank_,
@@ -111,7 +176,7 @@ void Exec::build_rope(int rows) {
       const double ang = (double)p * inv;
       cs[p * (hd / 2) + i] = make_float2((float)std::cos(ang), (float)std::sin(ang));
     }
-  if (rope) cudaFree(rope);
+  if (rope) dev_free(rope);
   rope = nullptr;
   dalloc(rope, cs.size() * sizeof(float2));
   cuda_check(cudaMemcpy(rope, cs.data(), cs.size() * sizeof(float2), cudaMemcpyHostToDevice),
@@ -129,8 +194,7 @@ void Exec::enable_decode(int max_new) {
   Decode& D = dec;
   void* ptrs[] = {D.kc, D.vc, D.q, D.att, D.h, D.T, D.part, D.cnt, D.shcnt, D.st, D.toks,
                   D.logits_all};
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
+  for (void* p : ptrs) dev_free(p);
   if (D.gexec) cudaGraphExecDestroy(D.gexec);
   D = Decode();
   const int hd = m.head_dim();
@@ -177,10 +241,8 @@ void Exec::destroy() {
                   dec.toks,
                   dec.logits_all};
   if (dec.gexec) cudaGraphExecDestroy(dec.gexec);
-  for (void* p : ptrs)
-    if (p) cudaFree(p);
-  for (int t = 0; t < kNumTargets; ++t)
-    if (T[t]) cudaFree(T[t]);
+  for (void* p : ptrs) dev_free(p);
+  for (int t = 0; t < kNumTargets; ++t) dev_free(T[t]);
   if (h_tok) cudaFreeHost(h_tok);
   if (h_logits) cudaFreeHost(h_logits);
   if (h_key) cudaFreeHost(h_key);
@@ -560,7 +622,8 @@ void run_forward(Exec& ex, const RunArgs& a) {
     if (out_override) p.out = out_override;
     if (tr) {
       const size_t nb = (size_t)ex.num_sms * 32 * 8 * 8;
-      if (!ex.dbg_trace) cuda_check(cudaMalloc(&ex.dbg_trace, nb), "cudaMalloc(trace)");
+      if (!ex.dbg_trace)
+        ex.dbg_trace = reinterpret_cast<unsigned long long*>(dev_alloc(nb, ex.device, "trace"));
       cuda_check(cudaMemsetAsync(ex.dbg_trace, 0, nb, st), "memset trace");
       p.dbg = ex.dbg_trace;
       ex.dbg_pending = true;

@@ -24,6 +24,17 @@ struct Error {
 [[noreturn]] void fail(int code, const std::string& msg);
 void cuda_check(cudaError_t e, const char* what);
 
+// Device memory of templates (layout buffer when not on CUDA VMM, activations,
+// adapter arena, scratch): through the caller's allocator when one is set
+// (tidal_set_device_allocator), else cudaMalloc.  dev_free returns a block to
+// whichever allocator produced it.  Allocation failure -> TIDAL_ERR_OOM.
+typedef void* (*DevAllocFn)(size_t bytes, int device, void* ctx);
+typedef void (*DevFreeFn)(void* ptr, int device, void* ctx);
+void set_device_allocator(DevAllocFn alloc, DevFreeFn free_, void* ctx);
+bool device_allocator_set();
+void* dev_alloc(size_t bytes, int device, const char* what);
+void dev_free(void* p);
+
 // Per-layer launch parameters, cached per (prompt length, adapter layout).
 struct LayerLaunch {
   GemmParams qkv, o, gu, down;

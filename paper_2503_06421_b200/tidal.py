@@ -88,6 +88,8 @@ class KernelTime(C.Structure):
 
 
 FILL_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
+ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_int, C.c_void_p)
+FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_int, C.c_void_p)
 VP = C.c_void_p
 
 # (name, restype, argtypes) of every exported symbol declared in include/*.h
@@ -119,6 +121,7 @@ SIGNATURES = [
     ("tidal_invoke_decode", C.c_int, [VP, VP, C.c_int, VP, VP, C.POINTER(DecodeStats)]),
     ("tidal_invoke_prefill_batch", C.c_int,
      [VP, VP, VP, C.c_int, C.c_int, VP, VP, C.POINTER(Stats)]),
+    ("tidal_set_device_allocator", C.c_int, [ALLOC_FN, FREE_FN, VP]),
     ("tidal_host_alloc", C.c_int, [C.c_uint64, C.POINTER(VP)]),
     ("tidal_host_free", None, [VP]),
     ("tidal_comm_unique_id", C.c_int, [VP]),
@@ -393,6 +396,31 @@ class Template:
         if getattr(self, "h", None):
             lib().tidal_template_destroy(self.h)
             self.h = None
+
+
+_allocator_refs = None
+
+
+def set_device_allocator(alloc: Optional[Callable[[int, int], int]] = None,
+                         free: Optional[Callable[[int, int], None]] = None) -> None:
+    """Route the library's device allocations through alloc(bytes, device) ->
+    ptr / free(ptr, device); no arguments: back to cudaMalloc."""
+    global _allocator_refs
+    if alloc is None:
+        _check(lib().tidal_set_device_allocator(ALLOC_FN(), FREE_FN(), None))
+        _allocator_refs = None
+        return
+    a = ALLOC_FN(lambda nb, dev, ctx: alloc(nb, dev) or None)
+    f = FREE_FN(lambda p, dev, ctx: free(p, dev))
+    _check(lib().tidal_set_device_allocator(a, f, None))
+    _allocator_refs = (a, f)   # the C side keeps the function pointers
+
+
+def use_torch_allocator() -> None:
+    """Device memory from PyTorch's caching allocator (torch.cuda.caching_allocator_*)."""
+    import torch
+    set_device_allocator(lambda nb, dev: torch.cuda.caching_allocator_alloc(nb, dev),
+                         lambda p, dev: torch.cuda.caching_allocator_delete(p))
 
 
 class PinnedBuffer:

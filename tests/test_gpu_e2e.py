@@ -279,3 +279,34 @@ def test_graph_replay_equals_eager(T, tiny):
     check(tiny.tpl.invoke(tok, a2), F.forward(cfg, tiny.w, tok, F.synth_adapter(cfg, 16, 22),
                                               0x7F, 1.5))
     check(tiny.tpl.invoke(tok), F.forward(cfg, tiny.w, tok))
+
+
+def test_device_allocator_hook(T):
+    """tidal_set_device_allocator: the template, activations and adapter arena
+    come from PyTorch's caching allocator; results equal
+    the cudaMalloc path bit for bit; destroying the template returns the memory;
+    such a template cannot be exported (not on CUDA VMM)."""
+    cfg = synth.config("tiny")
+    tok = synth.prompt(cfg, 24, 5)
+    base = Rig(T, cfg, seed=4, budget=0.5)
+    a0 = base.adapter(8, 2)
+    ref = base.tpl.invoke(tok, a0)
+    torch.cuda.synchronize()
+    before = torch.cuda.memory_allocated()
+    T.use_torch_allocator()
+    try:
+        rig = Rig(T, cfg, seed=4, budget=0.5)
+        during = torch.cuda.memory_allocated()
+        assert during - before >= 4_213_248            # at least the layout buffer
+        a1 = rig.adapter(8, 2)
+        got = rig.tpl.invoke(tok, a1)
+        assert got[0] == ref[0] and np.array_equal(got[1], ref[1])
+        with pytest.raises(T.TidalError):
+            rig.tpl.export()
+        del a1, rig
+        import gc
+        gc.collect()
+        torch.cuda.synchronize()
+        assert torch.cuda.memory_allocated() <= before + 4096
+    finally:
+        T.set_device_allocator()

@@ -26,6 +26,7 @@ from paper_2503_06421_b200 import tidal as T  # noqa: E402
 ap = argparse.ArgumentParser()
 ap.add_argument("--config", default="13b")
 ap.add_argument("--S", type=int, nargs="*", default=None, help="override prompt lengths")
+ap.add_argument("--rho", type=float, nargs="*", default=None, help="override resident fractions")
 ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
 args = ap.parse_args()
 
@@ -34,7 +35,8 @@ P, _ = bench.peaks()
 if args.config == "7b":
     pts = [(2048, 0, rho) for rho in (0.0, 1.0)]
 else:
-    pts = [(S, 16, rho) for S in (args.S or (256, 867, 2048, 6101, 8192)) for rho in (0.0, 0.5, 1.0)]
+    pts = [(S, 16, rho) for S in (args.S or (256, 867, 2048, 6101, 8192))
+           for rho in (args.rho or (0.0, 0.5, 1.0))]
     if not args.S:
         pts += [(2048, r, rho) for r in (8, 32, 64) for rho in (0.0, 1.0)]
 maxS = max(p[0] for p in pts)
@@ -85,13 +87,16 @@ with open(args.out, "a") as f:
         t_pcie = streamed / b_h2d * 1e3
         t_tc = flops / (P["bf16_tflops"] * 1e12) * 1e3
         t_tc_sus = flops / (P.get("bf16_tflops_sustained", P["bf16_tflops"]) * 1e12) * 1e3
-        roof = max(t_pcie, t_tc)
+        w_bytes = sts[0]["bytes_streamed"] + sts[0]["bytes_resident"] + sts[0]["bytes_adapter"]
+        t_hbm = w_bytes / (P["hbm_gbs"] * 1e9) * 1e3   # every weight read once from HBM
+        roof = max(t_pcie, t_tc, t_hbm)
+        bound = max((("pcie", t_pcie), ("tensor", t_tc), ("hbm", t_hbm)), key=lambda kv: kv[1])[0]
         line = {"config": args.config, "S": S, "lora_rank": r, "rho_requested": rho,
                 "rho_realized": sts[0]["bytes_resident"] / M, "ttft_ms": ms,
                 "tokens_per_s": S / (ms / 1e3), "t_pcie_ms": t_pcie, "t_tensor_ms": t_tc,
-                "t_tensor_sustained_ms": t_tc_sus, "roof_ms": roof,
-                "bound": "pcie" if t_pcie >= t_tc else "tensor", "frac": roof / ms,
-                "frac_sustained": max(t_pcie, t_tc_sus) / ms, "b_h2d_GBps": b_h2d / 1e9,
+                "t_tensor_sustained_ms": t_tc_sus, "t_hbm_ms": t_hbm, "roof_ms": roof,
+                "bound": bound, "frac": roof / ms,
+                "frac_sustained": max(t_pcie, t_tc_sus, t_hbm) / ms, "b_h2d_GBps": b_h2d / 1e9,
                 "h2d_span_ms": statistics.median(s["h2d_last_ms"] - s["h2d_first_ms"] for s in sts),
                 "compute_start_ms": statistics.median(s["compute_first_ms"] for s in sts)}
         print(json.dumps(line), flush=True)
