@@ -710,27 +710,35 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
           if (threadIdx.x == 64) st_release(flag, wk.split + 1 < ks ? wk.split + 1 : 0);
         }
       } else if (EPI == EPI_ROPE && sg.rope) {
+        // rotate-half RoPE: the (cos, sin) of this row's position and a
+        // 32-pair column block are loaded once and reused by every head of the
+        // tile; the loads are issued before the TMEM reads so their latency
+        // overlaps them (the table loads were the epilogue's main stall)
         const int hd = p.head_dim, half = hd >> 1;
         const int ncols = min(BNT, sg.n - n0);
+        const int pos = p.seq_len ? m % p.seq_len : m;  // batched prompts restart at 0
+        bf16* out = reinterpret_cast<bf16*>(p.out);
 #pragma unroll 1
-        for (int h = 0; h * hd < ncols; ++h) {
+        for (int j = 0; j * 32 < half; ++j) {
+          float2 cs[32];
+          if (m < p.M) {
+            const float2* src = p.rope + (size_t)pos * half + j * 32;
+#pragma unroll
+            for (int i = 0; i < 32; ++i) cs[i] = __ldg(src + i);
+          }
 #pragma unroll 1
-          for (int j = 0; j * 32 < half; ++j) {
+          for (int h = 0; h * hd < ncols; ++h) {
             const int c1 = h * hd + j * 32, c2 = c1 + half;
             ld_chunk(tacc + c1, v);
             ld_chunk(tacc + c2, w);
             if (m < p.M) {
-              const int pos = p.seq_len ? m % p.seq_len : m;  // batched prompts restart at 0
-              const float2* cs = p.rope + (size_t)pos * half + j * 32;
 #pragma unroll
               for (int i = 0; i < 32; ++i) {
-                const float2 t = cs[i];
                 const float x1 = v[i], x2 = w[i];
-                v[i] = x1 * t.x - x2 * t.y;
-                w[i] = x2 * t.x + x1 * t.y;
+                v[i] = x1 * cs[i].x - x2 * cs[i].y;
+                w[i] = x2 * cs[i].x + x1 * cs[i].y;
               }
             }
-            bf16* out = reinterpret_cast<bf16*>(p.out);
             store_chunk_bf16(v, stg, lane, out, p.ldo, row0, p.M, sg.out_col + n0 + c1, 32);
             store_chunk_bf16(w, stg, lane, out, p.ldo, row0, p.M, sg.out_col + n0 + c2, 32);
             if (sg.out2) {
@@ -766,9 +774,11 @@ __global__ void __launch_bounds__(NTHREADS, 1) gemm_tc_kernel(const __grid_const
 #pragma unroll
             for (int i = 0; i < 32; ++i)
               if (i < nv) dst[(size_t)i * p.vt_ld] = __float2bfloat16_rn(v[i]);
+            if (pad) {
 #pragma unroll 1
-            for (int i = 0; i < nv; ++i)
-              for (int c = 1; c <= pad; ++c) dst[(size_t)i * p.vt_ld + c] = __float2bfloat16_rn(0.f);
+              for (int i = 0; i < nv; ++i)
+                for (int c = 1; c <= pad; ++c) dst[(size_t)i * p.vt_ld + c] = __float2bfloat16_rn(0.f);
+            }
           }
         }
       }

@@ -144,18 +144,28 @@ __global__ void __launch_bounds__(HEAD_THREADS) head_kernel(const float* __restr
     float acc[HEAD_MAX_ROWS];
 #pragma unroll
     for (int b = 0; b < HEAD_MAX_ROWS; ++b) acc[b] = 0.f;
-    for (int c = lane * 8; c < d; c += 256) {  // each W row is read once for all rows
-      uint4 q = __ldg(reinterpret_cast<const uint4*>(w + c));
-      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q);
-      const float2 a = __bfloat1622float2(h[0]), bb = __bfloat1622float2(h[1]);
-      const float2 e = __bfloat1622float2(h[2]), f = __bfloat1622float2(h[3]);
+    // each W row is read once for all rows; 4 independent 16-B loads per lane
+    // in flight (the GEMV is HBM-latency bound with one)
+    for (int c0 = lane * 8; c0 < d; c0 += 1024) {
+      uint4 q[4];
 #pragma unroll
-      for (int b = 0; b < HEAD_MAX_ROWS; ++b) {
-        if (b >= nrows) break;
-        const float4 x0 = *reinterpret_cast<const float4*>(hs + b * d + c);
-        const float4 x1 = *reinterpret_cast<const float4*>(hs + b * d + c + 4);
-        acc[b] += a.x * x0.x + a.y * x0.y + bb.x * x0.z + bb.y * x0.w + e.x * x1.x + e.y * x1.y +
-                  f.x * x1.z + f.y * x1.w;
+      for (int u = 0; u < 4; ++u)
+        if (c0 + u * 256 < d) q[u] = __ldg(reinterpret_cast<const uint4*>(w + c0 + u * 256));
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        const int c = c0 + u * 256;
+        if (c >= d) break;
+        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
+        const float2 a = __bfloat1622float2(h[0]), bb = __bfloat1622float2(h[1]);
+        const float2 e = __bfloat1622float2(h[2]), f = __bfloat1622float2(h[3]);
+#pragma unroll
+        for (int b = 0; b < HEAD_MAX_ROWS; ++b) {
+          if (b >= nrows) break;
+          const float4 x0 = *reinterpret_cast<const float4*>(hs + b * d + c);
+          const float4 x1 = *reinterpret_cast<const float4*>(hs + b * d + c + 4);
+          acc[b] += a.x * x0.x + a.y * x0.y + bb.x * x0.z + bb.y * x0.w + e.x * x1.x + e.y * x1.y +
+                    f.x * x1.z + f.y * x1.w;
+        }
       }
     }
 #pragma unroll
