@@ -107,24 +107,39 @@ class Clocks:
                 "reasons": reasons, "samples": len(self.rows)}
 
 
-def oracle_sample(cfg, S, r, seed=0):
-    """One bounded oracle sample: embed + 1 decoder layer + head at full width
-    and full S, LoRA on all 7 targets; returns seconds."""
+ORACLE_LAYERS = 3   # decoder layers per bounded oracle sample (+ embed and head)
+
+
+def oracle_sampler(cfg, S, r, seed=0, n_layers=ORACLE_LAYERS):
+    """A bounded oracle sample: embed + the first n_layers decoder layers +
+    head at full width and full S, LoRA on all 7 targets.  Inputs (weights,
+    adapter, prompt) are generated once, outside any timing; the returned
+    callable times one forward and returns seconds."""
     from oracle import forward as F
+    n_layers = min(n_layers, cfg.n_layers)
     w = F.synth_weights(cfg, seed, fast=True, keep=True)
     a = F.synth_adapter(cfg, r, 1, fast=True) if r else None
     tok = synth.prompt_fast(cfg, S, 0)
-    # generate the inputs first: weight generation is not part of the timed sample
+    keep = tuple(f"model.layers.{i}." for i in range(n_layers))
     for s in synth.base_tensors(cfg):
-        if not s.name.startswith("model.layers.") or s.name.startswith("model.layers.0."):
+        if not s.name.startswith("model.layers.") or s.name.startswith(keep):
             w(s.name)
     if a is not None:
         for s in synth.adapter_tensors(cfg, r):
-            if s.name.startswith("model.layers.0."):
+            if s.name.startswith(keep):
                 a(s.name)
-    t = time.perf_counter()
-    F.forward(cfg, w, tok, a, 0x7F if r else 0, 1.0, n_layers=1)
-    return time.perf_counter() - t
+
+    def run():
+        t = time.perf_counter()
+        F.forward(cfg, w, tok, a, 0x7F if r else 0, 1.0, n_layers=n_layers)
+        return time.perf_counter() - t
+    return run
+
+
+def oracle_extrapolate(cfg, t_sample, n_layers=ORACLE_LAYERS):
+    """Full-forward ms from a sample of n_layers (+ embed + head): layers
+    scale linearly; the embed / head share is small (< 2 % at 13B)."""
+    return t_sample * 1e3 * cfg.n_layers / min(n_layers, cfg.n_layers)
 
 
 def workload_name(config, S, r):
@@ -141,14 +156,19 @@ def run_reference(args):
         return
     cfg = synth.config(args.config)
     cores = len(os.sched_getaffinity(0))
+    sample_fn = oracle_sampler(cfg, args.seq, args.rank)
     for _ in range(args.warmup):
-        oracle_sample(cfg, args.seq, args.rank)
-    ts = [oracle_sample(cfg, args.seq, args.rank) for _ in range(args.steps)]
-    ms = statistics.mean(ts) * 1e3 * cfg.n_layers
-    sample = f"embed + 1 of {cfg.n_layers} layers + head at S={args.seq}, r={args.rank}; x{cfg.n_layers}"
+        sample_fn()
+    ts = [sample_fn() for _ in range(args.steps)]
+    ms = oracle_extrapolate(cfg, statistics.median(ts))
+    sample = (f"embed + {min(ORACLE_LAYERS, cfg.n_layers)} of {cfg.n_layers} layers + head at S={args.seq}, "
+              f"r={args.rank}; value = median sample x {cfg.n_layers}/{min(ORACLE_LAYERS, cfg.n_layers)}")
     print(json.dumps({
         "impl": "reference", "metric": "template-start TTFT", "value": ms, "unit": "ms",
-        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+        "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+        # wall time of one timed step (one bounded sample), so steps x ms_per_step
+        # matches the run's own clock; value extrapolates the sample to the workload
+        "ms_per_step": statistics.mean(ts) * 1e3,
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
         "data": "synthetic (seeded splitmix64 weights, uniform prompt)",
         "config": {"workload": workload_name(args.config, args.seq, args.rank),
@@ -468,11 +488,15 @@ def main():
                            "compute stream, incl. bf16 pack/add kernels when bf16)"}
     cpu = None
     if world == 1 and not args.no_cpu_baseline:
-        t1 = oracle_sample(cfg, S, r)
-        cpu = {"value": t1 * 1e3 * cfg.n_layers, "unit": "ms",
+        sample_fn = oracle_sampler(cfg, S, r)
+        sample_fn()
+        t1 = statistics.median(sample_fn() for _ in range(2))
+        cpu = {"value": oracle_extrapolate(cfg, t1), "unit": "ms",
                "cores": len(os.sched_getaffinity(0)), "kind": "oracle",
-               "sample": f"numpy fp32 oracle: embed + 1 of {cfg.n_layers} layers + head at "
-                         f"S={S}, LoRA r{r}; value = t x {cfg.n_layers}"}
+               "sample": f"numpy fp32 oracle: embed + {ORACLE_LAYERS} of {cfg.n_layers} layers + "
+                         f"head at S={S}, LoRA r{r}, median of 2 after 1 warm-up; "
+                         f"value = t x {cfg.n_layers}/{min(ORACLE_LAYERS, cfg.n_layers)}",
+               "sample_s": t1}
     out = {
         "metric": "template-start TTFT", "value": ttft, "unit": "ms", "n_gpus": world,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": ttft,
