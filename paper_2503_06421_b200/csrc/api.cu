@@ -1225,9 +1225,25 @@ tidal_status tidal_k_attention_tc(const void* qkv, const void* vt, int vt_ld, vo
           "attention tensor maps");
   const char* rep = getenv("TIDAL_K_REPEAT");  // timing harness: n launches back to back
   const int reps = rep && atoi(rep) > 0 ? atoi(rep) : 1;
+  // diagnostic: TIDAL_ATTN_TRACE=<file> dumps a per-tile timeline of the last launch
+  const char* trace = getenv("TIDAL_ATTN_TRACE");
+  const size_t tn = (size_t)sms() * 64 * 8;
+  if (trace) {
+    cuda_check(cudaMalloc(&p.dbg, tn * 8), "cudaMalloc(trace)");
+    cuda_check(cudaMemset(p.dbg, 0, tn * 8), "memset(trace)");
+  }
   cudaError_t e = cudaSuccess;
   for (int i = 0; i < reps && e == cudaSuccess; ++i) e = attn_tc_launch(p, 0);
   tidal_status s = sync_status(e, "attention_tc");
+  if (trace && p.dbg) {
+    std::vector<unsigned long long> h(tn);
+    cudaMemcpy(h.data(), p.dbg, tn * 8, cudaMemcpyDeviceToHost);
+    cudaFree(p.dbg);
+    if (FILE* f = fopen(trace, "wb")) {
+      fwrite(h.data(), 8, h.size(), f);
+      fclose(f);
+    }
+  }
   if (s != TIDAL_OK) return s;
   TIDAL_CATCH
 }

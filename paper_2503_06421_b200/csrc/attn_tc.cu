@@ -81,6 +81,18 @@ __device__ __forceinline__ void softmax_bar() {  // the softmax warps only
 struct Item {
   int qt, h, z;
 };
+
+// diagnostic timeline (AttnParams::dbg): per CTA, per S/P tile (first 64), 8
+// slots: 0 MMA wants S, 1 S issued, 2 softmax sees S, 3 softmax done (P),
+// 4 MMA wants PV, 5 PV issued
+constexpr int ADBG_TILES = 64;
+__device__ __forceinline__ void adbg(const AttnParams& p, int tile, int slot) {
+  if (p.dbg && tile < ADBG_TILES) {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    p.dbg[((size_t)blockIdx.x * ADBG_TILES + tile) * 8 + slot] = t;
+  }
+}
 // Work item i of this CTA (round-robin rounds, snake order so that the CTAs
 // taking the heaviest item of one round take the lightest of the next);
 // items are numbered heaviest first: qt = nq-1 .. 0, then head, then sequence.
@@ -191,8 +203,10 @@ __global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __gr
       int kc = 0, vc = 0, gs = 0, gp = 0;  // K / V tiles, S and PV MMAs issued
       auto issue_s = [&]() {
         const int s = kc % KST;
+        adbg(p, gs, 0);
         ptx::mbar_wait(k_full(s), (kc / KST) & 1);
         ptx::tc_fence_after();
+        adbg(p, gs, 1);
         const uint32_t ks = sb + OFF_K + s * TILE;
 #pragma unroll
         for (int kk = 0; kk < HD / 16; ++kk) {
@@ -217,11 +231,13 @@ __global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __gr
           if (j + 1 < nkv) issue_s();
           if (j + 1 >= nkv) ptx::mma_commit(q_empty);  // all S MMAs of the item issued
           const int t = vc % VST, b = gp & 1;
+          adbg(p, gp, 4);
           ptx::mbar_wait(p_full(b), (gp >> 1) & 1);
           ptx::mbar_wait(v_full(t), (vc / VST) & 1);
           // O of the previous item has been read out by the epilogue
           if (j == 0 && i > 0) ptx::mbar_wait(o_empty, (i - 1) & 1);
           ptx::tc_fence_after();
+          adbg(p, gp, 5);
           const uint32_t vs = sb + OFF_V + t * TILE;
 #pragma unroll
           for (int kk = 0; kk < BKV / 16; ++kk) {
@@ -299,6 +315,7 @@ __global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __gr
         const int b = gt & 1;
         ptx::mbar_wait(s_full(b), (gt >> 1) & 1);
         ptx::tc_fence_after();
+        if (threadIdx.x == 64) adbg(p, gt, 2);
         float v[COLS];
         {
           const uint32_t sc = tmem + lane_base + COL_S0 + b * 128 + half * COLS;
@@ -378,6 +395,7 @@ __global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __gr
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full(b));
+        if (threadIdx.x == 64) adbg(p, gt, 3);
       }
       // hand the row sums to the epilogue warps (double-buffered by item: the
       // epilogue of item i has read them before item i+2's softmax can end)

@@ -139,6 +139,7 @@ struct alignas(64) AttnParams {
   float scale_log2;
   bf16* out;
   int ldo;
+  unsigned long long* dbg;  // diagnostic per-tile timeline (TIDAL_ATTN_TRACE); null in production
 };
 bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, bf16* out, int S,
                     int H, int KV, int nseq = 1);
