@@ -435,6 +435,13 @@ def main():
     e2e_ms = [max_over_ranks(s["e2e_ms"]) for s in stats]
     s0 = stats[0]
     ttft = statistics.mean(dev_ms)
+    if dist:
+        # tear down in order on every rank (template before communicator before
+        # the process group) so no rank exits through interpreter-shutdown GC
+        dist.barrier()
+        tpl = None
+        comm = None
+        dist.destroy_process_group()
     if rank != 0:
         return 0
 
