@@ -1223,6 +1223,8 @@ tidal_status tidal_k_attention_tc(const void* qkv, const void* vt, int vt_ld, vo
   memset(&p, 0, sizeof p);
   require(attn_tc_params(&p, (const bf16*)qkv, (const bf16*)vt, vt_ld, (bf16*)O, S, H, KV),
           "attention tensor maps");
+  // per-call variant (tests exercise both kernels): TIDAL_ATTN=1 single, 2 pairs
+  if (const char* v = getenv("TIDAL_ATTN")) p.variant = atoi(v);
   const char* rep = getenv("TIDAL_K_REPEAT");  // timing harness: n launches back to back
   const int reps = rep && atoi(rep) > 0 ? atoi(rep) : 1;
   // diagnostic: TIDAL_ATTN_TRACE=<file> dumps a per-tile timeline of the last launch

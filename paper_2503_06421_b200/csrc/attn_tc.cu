@@ -1,5 +1,9 @@
 // attn_tc.cu — causal GQA prefill attention on 5th-gen tensor cores (hd = 128).
 //   O_h = softmax(Q_h K_g^T / sqrt(hd) + causal) V_g,   g = h / (H / KV)
+// Two kernels: attn_pp_kernel (below the first one) takes PAIRS of query
+// tiles with one softmax warpgroup per tile, so one tile's softmax overlaps
+// the other's MMAs; it is used whenever there are enough pairs to fill the
+// SMs (attn_tc_launch).  The single-tile kernel first:
 // Persistent: one CTA per SM walks a static list of work items (128 queries
 // of one head of one sequence), heaviest (latest) query tiles first, in a
 // snake order across CTAs; TMEM, barriers and the K/V rings live across
@@ -411,6 +415,387 @@ __global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __gr
   }
 }
 
+
+// ---------------------------------------------------------------------------
+// Two-query-tile ping-pong (the default).  A work item is a PAIR of adjacent
+// query tiles of one head, A = qt - 1 and B = qt (A absent for the first tile
+// of an odd tile count), sharing every K / V tile they both need.  Two softmax
+// warpgroups, one per query tile, each thread owning one query row (all 128
+// keys of a tile in registers), so one tile's softmax runs while the tensor
+// core works for the other:
+//   MMA order per key tile j:  PV_A(j), S_A(j+1), PV_B(j), S_B(j+1)
+// S_X and P_X share TMEM columns (P packed bf16 in the first 64 columns of
+// S_X): tcgen05.mma executes in issue order, so S_X(j+1) cannot overwrite P_X(j)
+// before PV_X(j) has read it, and once S_X(j+1) has landed PV_X(j) — and every
+// earlier MMA — is complete, so the softmax may rescale O_X without a wait.
+// Warp roles (512 threads, one CTA per SM, registers rebalanced by setmaxnreg):
+//   WG0   warp 0 TMA (Q_A, Q_B per item; K / V^T rings), warp 1 MMA issue
+//   WG1   softmax of tile A       WG2   softmax of tile B
+//   WG3   epilogue: O_X / l -> bf16 rows, off the softmax path
+// TMEM columns: S_A/P_A [0,128), S_B/P_B [128,256), O_A [256,384), O_B [384,512).
+namespace pp {
+constexpr int KST = 2, VST = 2;
+constexpr int OFF_Q = 0;  // Q_A, Q_B
+constexpr int OFF_K = OFF_Q + 2 * TILE;
+constexpr int OFF_V = OFF_K + KST * TILE;
+constexpr int OFF_LSUM = OFF_V + VST * TILE;  // [tile X][item parity][128] row sums
+constexpr int OFF_BAR = OFF_LSUM + 2 * 2 * BQ * 4;
+// q_full[2] q_empty[2] k_full[KST] k_empty[KST] v_full[VST] v_empty[VST]
+// s_full[2] p_full[2] o_full[2] o_empty[2] l_ready[2][2]
+constexpr int N_BARS = 4 + 2 * KST + 2 * VST + 8 + 4;
+constexpr int OFF_TMEM = OFF_BAR + N_BARS * 8;
+constexpr int SMEM = OFF_TMEM + 16 + 1024;
+constexpr int NTH = 512;
+constexpr uint32_t COL_SX = 0, COL_OX = 256;  // + X * 128
+}  // namespace pp
+
+__device__ __forceinline__ void setmaxnreg_inc_176() {
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 176;" ::: "memory");
+}
+__device__ __forceinline__ void setmaxnreg_dec_112() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 112;" ::: "memory");
+}
+__device__ __forceinline__ void setmaxnreg_dec_48() {
+  asm volatile("setmaxnreg.dec.sync.aligned.u32 48;" ::: "memory");
+}
+
+// pair item i of this CTA (snake rounds, heaviest pair first): hi tile qb,
+// lo tile qb - 1 (< 0: absent)
+__device__ __forceinline__ bool pair_at(const AttnParams& p, int nq, int round, Item& it) {
+  const int G = gridDim.x;
+  const int c = blockIdx.x;
+  const int idx = round * G + ((round & 1) ? G - 1 - c : c);
+  const int per = p.H * p.nseq;
+  const int npair = (nq + 1) / 2;
+  if (idx >= npair * per) return false;
+  const int k = idx / per, rem = idx - k * per;
+  it.qt = nq - 1 - 2 * k;  // B
+  it.h = rem % p.H;
+  it.z = rem / p.H;
+  return true;
+}
+
+__global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_constant__ AttnParams p) {
+  constexpr int KST = pp::KST, VST = pp::VST, OFF_Q = pp::OFF_Q, OFF_K = pp::OFF_K,
+                OFF_V = pp::OFF_V, OFF_LSUM = pp::OFF_LSUM, OFF_BAR = pp::OFF_BAR,
+                OFF_TMEM = pp::OFF_TMEM;
+  constexpr uint32_t COL_SX = pp::COL_SX, COL_OX = pp::COL_OX;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = smem_raw + ((1024u - (ptx::smem_u32(smem_raw) & 1023u)) & 1023u);
+  const uint32_t sb = ptx::smem_u32(smem);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const uint32_t bars = sb + OFF_BAR;
+  auto q_full = [&](int x) { return bars + 8u * x; };
+  auto q_empty = [&](int x) { return bars + 8u * (2 + x); };
+  auto k_full = [&](int s) { return bars + 8u * (4 + s); };
+  auto k_empty = [&](int s) { return bars + 8u * (4 + KST + s); };
+  auto v_full = [&](int s) { return bars + 8u * (4 + 2 * KST + s); };
+  auto v_empty = [&](int s) { return bars + 8u * (4 + 2 * KST + VST + s); };
+  constexpr int B0 = 4 + 2 * KST + 2 * VST;
+  auto s_full = [&](int x) { return bars + 8u * (B0 + x); };
+  auto p_full = [&](int x) { return bars + 8u * (B0 + 2 + x); };
+  auto o_full = [&](int x) { return bars + 8u * (B0 + 4 + x); };
+  auto o_empty = [&](int x) { return bars + 8u * (B0 + 6 + x); };
+  auto l_ready = [&](int x, int b) { return bars + 8u * (B0 + 8 + 2 * x + b); };
+  uint32_t* tmem_holder = reinterpret_cast<uint32_t*>(smem + OFF_TMEM);
+
+  const int nq = (p.S + BQ - 1) / BQ;
+  const int vld = (p.S + 63) & ~63;
+
+  if (warp == 0 && lane == 0) {
+    ptx::prefetch_tmap(&p.q);
+    ptx::prefetch_tmap(&p.vt);
+    for (int x = 0; x < 2; ++x) {
+      ptx::mbar_init(q_full(x), 1);
+      ptx::mbar_init(q_empty(x), 1);
+      ptx::mbar_init(s_full(x), 1);
+      ptx::mbar_init(p_full(x), 128);
+      ptx::mbar_init(o_full(x), 1);
+      ptx::mbar_init(o_empty(x), 128);
+      ptx::mbar_init(l_ready(x, 0), 128);
+      ptx::mbar_init(l_ready(x, 1), 128);
+    }
+    for (int s = 0; s < KST; ++s) {
+      ptx::mbar_init(k_full(s), 1);
+      ptx::mbar_init(k_empty(s), 1);
+    }
+    for (int s = 0; s < VST; ++s) {
+      ptx::mbar_init(v_full(s), 1);
+      ptx::mbar_init(v_empty(s), 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 1) ptx::tmem_alloc(ptx::smem_u32(tmem_holder), 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tmem = *tmem_holder;
+  ptx::pdl_begin();
+
+  const int wg = warp >> 2;
+  Item it;
+  if (wg == 0) {
+    setmaxnreg_dec_112();
+    if (warp == 0 && lane == 0) {
+      int kc = 0, vc = 0, nx[2] = {0, 0};
+      for (int i = 0; pair_at(p, nq, i, it); ++i) {
+        const int g = it.h / (p.H / p.KV);
+        const int base = it.z * p.S;
+        const int qc = it.h * HD, kcol = (p.H + g) * HD, vr = g * HD;
+        for (int x = 0; x < 2; ++x) {
+          const int qt = it.qt - 1 + x;
+          if (qt < 0) continue;
+          ptx::mbar_wait(q_empty(x), (nx[x] & 1) ^ 1);
+          ptx::mbar_expect_tx(q_full(x), TILE);
+          const uint32_t qs = sb + OFF_Q + x * TILE;
+          ptx::tma_load_2d(&p.q, qs, q_full(x), qc, base + qt * BQ);
+          ptx::tma_load_2d(&p.q, qs + HALF, q_full(x), qc + 64, base + qt * BQ);
+          ++nx[x];
+        }
+        for (int j = 0; j <= it.qt; ++j, ++kc, ++vc) {
+          const int s = kc % KST, t = vc % VST;
+          ptx::mbar_wait(k_empty(s), ((kc / KST) & 1) ^ 1);
+          ptx::mbar_expect_tx(k_full(s), TILE);
+          const uint32_t ks = sb + OFF_K + s * TILE;
+          ptx::tma_load_2d(&p.q, ks, k_full(s), kcol, base + j * BKV);
+          ptx::tma_load_2d(&p.q, ks + HALF, k_full(s), kcol + 64, base + j * BKV);
+          ptx::mbar_wait(v_empty(t), ((vc / VST) & 1) ^ 1);
+          ptx::mbar_expect_tx(v_full(t), TILE);
+          const uint32_t vs = sb + OFF_V + t * TILE;
+          ptx::tma_load_2d(&p.vt, vs, v_full(t), it.z * vld + j * BKV, vr);
+          ptx::tma_load_2d(&p.vt, vs + HALF, v_full(t), it.z * vld + j * BKV + 64, vr);
+        }
+      }
+    } else if (warp == 1 && lane == 0) {
+      constexpr uint32_t IDESC = ptx::idesc_bf16(128, 128);
+      int kc = 0, vc = 0;
+      int ns[2] = {0, 0}, np[2] = {0, 0}, ni[2] = {0, 0};  // S, PV, items per tile X
+      auto issue_s = [&](int x, uint32_t ks) {
+        const uint32_t qs = sb + OFF_Q + x * TILE;
+#pragma unroll
+        for (int kk = 0; kk < HD / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * HALF;
+          ptx::mma_bf16(tmem + COL_SX + x * 128, ptx::desc_sw128(qs + off) + 2 * (kk & 3),
+                        ptx::desc_sw128(ks + off) + 2 * (kk & 3), IDESC, kk > 0);
+        }
+        ptx::mma_commit(s_full(x));
+        ++ns[x];
+      };
+      auto issue_pv = [&](int x, uint32_t vs, bool acc) {
+#pragma unroll
+        for (int kk = 0; kk < BKV / 16; ++kk) {
+          const uint32_t off = (kk >> 2) * HALF;
+          ptx::mma_bf16_ts(tmem + COL_OX + x * 128, tmem + COL_SX + x * 128 + kk * 8,
+                           ptx::desc_sw128(vs + off) + 2 * (kk & 3), IDESC, acc || kk != 0);
+        }
+        ++np[x];
+      };
+      for (int i = 0; pair_at(p, nq, i, it); ++i) {
+        const int nb = it.qt + 1, na = it.qt;  // key tiles of B and A (A absent: 0)
+        // S_A(0), S_B(0) from K_0
+        {
+          const int s = kc % KST;
+          ptx::mbar_wait(k_full(s), (kc / KST) & 1);
+          const uint32_t ks = sb + OFF_K + s * TILE;
+          if (na > 0) {
+            ptx::mbar_wait(q_full(0), ni[0] & 1);
+            ptx::tc_fence_after();
+            issue_s(0, ks);
+            if (na == 1) ptx::mma_commit(q_empty(0));
+          }
+          ptx::mbar_wait(q_full(1), ni[1] & 1);
+          ptx::tc_fence_after();
+          issue_s(1, ks);
+          if (nb == 1) ptx::mma_commit(q_empty(1));
+          ptx::mma_commit(k_empty(s));
+          ++kc;
+        }
+        for (int j = 0; j < nb; ++j) {
+          const int t = vc % VST;
+          const uint32_t vs = sb + OFF_V + t * TILE;
+          ptx::mbar_wait(v_full(t), (vc / VST) & 1);
+          const bool more = j + 1 < nb;
+          const int s = kc % KST;
+          const uint32_t ks = sb + OFF_K + s * TILE;
+          if (j < na) {
+            ptx::mbar_wait(p_full(0), np[0] & 1);
+            if (j == 0 && ni[0] > 0) ptx::mbar_wait(o_empty(0), (ni[0] - 1) & 1);
+            ptx::tc_fence_after();
+            issue_pv(0, vs, j > 0);
+            if (j == na - 1) ptx::mma_commit(o_full(0));
+            if (j + 1 < na) {
+              ptx::mbar_wait(k_full(s), (kc / KST) & 1);
+              ptx::tc_fence_after();
+              issue_s(0, ks);
+              if (j + 1 == na - 1) ptx::mma_commit(q_empty(0));
+            }
+          }
+          ptx::mbar_wait(p_full(1), np[1] & 1);
+          if (j == 0 && ni[1] > 0) ptx::mbar_wait(o_empty(1), (ni[1] - 1) & 1);
+          ptx::tc_fence_after();
+          issue_pv(1, vs, j > 0);
+          ptx::mma_commit(v_empty(t));
+          ++vc;
+          if (!more) ptx::mma_commit(o_full(1));
+          if (more) {
+            ptx::mbar_wait(k_full(s), (kc / KST) & 1);
+            ptx::tc_fence_after();
+            issue_s(1, ks);
+            if (j + 1 == nb - 1) ptx::mma_commit(q_empty(1));
+            ptx::mma_commit(k_empty(s));
+            ++kc;
+          }
+        }
+        if (na > 0) ++ni[0];
+        ++ni[1];
+      }
+    }
+    __syncwarp();
+  } else if (wg == 3) {
+    // ===================== epilogue: O_X / l -> bf16 =====================
+    setmaxnreg_dec_48();
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const float* lsum = reinterpret_cast<const float*>(smem + OFF_LSUM);
+    int ni[2] = {0, 0};
+    for (int i = 0; pair_at(p, nq, i, it); ++i) {
+      for (int x = 0; x < 2; ++x) {
+        const int qt = it.qt - 1 + x;
+        if (qt < 0) continue;
+        const int b = ni[x] & 1;
+        ptx::mbar_wait(l_ready(x, b), (ni[x] >> 1) & 1);
+        const float inv = 1.f / lsum[(x * 2 + b) * BQ + row];
+        ptx::mbar_wait(o_full(x), ni[x] & 1);
+        ptx::tc_fence_after();
+        ++ni[x];
+        const int qi = qt * BQ + row;
+        const uint32_t o_row = tmem + ((uint32_t)(q * 32) << 16) + COL_OX + x * 128;
+        bf16* out = p.out + (size_t)(it.z * p.S + qi) * p.ldo + it.h * HD;
+#pragma unroll 1
+        for (int c = 0; c < 4; ++c) {
+          uint32_t r[32];
+          ptx::tmem_ld32(o_row + c * 32, r);
+          ptx::tmem_ld_wait();
+          if (c == 3) {
+            ptx::tc_fence_before();
+            ptx::mbar_arrive(o_empty(x));
+          }
+          if (qi < p.S) {
+#pragma unroll
+            for (int k = 0; k < 4; ++k) {
+              uint4 w;
+              w.x = pack_bf16x2(__uint_as_float(r[8 * k + 0]) * inv, __uint_as_float(r[8 * k + 1]) * inv);
+              w.y = pack_bf16x2(__uint_as_float(r[8 * k + 2]) * inv, __uint_as_float(r[8 * k + 3]) * inv);
+              w.z = pack_bf16x2(__uint_as_float(r[8 * k + 4]) * inv, __uint_as_float(r[8 * k + 5]) * inv);
+              w.w = pack_bf16x2(__uint_as_float(r[8 * k + 6]) * inv, __uint_as_float(r[8 * k + 7]) * inv);
+              *reinterpret_cast<uint4*>(out + c * 32 + k * 8) = w;
+            }
+          }
+        }
+      }
+    }
+  } else {
+    // ===================== softmax of tile X (WG1: A, WG2: B) =====================
+    setmaxnreg_inc_176();
+    const int x = wg - 1;
+    const int q = warp & 3;
+    const int row = q * 32 + lane;
+    const uint32_t lane_base = (uint32_t)(q * 32) << 16;
+    const uint32_t s_col = tmem + lane_base + COL_SX + x * 128;
+    const uint32_t o_col = tmem + lane_base + COL_OX + x * 128;
+    float* lsum = reinterpret_cast<float*>(smem + OFF_LSUM);
+    int gt = 0, ni = 0;
+    for (int i = 0; pair_at(p, nq, i, it); ++i) {
+      const int qt = it.qt - 1 + x;
+      if (qt < 0) continue;
+      const int q0 = qt * BQ, qi = q0 + row;
+      const int nkv = qt + 1;
+      float m_used = -INFINITY, l = 0.f;
+      for (int j = 0; j < nkv; ++j, ++gt) {
+        ptx::mbar_wait(s_full(x), gt & 1);
+        ptx::tc_fence_after();
+        // all 128 scores of the row in registers (one TMEM round trip)
+        const bool diag = j == qt;  // the diagonal tile: causal mask key > qi
+        const int kq = qi - j * BKV;
+        float v[128];
+#pragma unroll
+        for (int c0 = 0; c0 < 128; c0 += 32) {
+          uint32_t r0[32];
+          ptx::tmem_ld32(s_col + c0, r0);
+#pragma unroll
+          for (int c = 0; c < 32; ++c) v[c0 + c] = __uint_as_float(r0[c]);
+        }
+        ptx::tmem_ld_wait();
+        if (diag) {
+#pragma unroll
+          for (int c = 0; c < 128; ++c)
+            if (c > kq) v[c] = -INFINITY;
+        }
+        float mr[8];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) mr[k] = v[k];
+#pragma unroll
+        for (int c = 8; c < 128; ++c) mr[c & 7] = fmaxf(mr[c & 7], v[c]);
+        const float mraw = fmaxf(fmaxf(fmaxf(mr[0], mr[1]), fmaxf(mr[2], mr[3])),
+                                 fmaxf(fmaxf(mr[4], mr[5]), fmaxf(mr[6], mr[7])));
+        const float mx = fmaxf(m_used, mraw * p.scale_log2);
+        const bool need = mx > m_used + 8.f;
+        if (j > 0 && __any_sync(0xffffffffu, need)) {
+          // O_X settled: S_X(j) was issued after PV_X(j-1) (in-order tensor pipe)
+          const float corr = need ? ptx::ex2(m_used - mx) : 1.f;
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            uint32_t r[32];
+            ptx::tmem_ld32(o_col + c * 32, r);
+            ptx::tmem_ld_wait();
+#pragma unroll
+            for (int e = 0; e < 32; ++e) r[e] = __float_as_uint(__uint_as_float(r[e]) * corr);
+            ptx::tmem_st32(o_col + c * 32, r);
+          }
+          l *= corr;
+        }
+        if (need) m_used = mx;
+        // P = 2^(s*scale - m) -> packed bf16 pairs over the first 64 columns of
+        // S_X; chunk c lands on columns [16c, 16c+16), whose scores are in
+        // registers already (masked scores are -inf: 2^-inf = 0)
+        float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          uint32_t pk[16];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            float e[8];
+#pragma unroll
+            for (int k = 0; k < 8; ++k) {
+              const float a = fmaf(v[c * 32 + u * 8 + k], p.scale_log2, -m_used);
+              e[k] = ptx::ex2(a);
+              ls[k] += e[k];
+            }
+            pk[4 * u + 0] = pack_bf16x2(e[0], e[1]);
+            pk[4 * u + 1] = pack_bf16x2(e[2], e[3]);
+            pk[4 * u + 2] = pack_bf16x2(e[4], e[5]);
+            pk[4 * u + 3] = pack_bf16x2(e[6], e[7]);
+          }
+          ptx::tmem_st16(s_col + c * 16, pk);
+        }
+        l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+        ptx::tmem_st_wait();
+        ptx::tc_fence_before();
+        ptx::mbar_arrive(p_full(x));
+      }
+      lsum[(x * 2 + (ni & 1)) * BQ + row] = l;
+      ptx::mbar_arrive(l_ready(x, ni & 1));
+      ++ni;
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tmem, 512);
+  }
+}
+
 }  // namespace
 
 bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, bf16* out, int S,
@@ -453,6 +838,17 @@ static cudaError_t attn_set_attr() {
 // us; S = 8192: 775 vs 735 us, tools/attn_bench.py): the per-tile softmax is
 // not latency-hidden by more warps — the extra row-max exchange and barrier
 // of 512 threads cost more than they hide.
+static cudaError_t attn_pp_launch(const AttnParams& p, cudaStream_t s, int grid) {
+  static bool attr = false;
+  if (!attr) {
+    cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         pp::SMEM);
+    if (e != cudaSuccess) return e;
+    attr = true;
+  }
+  return launch_kt("attn", attn_pp_kernel, dim3(grid), dim3(pp::NTH), pp::SMEM, s, 1, p);
+}
+
 cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
   constexpr int split = 2;
   cudaError_t ea = attn_set_attr<split>();
@@ -463,6 +859,21 @@ cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
   }
+  // TIDAL_ATTN=1 / 2: force single tiles / pairs (A/B; the adbg trace is in
+  // the single-tile kernel)
+  static int forced = -1;
+  if (forced < 0) {
+    const char* e = getenv("TIDAL_ATTN");
+    forced = e ? atoi(e) : 0;
+  }
+  const int variant = p.variant ? p.variant : forced;
+  // pairs of query tiles unless there are too few pairs to fill the SMs about
+  // 1.25 times (13B, H = 40, tools/attn_bench.py: paired 22.6 / 28.2 / 59.9 /
+  // 175 / 638 us against single 20.0 / 32.0 / 64.6 / 205 / 764 us at S = 867 /
+  // 1154 / 2048 / 4096 / 8192 — 160 pairs on 148 SMs quantise badly)
+  const long pairs = (long)((p.S + BQ - 1) / BQ + 1) / 2 * p.H * p.nseq;
+  if (!p.dbg && (variant == 2 || (variant == 0 && 4 * pairs >= 5L * sms)))
+    return attn_pp_launch(p, s, (int)(pairs < sms ? pairs : sms));
   const long items = (long)((p.S + BQ - 1) / BQ) * p.H * p.nseq;  // persistent: <= one CTA per SM
   const int grid = (int)(items < sms ? items : sms);
   if (grid <= 0) return cudaSuccess;

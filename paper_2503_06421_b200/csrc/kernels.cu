@@ -139,45 +139,67 @@ __global__ void __launch_bounds__(HEAD_THREADS) head_kernel(const float* __restr
   unsigned long long best[HEAD_MAX_ROWS];
 #pragma unroll
   for (int b = 0; b < HEAD_MAX_ROWS; ++b) best[b] = 0;
-  for (int v = gw; v < V; v += nw) {
-    const bf16* w = W + (size_t)v * d;
-    float acc[HEAD_MAX_ROWS];
+  // The warp's rows v = gw, gw + nw, ... are streamed as one sequence of
+  // 2048-element batches (8 x 16-B loads per lane); the next batch — possibly
+  // the next row's first — is issued before the current one is consumed, so
+  // every warp keeps two batches (16 loads per lane) in flight and a row costs
+  // no dependent round trip of its own.
+  constexpr int BU = 8, BE = BU * 256;  // loads per lane, elements per batch
+  const int nbr = (d + BE - 1) / BE;    // batches per row
+  auto load = [&](int v, int b, uint4 (&q)[BU]) {
+    const bf16* w = W + (size_t)v * d + b * BE + lane * 8;
 #pragma unroll
-    for (int b = 0; b < HEAD_MAX_ROWS; ++b) acc[b] = 0.f;
-    // each W row is read once for all rows; 4 independent 16-B loads per lane
-    // in flight (the GEMV is HBM-latency bound with one)
-    for (int c0 = lane * 8; c0 < d; c0 += 1024) {
-      uint4 q[4];
+    for (int u = 0; u < BU; ++u)
+      q[u] = (b * BE + u * 256 + lane * 8 < d) ? __ldcs(reinterpret_cast<const uint4*>(w + u * 256))
+                                               : make_uint4(0, 0, 0, 0);
+  };
+  float acc[HEAD_MAX_ROWS];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (c0 + u * 256 < d) q[u] = __ldg(reinterpret_cast<const uint4*>(w + c0 + u * 256));
+  for (int r = 0; r < HEAD_MAX_ROWS; ++r) acc[r] = 0.f;
+  uint4 cur[BU];
+  int v = gw, b = 0;
+  if (v < V) load(v, b, cur);
+  while (v < V) {
+    int vn = v, bn = b + 1;
+    if (bn == nbr) {
+      bn = 0;
+      vn = v + nw;
+    }
+    uint4 nxt[BU];
+    if (vn < V) load(vn, bn, nxt);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const int c = c0 + u * 256;
-        if (c >= d) break;
-        const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&q[u]);
-        const float2 a = __bfloat1622float2(h[0]), bb = __bfloat1622float2(h[1]);
-        const float2 e = __bfloat1622float2(h[2]), f = __bfloat1622float2(h[3]);
+    for (int u = 0; u < BU; ++u) {
+      const int c = b * BE + u * 256 + lane * 8;
+      if (c >= d) break;
+      const __nv_bfloat162* h = reinterpret_cast<const __nv_bfloat162*>(&cur[u]);
+      const float2 a = __bfloat1622float2(h[0]), bb = __bfloat1622float2(h[1]);
+      const float2 e = __bfloat1622float2(h[2]), f = __bfloat1622float2(h[3]);
 #pragma unroll
-        for (int b = 0; b < HEAD_MAX_ROWS; ++b) {
-          if (b >= nrows) break;
-          const float4 x0 = *reinterpret_cast<const float4*>(hs + b * d + c);
-          const float4 x1 = *reinterpret_cast<const float4*>(hs + b * d + c + 4);
-          acc[b] += a.x * x0.x + a.y * x0.y + bb.x * x0.z + bb.y * x0.w + e.x * x1.x + e.y * x1.y +
-                    f.x * x1.z + f.y * x1.w;
+      for (int r = 0; r < HEAD_MAX_ROWS; ++r) {
+        if (r >= nrows) break;
+        const float4 x0 = *reinterpret_cast<const float4*>(hs + r * d + c);
+        const float4 x1 = *reinterpret_cast<const float4*>(hs + r * d + c + 4);
+        acc[r] += a.x * x0.x + a.y * x0.y + bb.x * x0.z + bb.y * x0.w + e.x * x1.x + e.y * x1.y +
+                  f.x * x1.z + f.y * x1.w;
+      }
+    }
+    if (bn == 0) {  // row v complete
+#pragma unroll
+      for (int r = 0; r < HEAD_MAX_ROWS; ++r) {
+        if (r >= nrows) break;
+        const float t = warp_sum(acc[r]);
+        acc[r] = 0.f;
+        if (lane == 0) {
+          logits[(size_t)r * ldl + v] = t;
+          const unsigned long long k = argmax_key(t, v + voff);
+          best[r] = k > best[r] ? k : best[r];
         }
       }
     }
 #pragma unroll
-    for (int b = 0; b < HEAD_MAX_ROWS; ++b) {
-      if (b >= nrows) break;
-      const float r = warp_sum(acc[b]);
-      if (lane == 0) {
-        logits[(size_t)b * ldl + v] = r;
-        const unsigned long long k = argmax_key(r, v + voff);
-        best[b] = k > best[b] ? k : best[b];
-      }
-    }
+    for (int u = 0; u < BU; ++u) cur[u] = nxt[u];
+    v = vn;
+    b = bn;
   }
   if (lane == 0)
 #pragma unroll
@@ -279,7 +301,19 @@ cudaError_t head_launch(const float* X_last, size_t x_stride, int nseq, const bf
   int per = (int)((200 * 1024) / ((size_t)d * sizeof(float)));
   per = per < HEAD_MAX_ROWS ? per : HEAD_MAX_ROWS;
   if (per < 1) return cudaErrorInvalidValue;
-  int grid = num_sms * 4;
+  // one wave of co-resident CTAs (the shared rows and ~125 registers per
+  // thread allow 2 per SM at d = 5120)
+  static size_t occ_smem = 0;
+  static int per_sm = 0;
+  const size_t smem = (size_t)(nseq < per ? nseq : per) * d * sizeof(float);
+  if (smem != occ_smem || per_sm < 1) {
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, head_kernel, HEAD_THREADS, smem) !=
+            cudaSuccess ||
+        per_sm < 1)
+      per_sm = 1;
+    occ_smem = smem;
+  }
+  int grid = num_sms * per_sm;
   const int need = (V + HEAD_THREADS / 32 - 1) / (HEAD_THREADS / 32);
   if (grid > need) grid = need;
   for (int b0 = 0; b0 < nseq; b0 += per) {

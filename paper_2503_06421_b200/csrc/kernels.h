@@ -140,6 +140,7 @@ struct alignas(64) AttnParams {
   bf16* out;
   int ldo;
   unsigned long long* dbg;  // diagnostic per-tile timeline (TIDAL_ATTN_TRACE); null in production
+  int variant;  // 0: by size (pairs of query tiles when >= 2 rounds), 1: single tiles, 2: pairs
 };
 bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, bf16* out, int S,
                     int H, int KV, int nseq = 1);

@@ -527,6 +527,8 @@ cudaError_t Exec::attention_tc(int S, int nseq, cudaStream_t s) {
     if (!attn_tc_params(&p, QKV, Vt, vt_ld, O, S / nseq, m.n_heads / world, m.n_kv_heads / world,
                         nseq))
       fail(3, "attention tensor maps");
+    // TIDAL_ATTN=1 / 2 pins the single-tile / paired kernel for this template (A/B, tests)
+    if (const char* v = getenv("TIDAL_ATTN")) p.variant = atoi(v);
     it = attn_cache.emplace(std::make_pair(S, nseq), p).first;
   }
   return attn_tc_launch(it->second, s);

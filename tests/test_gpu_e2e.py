@@ -235,10 +235,14 @@ def test_load_order_ablation_correct(T, order):
     (synth.ModelConfig("gqa128", 2, 512, 4, 2, 1376, 2048, rope_theta=500000.0), 4, 130, 0.4, 16),
     (synth.ModelConfig("gqa128", 2, 512, 4, 2, 1376, 2048, rope_theta=500000.0), 2, 256, 0.0, 0),
 ])
-def test_batch_prompts_match_oracle(T, cfg, B, Ls, rho, rank):
+@pytest.mark.parametrize("attn", ["auto", "2"])
+def test_batch_prompts_match_oracle(T, cfg, B, Ls, rho, rank, attn, monkeypatch):
     """Batched prefill (§7.2, Fig. ttft-bs): B prompts of one length in
     one invocation, weights streamed once; each prompt's first token and logits
-    equal the oracle run on that prompt alone."""
+    equal the oracle run on that prompt alone.  attn = "2" pins the paired
+    query-tile attention kernel (auto picks it only for large S x H)."""
+    if attn != "auto":
+        monkeypatch.setenv("TIDAL_ATTN", attn)
     rig = Rig(T, cfg, seed=8, budget=rho, max_tokens=B * Ls)
     rig.tpl.set_debug(T.DEBUG_POISON)
     toks = np.stack([synth.prompt(cfg, Ls, 40 + b) for b in range(B)])

@@ -249,10 +249,15 @@ def test_attention_causal_gqa(T, S, H, KV, hd):
     _close_rows_bf16(_host(O), ref)
 
 
-@pytest.mark.parametrize("S,H,KV", [(1, 2, 1), (128, 2, 2), (300, 4, 2), (1000, 3, 1), (2048, 2, 2)])
-def test_attention_tcgen05(T, S, H, KV):
+@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("S,H,KV", [(1, 2, 1), (128, 2, 2), (129, 1, 1), (300, 4, 2), (640, 2, 1),
+                                    (1000, 3, 1), (2048, 2, 2)])
+def test_attention_tcgen05(T, S, H, KV, variant, monkeypatch):
     """The tcgen05/TMEM attention (hd = 128) against the oracle; V passed
-    transposed as the QKV epilogue writes it."""
+    transposed as the QKV epilogue writes it.  variant 1: one query tile per
+    item; 2: pairs of query tiles (odd tile counts leave the first pair with
+    one tile: S = 1, 300, 640)."""
+    monkeypatch.setenv("TIDAL_ATTN", variant)
     hd = 128
     rng = np.random.default_rng(S * 7 + H)
     qkv = _bf(rng, (S, (H + 2 * KV) * hd))
@@ -268,8 +273,10 @@ def test_attention_tcgen05(T, S, H, KV):
     _close_rows_bf16(_host(O), ref)
 
 
-def test_attention_tcgen05_large_logits(T):
+@pytest.mark.parametrize("variant", ["1", "2"])
+def test_attention_tcgen05_large_logits(T, variant, monkeypatch):
     """Scores spanning > 2^8 in exp2 units exercise the lazy O rescale."""
+    monkeypatch.setenv("TIDAL_ATTN", variant)
     S, H, KV, hd = 512, 1, 1, 128
     rng = np.random.default_rng(11)
     qkv = _bf(rng, (S, 3 * hd))
