@@ -150,10 +150,12 @@ __device__ __forceinline__ void fma8(const uint4& u, const float* x, float& s) {
 }
 // nx0/nx1 (nullable): the next pair's rows — their first batch is issued in
 // place of this pair's (empty) batch past the end, so the stream never drains
+// xs1 (nullable): row w1's input (the second K half of a split row), else xs
 __device__ __forceinline__ void dot2(const bf16* __restrict__ w0, const bf16* __restrict__ w1,
                                      const float* xs, int K, uint4 (&ca)[4], uint4 (&cb)[4],
                                      float& a0, float& a1, const bf16* nx0 = nullptr,
-                                     const bf16* nx1 = nullptr) {
+                                     const bf16* nx1 = nullptr, const float* xs1 = nullptr) {
+  if (!xs1) xs1 = xs;
   const int lane = threadIdx.x & 31;
   const uint4* r0 = reinterpret_cast<const uint4*>(w0);
   const uint4* r1 = reinterpret_cast<const uint4*>(w1);
@@ -171,7 +173,7 @@ __device__ __forceinline__ void dot2(const bf16* __restrict__ w0, const bf16* __
       const int j = i + 32 * k;
       if (j < n) {
         fma8(ca[k], xs + 8 * j, s0);
-        fma8(cb[k], xs + 8 * j, s1);
+        fma8(cb[k], xs1 + 8 * j, s1);
       }
     }
 #pragma unroll
@@ -272,6 +274,11 @@ __device__ __forceinline__ void pair_rows(const DecGemv& p, int pr, const bf16*&
     r0 = r1 = pr;
     w0 = p.W[0] + (size_t)pr * p.K;
     w1 = p.W[1] + (size_t)pr * p.K;
+  } else if (p.split) {  // one row, its two K halves (summed in the epilogue)
+    seg = 0;
+    r0 = r1 = pr;
+    w0 = p.W[0] + (size_t)pr * p.K;
+    w1 = w0 + (p.K >> 1);
   } else {
     seg = 0;
     r0 = 2 * pr;
@@ -330,10 +337,11 @@ __global__ void __launch_bounds__(DT) dec_gemv_kernel(DecGemv p) {
   uint4 ca[4], cb[4];
   const bf16 *w0 = nullptr, *w1 = nullptr;
   int seg = 0, r0 = 0, r1 = 0;
+  const int kd = MODE == DEC_RESID && p.split ? p.K >> 1 : p.K;  // dot length per "row"
   if (pr < p.npairs) {
     pair_rows<MODE>(p, pr, w0, w1, seg, r0, r1);
     load_batch(reinterpret_cast<const uint4*>(w0), reinterpret_cast<const uint4*>(w1), lane,
-               p.K >> 3, ca, cb);
+               kd >> 3, ca, cb);
   }
   ptx::pdl_wait();
   load_input(xs, p.X, p.g, p.xin, p.K, p.eps, red);
@@ -366,7 +374,7 @@ __global__ void __launch_bounds__(DT) dec_gemv_kernel(DecGemv p) {
     int nseg = 0, nr0 = 0, nr1 = 0;
     if (pr + stride < p.npairs) pair_rows<MODE>(p, pr + stride, n0, n1, nseg, nr0, nr1);
     float a0, a1;
-    dot2(w0, w1, xs, p.K, ca, cb, a0, a1, n0, n1);
+    dot2(w0, w1, xs, kd, ca, cb, a0, a1, n0, n1, kd != p.K ? xs + kd : nullptr);
     if (!t_ready) fetch_t();
     if (MODE == DEC_QKV) {
       a0 += lora_row_r(p.B[seg], r0, p.r, tv[seg][0], tv[seg][1]);
@@ -387,6 +395,9 @@ __global__ void __launch_bounds__(DT) dec_gemv_kernel(DecGemv p) {
       const float gt = a0 + lora_row_r(p.B[0], pr, p.r, tv[0][0], tv[0][1]);
       const float up = a1 + lora_row_r(p.B[1], pr, p.r, tv[1][0], tv[1][1]);
       if (lane == 0) p.h[pr] = __float2bfloat16_rn(gt / (1.f + __expf(-gt)) * up);
+    } else if (p.split) {  // DEC_RESID, split row: X[row] += (half0 + half1) + LoRA
+      const float lr = lora_row_r(p.B[0], r0, p.r, tv[0][0], tv[0][1]);
+      if (lane == 0) p.Xout[r0] += (a0 + a1) + lr;
     } else {  // DEC_RESID: X[row] += W[row] . x
       a0 += lora_row_r(p.B[0], r0, p.r, tv[0][0], tv[0][1]);
       a1 += lora_row_r(p.B[0], r1, p.r, tv[0][0], tv[0][1]);
@@ -543,7 +554,20 @@ cudaError_t dec_save_logits_launch(const DecodeState* st, const float* logits, f
                   all, V);
 }
 
-cudaError_t dec_gemv_launch(const DecGemv& p, int mode, int num_sms, cudaStream_t s) {
+cudaError_t dec_gemv_launch(const DecGemv& p0, int mode, int num_sms, cudaStream_t s) {
+  // residual GEMVs (N = d rows): split every row into its two K halves so
+  // twice as many warps stream (N / 2 row pairs leave half of them idle);
+  // TIDAL_DEC_SPLIT=0 keeps row pairs
+  static const bool split_off = [] {
+    const char* e = getenv("TIDAL_DEC_SPLIT");
+    return e && e[0] == '0';
+  }();
+  DecGemv p = p0;
+  p.split = 0;
+  if (mode == DEC_RESID && !split_off && p.K % 16 == 0) {
+    p.split = 1;
+    p.npairs = p.N;
+  }
   static bool attr[3] = {false, false, false};
   auto k = mode == DEC_QKV ? dec_gemv_kernel<DEC_QKV>
                            : (mode == DEC_GU ? dec_gemv_kernel<DEC_GU> : dec_gemv_kernel<DEC_RESID>);

@@ -228,6 +228,8 @@ struct DecGemv {
   float sh_scale;
   int nsh;
   int* sh_cnt;                 // monotonic count of finished shrink CTAs (0 at decode start)
+  int split;                   // DEC_RESID (set by dec_gemv_launch): a "pair" is one row's two
+                               // K halves, so twice as many warps stream the (short) matrix
 };
 inline int dec_shrink_ctas(int nt, int r) { return ((nt * r + 7) / 8) * DEC_TSPLIT; }
 struct DecAttn {
