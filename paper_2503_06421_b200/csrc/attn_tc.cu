@@ -40,6 +40,11 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <map>
+#include <mutex>
+#include <queue>
+#include <vector>
+
 #include <cstdint>
 #include <cstdlib>
 
@@ -96,6 +101,13 @@ __device__ __forceinline__ void adbg(const AttnParams& p, int tile, int slot) {
     asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
     p.dbg[((size_t)blockIdx.x * ADBG_TILES + tile) * 8 + slot] = t;
   }
+}
+// paired-kernel timeline (same buffer): per CTA, per pair item (first 64), 8
+// slots: 0 producer issues Q, 1 MMA wants S(0), 2 MMA issued S_B(0),
+// 3 MMA issued PV_A(0) (after o_empty), 4 softmax B sees S(0), 5 softmax B
+// stored P(0), 6 MMA issued the item's last PV, 7 epilogue drained O_B
+__device__ __forceinline__ void pdbg(const AttnParams& p, int item, int slot) {
+  adbg(p, item, slot);
 }
 // Work item i of this CTA (round-robin rounds, snake order so that the CTAs
 // taking the heaviest item of one round take the lightest of the next);
@@ -464,10 +476,17 @@ __device__ __forceinline__ void setmaxnreg_dec_48() {
 __device__ __forceinline__ bool pair_at(const AttnParams& p, int nq, int round, Item& it) {
   const int G = gridDim.x;
   const int c = blockIdx.x;
-  const int idx = round * G + ((round & 1) ? G - 1 - c : c);
   const int per = p.H * p.nseq;
   const int npair = (nq + 1) / 2;
-  if (idx >= npair * per) return false;
+  int idx;
+  if (p.sched) {  // host LPT schedule: this CTA's items, heaviest first
+    const int o0 = __ldg(p.sched + c), o1 = __ldg(p.sched + c + 1);
+    if (round >= o1 - o0) return false;
+    idx = __ldg(p.sched + G + 1 + o0 + round);
+  } else {
+    idx = round * G + ((round & 1) ? G - 1 - c : c);
+    if (idx >= npair * per) return false;
+  }
   const int k = idx / per, rem = idx - k * per;
   it.qt = nq - 1 - 2 * k;  // B
   it.h = rem % p.H;
@@ -546,6 +565,7 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
           const int qt = it.qt - 1 + x;
           if (qt < 0) continue;
           ptx::mbar_wait(q_empty(x), (nx[x] & 1) ^ 1);
+          if (x == 1) pdbg(p, i, 0);
           ptx::mbar_expect_tx(q_full(x), TILE);
           const uint32_t qs = sb + OFF_Q + x * TILE;
           ptx::tma_load_2d(&p.q, qs, q_full(x), qc, base + qt * BQ);
@@ -590,25 +610,34 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
         }
         ++np[x];
       };
+      // S_A(0) of an item is issued during the previous item's last step (it
+      // needs only Q_A and K_0 of the new item, both loaded by then), so softmax
+      // A starts the new item while softmax B finishes the old one
+      bool a_pre = false;
+      static_assert(KST >= 2, "the next item's K_0 needs a free K slot");
+      const bool pre_ok = p.variant != 3;  // 3: no cross-item S_A(0) (A/B diagnostic)
       for (int i = 0; pair_at(p, nq, i, it); ++i) {
         const int nb = it.qt + 1, na = it.qt;  // key tiles of B and A (A absent: 0)
+        pdbg(p, i, 1);
         // S_A(0), S_B(0) from K_0
         {
           const int s = kc % KST;
           ptx::mbar_wait(k_full(s), (kc / KST) & 1);
           const uint32_t ks = sb + OFF_K + s * TILE;
-          if (na > 0) {
+          if (na > 0 && !a_pre) {
             ptx::mbar_wait(q_full(0), ni[0] & 1);
             ptx::tc_fence_after();
             issue_s(0, ks);
             if (na == 1) ptx::mma_commit(q_empty(0));
           }
+          a_pre = false;
           ptx::mbar_wait(q_full(1), ni[1] & 1);
           ptx::tc_fence_after();
           issue_s(1, ks);
           if (nb == 1) ptx::mma_commit(q_empty(1));
           ptx::mma_commit(k_empty(s));
           ++kc;
+          pdbg(p, i, 2);
         }
         for (int j = 0; j < nb; ++j) {
           const int t = vc % VST;
@@ -622,6 +651,7 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
             if (j == 0 && ni[0] > 0) ptx::mbar_wait(o_empty(0), (ni[0] - 1) & 1);
             ptx::tc_fence_after();
             issue_pv(0, vs, j > 0);
+            if (j == 0) pdbg(p, i, 3);
             if (j == na - 1) ptx::mma_commit(o_full(0));
             if (j + 1 < na) {
               ptx::mbar_wait(k_full(s), (kc / KST) & 1);
@@ -630,13 +660,28 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
               if (j + 1 == na - 1) ptx::mma_commit(q_empty(0));
             }
           }
+          if (!more && pre_ok) {
+            Item nx;
+            if (pair_at(p, nq, i + 1, nx) && nx.qt > 0) {  // next item's S_A(0)
+              const int s2 = kc % KST;
+              ptx::mbar_wait(k_full(s2), (kc / KST) & 1);
+              ptx::mbar_wait(q_full(0), (ni[0] + (na > 0 ? 1 : 0)) & 1);
+              ptx::tc_fence_after();
+              issue_s(0, sb + OFF_K + s2 * TILE);
+              if (nx.qt == 1) ptx::mma_commit(q_empty(0));
+              a_pre = true;
+            }
+          }
           ptx::mbar_wait(p_full(1), np[1] & 1);
           if (j == 0 && ni[1] > 0) ptx::mbar_wait(o_empty(1), (ni[1] - 1) & 1);
           ptx::tc_fence_after();
           issue_pv(1, vs, j > 0);
           ptx::mma_commit(v_empty(t));
           ++vc;
-          if (!more) ptx::mma_commit(o_full(1));
+          if (!more) {
+            ptx::mma_commit(o_full(1));
+            pdbg(p, i, 6);
+          }
           if (more) {
             ptx::mbar_wait(k_full(s), (kc / KST) & 1);
             ptx::tc_fence_after();
@@ -679,6 +724,7 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
           if (c == 3) {
             ptx::tc_fence_before();
             ptx::mbar_arrive(o_empty(x));
+            if (x == 1 && threadIdx.x == 3 * 128) pdbg(p, i, 7);
           }
           if (qi < p.S) {
 #pragma unroll
@@ -714,6 +760,7 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
       for (int j = 0; j < nkv; ++j, ++gt) {
         ptx::mbar_wait(s_full(x), gt & 1);
         ptx::tc_fence_after();
+        if (x == 1 && j == 0 && threadIdx.x == 2 * 128) pdbg(p, i, 4);
         // all 128 scores of the row in registers (one TMEM round trip)
         const bool diag = j == qt;  // the diagonal tile: causal mask key > qi
         const int kq = qi - j * BKV;
@@ -782,6 +829,7 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full(x));
+        if (x == 1 && j == 0 && threadIdx.x == 2 * 128) pdbg(p, i, 5);
       }
       lsum[(x * 2 + (ni & 1)) * BQ + row] = l;
       ptx::mbar_arrive(l_ready(x, ni & 1));
@@ -838,7 +886,81 @@ static cudaError_t attn_set_attr() {
 // us; S = 8192: 775 vs 735 us, tools/attn_bench.py): the per-tile softmax is
 // not latency-hidden by more warps — the extra row-max exchange and barrier
 // of 512 threads cost more than they hide.
-static cudaError_t attn_pp_launch(const AttnParams& p, cudaStream_t s, int grid) {
+// Longest-processing-time schedule of the pair items over the grid: items
+// (numbered as pair_at's snake order: k = idx / (H nseq) the pair rank,
+// heaviest first) cost their key-tile steps (qt + 1 for B, qt for A) plus ~3
+// steps of per-item fill / drain (tools/attn_pp_trace.py: 13B S = 2048 items
+// take ~1.4 us per step plus ~3 us at the item boundary); each goes to the
+// CTA with the least load so far, so every CTA's list stays heaviest first.
+// The static snake order left the last CTA ~15 % behind the mean at S =
+// 2048.  One table per (S, H, nseq, grid, device), built once and kept.
+static const int* attn_schedule(int nq, int per, int grid) {
+  struct Key {
+    int nq, per, grid, dev;
+    bool operator<(const Key& o) const {
+      return nq != o.nq ? nq < o.nq : per != o.per ? per < o.per : grid != o.grid ? grid < o.grid : dev < o.dev;
+    }
+  };
+  static std::mutex mu;
+  static std::map<Key, int*> cache;
+  int dev = 0;
+  cudaGetDevice(&dev);
+  std::lock_guard<std::mutex> lk(mu);
+  const Key key{nq, per, grid, dev};
+  auto f = cache.find(key);
+  if (f != cache.end()) return f->second;
+  const int npair = (nq + 1) / 2, n = npair * per;
+  std::vector<std::vector<int>> lists(grid);
+  std::vector<long> load(grid, 0);
+  // min-heap of (load, cta): ties to the lower CTA index
+  std::priority_queue<std::pair<long, int>, std::vector<std::pair<long, int>>,
+                      std::greater<std::pair<long, int>>> heap;
+  for (int c = 0; c < grid; ++c) heap.push({0, c});
+  for (int idx = 0; idx < n; ++idx) {  // already heaviest first
+    const int qt = nq - 1 - 2 * (idx / per);
+    const long cost = (qt + 1) + qt + 3;
+    auto top = heap.top();
+    heap.pop();
+    lists[top.second].push_back(idx);
+    heap.push({top.first + cost, top.second});
+  }
+  std::vector<int> h(grid + 1 + n);
+  int o = 0;
+  for (int c = 0; c < grid; ++c) {
+    h[c] = o;
+    for (int idx : lists[c]) h[grid + 1 + o++] = idx;
+  }
+  h[grid] = o;
+  // may run while the caller's stream is being captured into a CUDA graph:
+  // relaxed capture mode for this thread, and the upload on a private
+  // non-blocking stream (never the capturing one, never the legacy stream)
+  cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  int* d = nullptr;
+  cudaStream_t up = nullptr;
+  bool ok = cudaMalloc(&d, h.size() * sizeof(int)) == cudaSuccess &&
+            cudaStreamCreateWithFlags(&up, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaMemcpyAsync(d, h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice, up) ==
+                cudaSuccess &&
+            cudaStreamSynchronize(up) == cudaSuccess;
+  if (up) cudaStreamDestroy(up);
+  cudaThreadExchangeStreamCaptureMode(&mode);
+  if (!ok) {
+    cudaGetLastError();
+    if (d) cudaFree(d);
+    return nullptr;  // the kernel falls back to the snake order
+  }
+  cache[key] = d;
+  return d;
+}
+
+static cudaError_t attn_pp_launch(const AttnParams& p0, cudaStream_t s, int grid) {
+  AttnParams p = p0;
+  static const bool lpt_off = [] {
+    const char* e = getenv("TIDAL_ATTN_LPT");
+    return e && e[0] == '0';
+  }();
+  p.sched = lpt_off ? nullptr : attn_schedule((p.S + BQ - 1) / BQ, p.H * p.nseq, grid);
   static bool attr = false;
   if (!attr) {
     cudaError_t e = cudaFuncSetAttribute(attn_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -859,21 +981,21 @@ cudaError_t attn_tc_launch(const AttnParams& p, cudaStream_t s) {
     cudaGetDevice(&dev);
     if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess) sms = 148;
   }
-  // TIDAL_ATTN=1 / 2: force single tiles / pairs (A/B; the adbg trace is in
-  // the single-tile kernel)
-  static int forced = -1;
-  if (forced < 0) {
-    const char* e = getenv("TIDAL_ATTN");
-    forced = e ? atoi(e) : 0;
-  }
+  // TIDAL_ATTN=1 / 2 / 3: force single tiles / pairs / pairs without the
+  // cross-item S_A(0) (A/B; with TIDAL_ATTN_TRACE, 2 and 3 trace the paired kernel)
+  const char* fe = getenv("TIDAL_ATTN");  // read per launch: tests switch it
+  const int forced = fe ? atoi(fe) : 0;
   const int variant = p.variant ? p.variant : forced;
   // pairs of query tiles unless there are too few pairs to fill the SMs about
   // 1.25 times (13B, H = 40, tools/attn_bench.py: paired 22.6 / 28.2 / 59.9 /
   // 175 / 638 us against single 20.0 / 32.0 / 64.6 / 205 / 764 us at S = 867 /
   // 1154 / 2048 / 4096 / 8192 — 160 pairs on 148 SMs quantise badly)
   const long pairs = (long)((p.S + BQ - 1) / BQ + 1) / 2 * p.H * p.nseq;
-  if (!p.dbg && (variant == 2 || (variant == 0 && 4 * pairs >= 5L * sms)))
-    return attn_pp_launch(p, s, (int)(pairs < sms ? pairs : sms));
+  if (variant == 2 || variant == 3 || (!p.dbg && variant == 0 && 4 * pairs >= 5L * sms)) {
+    AttnParams q = p;
+    q.variant = variant;  // 3: pairs without the cross-item S_A(0) (A/B)
+    return attn_pp_launch(q, s, (int)(pairs < sms ? pairs : sms));
+  }
   const long items = (long)((p.S + BQ - 1) / BQ) * p.H * p.nseq;  // persistent: <= one CTA per SM
   const int grid = (int)(items < sms ? items : sms);
   if (grid <= 0) return cudaSuccess;

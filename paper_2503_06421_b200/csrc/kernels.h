@@ -141,6 +141,8 @@ struct alignas(64) AttnParams {
   int ldo;
   unsigned long long* dbg;  // diagnostic per-tile timeline (TIDAL_ATTN_TRACE); null in production
   int variant;  // 0: by size (pairs of query tiles when >= 2 rounds), 1: single tiles, 2: pairs
+  const int* sched;  // paired kernel (set by attn_tc_launch): per-CTA pair-item lists,
+                     // [G + 1] offsets then the item indices (host LPT schedule)
 };
 bool attn_tc_params(AttnParams* p, const bf16* qkv, const bf16* vt, int vt_ld, bf16* out, int S,
                     int H, int KV, int nseq = 1);

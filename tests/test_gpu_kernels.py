@@ -249,14 +249,18 @@ def test_attention_causal_gqa(T, S, H, KV, hd):
     _close_rows_bf16(_host(O), ref)
 
 
-@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
 @pytest.mark.parametrize("S,H,KV", [(1, 2, 1), (128, 2, 2), (129, 1, 1), (300, 4, 2), (640, 2, 1),
-                                    (1000, 3, 1), (2048, 2, 2)])
+                                    (1000, 3, 1), (2048, 2, 2), (256, 300, 100),
+                                    (384, 150, 50)])
 def test_attention_tcgen05(T, S, H, KV, variant, monkeypatch):
     """The tcgen05/TMEM attention (hd = 128) against the oracle; V passed
     transposed as the QKV epilogue writes it.  variant 1: one query tile per
     item; 2: pairs of query tiles (odd tile counts leave the first pair with
-    one tile: S = 1, 300, 640)."""
+    one tile: S = 1, 300, 640), each item's S_A(0) issued during the previous
+    item's last step; 3: pairs without that cross-item issue.  (256, 300,
+    100) and (384, 150, 50) have more pairs than SMs, so CTAs cross item
+    boundaries (S = 384: the A-absent pairs come last)."""
     monkeypatch.setenv("TIDAL_ATTN", variant)
     hd = 128
     rng = np.random.default_rng(S * 7 + H)
@@ -273,7 +277,7 @@ def test_attention_tcgen05(T, S, H, KV, variant, monkeypatch):
     _close_rows_bf16(_host(O), ref)
 
 
-@pytest.mark.parametrize("variant", ["1", "2"])
+@pytest.mark.parametrize("variant", ["1", "2", "3"])
 def test_attention_tcgen05_large_logits(T, variant, monkeypatch):
     """Scores spanning > 2^8 in exp2 units exercise the lazy O rescale."""
     monkeypatch.setenv("TIDAL_ATTN", variant)

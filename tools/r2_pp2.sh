@@ -1,9 +1,8 @@
-# ping-pong attention: exp2 split between MUFU and FMA (TIDAL_ATTN_EMU), pipelined head GEMV
-mkdir -p gpurun_out
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
-for emu in 0 2 4; do TIDAL_ATTN_EMU=$emu timeout 600 python -m pytest tests/test_gpu_kernels.py -q -m gpu -k "attention or head" -x 2>&1 | tail -1; done
-for i in 1 2; do
-  echo "single"; TIDAL_ATTN=1 timeout 300 python tools/attn_bench.py --S 867 2048 8192
-  for emu in 0 2 3 4; do echo "pp emu=$emu"; TIDAL_ATTN_EMU=$emu timeout 300 python tools/attn_bench.py --S 867 2048 8192; done
-done
-timeout 600 ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum --clock-control none -k regex:head_kernel python -m pytest tests/test_gpu_kernels.py -q -m gpu -k "head_logits" 2>&1 | grep -E "head_kernel|duration|dram" | head -8
+# cross-item S_A(0) in the paired attention: parity (variants 1/2/3) + A/B timing + trace
+mkdir -p gpurun_out/pp
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
+timeout 900 python -m pytest tests/test_gpu_kernels.py -q -x -k "attention" 2>&1 | tail -3
+timeout 900 python -m pytest tests/test_gpu_e2e.py -q -x -k "batch" 2>&1 | tail -2
+for r in 1 2; do for v in 2 3; do TIDAL_ATTN=$v timeout 300 python tools/attn_bench.py --S 867 1154 2048 4096 8192 --reps 10 | sed "s/^/v$v /"; done; done
+TIDAL_ATTN=2 TIDAL_ATTN_TRACE=gpurun_out/pp/t2048.bin timeout 300 python tools/attn_bench.py --S 2048 --reps 1 | tail -1
+python tools/attn_pp_trace.py gpurun_out/pp/t2048.bin 2048 40
