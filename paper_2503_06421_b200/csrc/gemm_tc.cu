@@ -953,11 +953,12 @@ void gemm_plan_resid(int M, int N, int K, int num_sms, int* bn_out, int* ks_out,
       const long tiles = mt * ((N + bn - 1) / bn);
       if (tiles * mc * cg > GEMM_MAX_FLAGS) continue;
       // with one or two M tiles the K-block rate is bound by each SM's operand
-      // stream (A + B bytes), not the MMA: a 192-wide K-block then costs ~0.8
+      // stream (A + B bytes), not the MMA: a 192-wide K-block then costs ~0.75
       // of a 256-wide one (13B S = 256: O 192 x 2 parts 25.5-26 us vs 256 x 3
-      // 33.5 us; down 192 x 2 46.4 us vs 256 x 3 51.6 us)
+      // 33.5 us; down 192 x 2 45.7-46.4 us vs 256 x 3 51.6-51.7 us; at 0.8 the
+      // 2 % hysteresis below kept down at 256 x 3, profiles/short_r02.txt)
       const bool stream_bound = M <= 2 * BM * 2;
-      const double kb_cost = (bn == 128 ? 0.75 : (bn == 192 && stream_bound ? 0.8 : 1.0)) *
+      const double kb_cost = (bn == 128 ? 0.75 : (bn == 192 && stream_bound ? 0.75 : 1.0)) *
                              (cg == 1 ? 1.03 : 1.0);
       for (int ks = 1; ks <= (split_ok ? 8 : 1) && ks <= nk; ++ks) {
         const int kps = (nk + ks - 1) / ks;

@@ -1,0 +1,8 @@
+# residual planner at stream-bound M (192-wide K-block cost 0.75): same-box A/B against HEAD~ built under ab/old
+python -c "import __graft_entry__ as g; g.build()" > /dev/null 2>&1 || exit 1
+timeout 600 python -m pytest tests/test_gpu_kernels.py -q -x -k "resid or split" 2>&1 | tail -1
+timeout 900 python -m pytest tests/test_gpu_e2e.py -q -x 2>&1 | tail -1
+for r in 1 2 3; do for S in 256 512; do
+  timeout 300 python tools/warm.py --seq $S --steps 10 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('new', d['seq'], round(d['mean_ms'],3), round(d['median_ms'],3), d['token'])"
+  (cd ab/old && timeout 300 python tools/warm.py --seq $S --steps 10 | python -c "import json,sys; d=json.loads(sys.stdin.read()); print('old', d['seq'], round(d['mean_ms'],3), round(d['median_ms'],3), d['token'])")
+done; done
