@@ -234,6 +234,8 @@ def main():
     ap.add_argument("--seq", type=int, default=2048)
     ap.add_argument("--rank", type=int, default=16)
     ap.add_argument("--rho", default="eq1")
+    ap.add_argument("--eq1-adapter", default="on", choices=["on", "off"],
+                    help="count the streamed adapter's bytes in Eq. 1 (reading A7b)")
     ap.add_argument("--policy", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-sweep", action="store_true")
@@ -364,8 +366,17 @@ def main():
         sweep[f"warm_rho1_allreduce_{other}"] = max_over_ranks(statistics.mean(w2))
         tpl.set_allreduce_dtype(T.DTYPE_BF16 if args.allreduce == "bf16" else T.DTYPE_F32)
     # (3) template size
+    # Eq. 1 balances loading against inference: every
+    # invocation also streams its dynamic adapter (never template-resident),
+    # so those bytes take their share of T_TTFT x B_PCIe and the template
+    # absorbs it (reading A7b): M_prefetch = max(M_model +
+    # M_adapter - T_TTFT x B_PCIe, 0), passed to the planner's Eq. 1 as
+    # T' = T_TTFT - M_adapter / B_PCIe.  --eq1-adapter off: the adapter ignored.
+    t_eq1 = t_warm / 1e3
+    if args.eq1_adapter == "on" and r:
+        t_eq1 = max(t_eq1 - anb / b_h2d, 0.0)
     if args.rho == "eq1":
-        tpl.resize(T.template_opts(eq1=True, t_ttft_s=t_warm / 1e3, b_pcie_Bps=b_h2d))
+        tpl.resize(T.template_opts(eq1=True, t_ttft_s=t_eq1, b_pcie_Bps=b_h2d))
     else:
         M = sum(s.nbytes for s in synth.base_tensors(cfg)) // world
         tpl.resize(T.template_opts(resident_bytes=int(float(args.rho) * M)))
@@ -510,7 +521,8 @@ def main():
         "higher_is_better": False, "scaling": "strong", "vs_baseline": None, "dtype": "bf16",
         "data": "synthetic (seeded splitmix64 random-init bf16 weights + LoRA, uniform prompt)",
         "config": {"workload": workload_name(args.config, S, r),
-                   "seq_len": S, "lora_rank": r, "resident_rule": args.rho,
+                   "seq_len": S, "lora_rank": r, "resident_rule": (args.rho + ("+adapter" if args.eq1_adapter == "on" and r else ""))
+                   if args.rho == "eq1" else args.rho,
                    "rho": s0["bytes_resident"] / max(1, s0["bytes_resident"] + s0["bytes_streamed"]),
                    "group_policy": args.policy, "parallelism": f"tp{world}" if world > 1 else "single",
                    "l2": "flushed before every step (512 MB write, outside the timed window)"},
@@ -539,6 +551,8 @@ def main():
         "sweep_ms": sweep,
         "clocks": clk.summary(),
         "eq1": {"t_warm_ms": t_warm, "b_h2d_GBps": b_h2d / 1e9,
+                "adapter_bytes_per_rank": anb if r else 0, "t_ttft_ms_passed": t_eq1 * 1e3,
+                "adapter_counted": args.eq1_adapter == "on",
                 "t_warm_protocol": f"mean of {n_warm} back-to-back rho=1 steps after "
                                    f"{args.warmup} warm-up, L2 flushed, no profiling events"},
         "tp": tp_info,
