@@ -1,3 +1,5 @@
+# NOTE: measured with an experimental patch that was not kept (see DESIGN.md 7d and
+# profiles/short_r02.txt); the flags it uses no longer exist in the tree.
 # row-major vs K-block-major weight boxes (DRAM locality), 13B GEMMs at S = 256 / 867 / 2048
 mkdir -p gpurun_out/layout
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }

@@ -1,3 +1,5 @@
+# NOTE: measured with an experimental patch that was not kept (see DESIGN.md 7d and
+# profiles/short_r02.txt); the flags it uses no longer exist in the tree.
 # A/B: weight boxes issued before griddepcontrol.wait (TIDAL_GEMM_PRE / _PREPF), warm rho = 1
 mkdir -p gpurun_out/pre
 python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build.log 2>&1 || { cat gpurun_out/build.log; exit 1; }
