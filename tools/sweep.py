@@ -28,11 +28,15 @@ ap.add_argument("--config", default="13b")
 ap.add_argument("--S", type=int, nargs="*", default=None, help="override prompt lengths")
 ap.add_argument("--rho", type=float, nargs="*", default=None, help="override resident fractions")
 ap.add_argument("--out", default=os.path.join(ROOT, "gpurun_out", "sweep.jsonl"))
+ap.add_argument("--eq1", action="store_true",
+                help="template sized by Eq. 1 per S (warm TTFT measured first, adapter counted)")
 args = ap.parse_args()
 
 cfg = synth.config(args.config)
 P, _ = bench.peaks()
-if args.config == "7b":
+if args.eq1:  # rho < 0: Eq. 1 (bench.py's rule, reading A7b)
+    pts = [(S, 0 if args.config == "7b" else 16, -1.0) for S in (args.S or (256, 867, 1154, 2048, 4096, 8192))]
+elif args.config == "7b":
     pts = [(2048, 0, rho) for rho in (0.0, 1.0)]
 else:
     pts = [(S, 16, rho) for S in (args.S or (256, 867, 2048, 6101, 8192))
@@ -79,7 +83,15 @@ b_h2d = (st["bytes_streamed"] + st["bytes_adapter"]) / ((st["h2d_last_ms"] - st[
 os.makedirs(os.path.dirname(args.out), exist_ok=True)
 with open(args.out, "a") as f:
     for S, r, rho in pts:
-        tpl.resize(T.template_opts(resident_bytes=T.U64_MAX if rho >= 1 else int(rho * M)))
+        t_warm = None
+        if rho < 0:  # Eq. 1: warm TTFT at this S, then M_prefetch = M + M_adapter - T x B
+            tpl.resize(T.template_opts(resident_bytes=T.U64_MAX))
+            t_warm = statistics.median(s["device_ms"] for s in run(S, r, T.DEBUG_SCRUB_L2))
+            anb = adapters[r][1] if r else 0
+            t_eq1 = max(t_warm / 1e3 - anb / b_h2d, 0.0)
+            tpl.resize(T.template_opts(eq1=True, t_ttft_s=t_eq1, b_pcie_Bps=b_h2d))
+        else:
+            tpl.resize(T.template_opts(resident_bytes=T.U64_MAX if rho >= 1 else int(rho * M)))
         sts = run(S, r, T.DEBUG_SCRUB_L2)
         ms = statistics.median(s["device_ms"] for s in sts)
         streamed = sts[0]["bytes_streamed"] + sts[0]["bytes_adapter"]
@@ -91,7 +103,8 @@ with open(args.out, "a") as f:
         t_hbm = w_bytes / (P["hbm_gbs"] * 1e9) * 1e3   # every weight read once from HBM
         roof = max(t_pcie, t_tc, t_hbm)
         bound = max((("pcie", t_pcie), ("tensor", t_tc), ("hbm", t_hbm)), key=lambda kv: kv[1])[0]
-        line = {"config": args.config, "S": S, "lora_rank": r, "rho_requested": rho,
+        line = {"config": args.config, "S": S, "lora_rank": r,
+                "rho_requested": "eq1" if rho < 0 else rho, "t_warm_ms": t_warm,
                 "rho_realized": sts[0]["bytes_resident"] / M, "ttft_ms": ms,
                 "tokens_per_s": S / (ms / 1e3), "t_pcie_ms": t_pcie, "t_tensor_ms": t_tc,
                 "t_tensor_sustained_ms": t_tc_sus, "t_hbm_ms": t_hbm, "roof_ms": roof,
