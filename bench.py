@@ -182,6 +182,15 @@ def run_reference(args):
         "e2e": {"value": ms, "unit": "ms", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
 
 
+def eq1_t_ttft(t_warm_s, adapter_bytes, b_pcie_Bps):
+    """The T_TTFT handed to the planner's Eq. 1 (M_prefetch =
+    max(M_model - T_TTFT x B_PCIe, 0)) so that it sizes the template for the
+    invocation's whole footprint, base weights plus a dynamic adapter that
+    always streams (reading A7b): M_model + M_adapter - T x B =
+    M_model - (T - M_adapter / B) x B."""
+    return max(t_warm_s - adapter_bytes / b_pcie_Bps, 0.0)
+
+
 def _free_port():
     with socket.socket() as sk:
         sk.bind(("127.0.0.1", 0))
@@ -372,9 +381,7 @@ def main():
     # absorbs it (reading A7b): M_prefetch = max(M_model +
     # M_adapter - T_TTFT x B_PCIe, 0), passed to the planner's Eq. 1 as
     # T' = T_TTFT - M_adapter / B_PCIe.  --eq1-adapter off: the adapter ignored.
-    t_eq1 = t_warm / 1e3
-    if args.eq1_adapter == "on" and r:
-        t_eq1 = max(t_eq1 - anb / b_h2d, 0.0)
+    t_eq1 = eq1_t_ttft(t_warm / 1e3, anb if (args.eq1_adapter == "on" and r) else 0, b_h2d)
     if args.rho == "eq1":
         tpl.resize(T.template_opts(eq1=True, t_ttft_s=t_eq1, b_pcie_Bps=b_h2d))
     else:

@@ -41,3 +41,18 @@ def test_reference_arm_rank_nonzero_exits_clean():
     p = _run(["--impl", "reference", "--gpus", "2"], env={"WORLD_SIZE": "2", "RANK": "1",
                                                           "LOCAL_RANK": "1"})
     assert p.returncode == 0 and p.stdout.strip() == ""
+
+
+def test_eq1_counts_the_adapter():
+    """Reading A7b: with an adapter of A bytes streaming every invocation,
+    Eq. 1 (M_prefetch = max(M - T B, 0)) is applied to M + A, i.e. the planner
+    gets T' = T - A / B; T' x B + A = T x B bytes cross PCIe in T."""
+    sys.path.insert(0, ROOT)
+    import bench
+    B = 55.5e9
+    assert bench.eq1_t_ttft(0.045, 0, B) == 0.045
+    t = bench.eq1_t_ttft(0.045, 125173760, B)
+    assert abs(t * B + 125173760 - 0.045 * B) < 1.0
+    M = 26_030_000_000
+    assert abs((M + 125173760 - 0.045 * B) - (M - t * B)) < 1.0   # same M_prefetch
+    assert bench.eq1_t_ttft(0.001, 10**9, B) == 0.0                 # clamped like Eq. 1
