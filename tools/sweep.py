@@ -88,7 +88,7 @@ with open(args.out, "a") as f:
             tpl.resize(T.template_opts(resident_bytes=T.U64_MAX))
             t_warm = statistics.median(s["device_ms"] for s in run(S, r, T.DEBUG_SCRUB_L2))
             anb = adapters[r][1] if r else 0
-            t_eq1 = max(t_warm / 1e3 - anb / b_h2d, 0.0)
+            t_eq1 = bench.eq1_t_ttft(t_warm / 1e3, anb, b_h2d)
             tpl.resize(T.template_opts(eq1=True, t_ttft_s=t_eq1, b_pcie_Bps=b_h2d))
         else:
             tpl.resize(T.template_opts(resident_bytes=T.U64_MAX if rho >= 1 else int(rho * M)))
