@@ -461,6 +461,22 @@ constexpr int NTH = 512;
 constexpr uint32_t COL_SX = 0, COL_OX = 256;  // + X * 128
 }  // namespace pp
 
+// packed two-lane fp32 math (FFMA2 / FADD2 on sm_100a): half the issue slots
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
 __device__ __forceinline__ void setmaxnreg_inc_176() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 176;" ::: "memory");
 }
@@ -805,7 +821,8 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
         // P = 2^(s*scale - m) -> packed bf16 pairs over the first 64 columns of
         // S_X; chunk c lands on columns [16c, 16c+16), whose scores are in
         // registers already (masked scores are -inf: 2^-inf = 0)
-        float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+        float2 ls2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m_used, -m_used);
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
           uint32_t pk[16];
@@ -813,10 +830,11 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
           for (int u = 0; u < 4; ++u) {
             float e[8];
 #pragma unroll
-            for (int k = 0; k < 8; ++k) {
-              const float a = fmaf(v[c * 32 + u * 8 + k], p.scale_log2, -m_used);
-              e[k] = ptx::ex2(a);
-              ls[k] += e[k];
+            for (int k = 0; k < 8; k += 2) {
+              const float2 a = ffma2(make_float2(v[c * 32 + u * 8 + k], v[c * 32 + u * 8 + k + 1]), sc2, nm2);
+              e[k] = ptx::ex2(a.x);
+              e[k + 1] = ptx::ex2(a.y);
+              ls2[k >> 1] = fadd2(ls2[k >> 1], make_float2(e[k], e[k + 1]));
             }
             pk[4 * u + 0] = pack_bf16x2(e[0], e[1]);
             pk[4 * u + 1] = pack_bf16x2(e[2], e[3]);
@@ -825,7 +843,8 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
           }
           ptx::tmem_st16(s_col + c * 16, pk);
         }
-        l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+        l += ((ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y)) +
+             ((ls2[2].x + ls2[2].y) + (ls2[3].x + ls2[3].y));
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full(x));
