@@ -91,6 +91,22 @@ struct Item {
   int qt, h, z;
 };
 
+// packed two-lane fp32 math (FFMA2 / FADD2 on sm_100a): half the issue slots
+__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
+        "l"(*reinterpret_cast<unsigned long long*>(&c)));
+  return *reinterpret_cast<float2*>(&r);
+}
+__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;"
+      : "=l"(r)
+      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
+  return *reinterpret_cast<float2*>(&r);
+}
 // diagnostic timeline (AttnParams::dbg): per CTA, per S/P tile (first 64), 8
 // slots: 0 MMA wants S, 1 S issued, 2 softmax sees S, 3 softmax done (P),
 // 4 MMA wants PV, 5 PV issued
@@ -387,15 +403,19 @@ __global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __gr
         // P buffer b was last read by the PV of tile gt-2
         if (gt >= 2) ptx::mbar_wait(pv_done(b), ((gt - 2) >> 1) & 1);
         // P = 2^(s*scale - m) -> packed bf16 pairs, COLS / 2 TMEM columns per group
-        float ls[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};  // independent sum chains
+        // independent sum chains, two lanes per packed FADD2
+        float2 ls2[4] = {{0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}, {0.f, 0.f}};
+        const float2 sc2 = make_float2(p.scale_log2, p.scale_log2), nm2 = make_float2(-m_used, -m_used);
         uint32_t pk[COLS / 2];
 #pragma unroll
         for (int c = 0; c < COLS / 8; ++c) {
           float e[8];
 #pragma unroll
-          for (int k = 0; k < 8; ++k) {
-            e[k] = ptx::ex2(fmaf(v[c * 8 + k], p.scale_log2, -m_used));
-            ls[k] += e[k];
+          for (int k = 0; k < 8; k += 2) {
+            const float2 a = ffma2(make_float2(v[c * 8 + k], v[c * 8 + k + 1]), sc2, nm2);
+            e[k] = ptx::ex2(a.x);
+            e[k + 1] = ptx::ex2(a.y);
+            ls2[k >> 1] = fadd2(ls2[k >> 1], make_float2(e[k], e[k + 1]));
           }
           pk[4 * c + 0] = pack_bf16x2(e[0], e[1]);
           pk[4 * c + 1] = pack_bf16x2(e[2], e[3]);
@@ -407,7 +427,8 @@ __global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __gr
           ptx::tmem_st32(tmem + lane_base + COL_P + b * 64 + half * 32, pk);
         else
           ptx::tmem_st16(tmem + lane_base + COL_P + b * 64 + half * 16, pk);
-        l += ((ls[0] + ls[1]) + (ls[2] + ls[3])) + ((ls[4] + ls[5]) + (ls[6] + ls[7]));
+        l += ((ls2[0].x + ls2[0].y) + (ls2[1].x + ls2[1].y)) +
+             ((ls2[2].x + ls2[2].y) + (ls2[3].x + ls2[3].y));
         ptx::tmem_st_wait();
         ptx::tc_fence_before();
         ptx::mbar_arrive(p_full(b));
@@ -461,22 +482,6 @@ constexpr int NTH = 512;
 constexpr uint32_t COL_SX = 0, COL_OX = 256;  // + X * 128
 }  // namespace pp
 
-// packed two-lane fp32 math (FFMA2 / FADD2 on sm_100a): half the issue slots
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
-}
 __device__ __forceinline__ void setmaxnreg_inc_176() {
   asm volatile("setmaxnreg.inc.sync.aligned.u32 176;" ::: "memory");
 }
