@@ -91,22 +91,6 @@ struct Item {
   int qt, h, z;
 };
 
-// packed two-lane fp32 math (FFMA2 / FADD2 on sm_100a): half the issue slots
-__device__ __forceinline__ float2 ffma2(float2 a, float2 b, float2 c) {
-  unsigned long long r;
-  asm("fma.rn.f32x2 %0, %1, %2, %3;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)),
-        "l"(*reinterpret_cast<unsigned long long*>(&c)));
-  return *reinterpret_cast<float2*>(&r);
-}
-__device__ __forceinline__ float2 fadd2(float2 a, float2 b) {
-  unsigned long long r;
-  asm("add.rn.f32x2 %0, %1, %2;"
-      : "=l"(r)
-      : "l"(*reinterpret_cast<unsigned long long*>(&a)), "l"(*reinterpret_cast<unsigned long long*>(&b)));
-  return *reinterpret_cast<float2*>(&r);
-}
 // diagnostic timeline (AttnParams::dbg): per CTA, per S/P tile (first 64), 8
 // slots: 0 MMA wants S, 1 S issued, 2 softmax sees S, 3 softmax done (P),
 // 4 MMA wants PV, 5 PV issued
@@ -412,10 +396,10 @@ __global__ void __launch_bounds__(ACfg<SPLIT>::NTH, 1) attn_tc_kernel(const __gr
           float e[8];
 #pragma unroll
           for (int k = 0; k < 8; k += 2) {
-            const float2 a = ffma2(make_float2(v[c * 8 + k], v[c * 8 + k + 1]), sc2, nm2);
+            const float2 a = ptx::ffma2(make_float2(v[c * 8 + k], v[c * 8 + k + 1]), sc2, nm2);
             e[k] = ptx::ex2(a.x);
             e[k + 1] = ptx::ex2(a.y);
-            ls2[k >> 1] = fadd2(ls2[k >> 1], make_float2(e[k], e[k + 1]));
+            ls2[k >> 1] = ptx::fadd2(ls2[k >> 1], make_float2(e[k], e[k + 1]));
           }
           pk[4 * c + 0] = pack_bf16x2(e[0], e[1]);
           pk[4 * c + 1] = pack_bf16x2(e[2], e[3]);
@@ -836,10 +820,10 @@ __global__ void __launch_bounds__(pp::NTH, 1) attn_pp_kernel(const __grid_consta
             float e[8];
 #pragma unroll
             for (int k = 0; k < 8; k += 2) {
-              const float2 a = ffma2(make_float2(v[c * 32 + u * 8 + k], v[c * 32 + u * 8 + k + 1]), sc2, nm2);
+              const float2 a = ptx::ffma2(make_float2(v[c * 32 + u * 8 + k], v[c * 32 + u * 8 + k + 1]), sc2, nm2);
               e[k] = ptx::ex2(a.x);
               e[k + 1] = ptx::ex2(a.y);
-              ls2[k >> 1] = fadd2(ls2[k >> 1], make_float2(e[k], e[k + 1]));
+              ls2[k >> 1] = ptx::fadd2(ls2[k >> 1], make_float2(e[k], e[k + 1]));
             }
             pk[4 * u + 0] = pack_bf16x2(e[0], e[1]);
             pk[4 * u + 1] = pack_bf16x2(e[2], e[3]);
