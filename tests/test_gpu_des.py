@@ -71,19 +71,26 @@ def test_des_predicts_streamed_ttft(T):
 
     st0, _ = run(T.DEBUG_SERIAL)                      # serial rho = 0: the copy rate alone
     b_pcie = (st0["bytes_streamed"] + st0["bytes_adapter"]) / ((st0["h2d_last_ms"] - st0["h2d_first_ms"]) / 1e3)
-    tpl.resize(T.template_opts(resident_bytes=T.U64_MAX))
-    for _ in range(2):
-        run(T.DEBUG_TIMELINE)
-    st1, _ = run(T.DEBUG_TIMELINE)
-    tl1 = tpl.timeline()
-    starts = tl1["op_start_ms"]
-    dur = np.diff(np.append(starts, tl1["end_ms"]))
-    warm_ms = st1["device_ms"]
+    def warm_durations():
+        tpl.resize(T.template_opts(resident_bytes=T.U64_MAX))
+        for _ in range(2):
+            run(T.DEBUG_TIMELINE)
+        st, _ = run(T.DEBUG_TIMELINE)
+        tl = tpl.timeline()
+        return np.diff(np.append(tl["op_start_ms"], tl["end_ms"])), st["device_ms"]
+
+    dur_a, warm_ms = warm_durations()
     tpl.resize(T.template_opts(eq1=True, t_ttft_s=warm_ms / 1e3, b_pcie_Bps=b_pcie))
     run(T.DEBUG_TIMELINE)
     st2, ad = run(T.DEBUG_TIMELINE)
     tl2 = tpl.timeline()
-    gbytes, barriers = _plan(tpl.plan_dump(ad))
+    gdump = tpl.plan_dump(ad)
+    # the op durations bracket the streamed run (warm before and after, averaged):
+    # the SM clock drifts under the power cap over the seconds the test takes,
+    # which is not what the overlap model is about
+    dur_b, warm_b = warm_durations()
+    dur = 0.5 * (dur_a + dur_b)
+    gbytes, barriers = _plan(gdump)
     assert len(gbytes) == len(tl2["group_end_ms"])
     measured = st2["device_ms"]
     # (a) measured landing times: a copy "duration" per group in FIFO order
@@ -103,7 +110,8 @@ def test_des_predicts_streamed_ttft(T):
     pred_b = t0 + sim_b["ttft"]
     rec = {"workload": "13B S=2048 r16 LoRA, Eq. 1 template", "rho": st2["bytes_resident"] /
            (st2["bytes_resident"] + st2["bytes_streamed"]),
-           "measured_ttft_ms": measured, "warm_rho1_ms": warm_ms, "b_pcie_GBps": b_pcie / 1e9,
+           "measured_ttft_ms": measured, "warm_rho1_ms": warm_ms, "warm_rho1_after_ms": warm_b,
+           "b_pcie_GBps": b_pcie / 1e9,
            "des_measured_copies_ms": pred_a, "des_bytes_over_bpcie_ms": pred_b,
            "last_group_landed_ms": float(ends.max()),
            "copy_rate_overlapped_GBps": (st2["bytes_streamed"] + st2["bytes_adapter"]) /
